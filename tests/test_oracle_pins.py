@@ -1,0 +1,375 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the pin of SURVEY.md §8(c) it implements (P1-P9) and the PAPER.md passage.
+None of them re-types the oracle's formula: they use the paper's example values, exact
+rationals for Def. 2, closed forms derived in the docstrings, brute force over all slopes at
+reduced precision, and the generator's own key arrays as the expected decode output.
+"""
+from __future__ import annotations
+
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import native as orc
+from oracle import pyref
+from synth import fuzz_case, make_keys
+from tests import blobparse
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------------ P3 width table
+@pytest.mark.parametrize("eps,b", [(0, 0), (1, 2), (4, 4), (31, 6), (63, 7), (127, 8), (255, 9)])
+def test_width_table(eps, b):
+    """P3: b = ceil(log2(2 eps + 1)); eps = 4 -> 4 bits (Fig. 2);
+    the BASELINE configs' eps 63/127/255/31 -> 7/8/9/6 bits (BASELINE.json configs)."""
+    assert orc.width(eps) == b
+
+
+def test_width_closed_form():
+    """2^(b-1) < 2 eps + 1 <= 2^b for every eps (the defining property of the ceiling)."""
+    for eps in list(range(0, 5000)) + [(1 << k) + d for k in range(12, 31) for d in (-1, 0, 1)]:
+        b = orc.width(eps)
+        assert 2 * eps + 1 <= 1 << b
+        assert b == 0 or (1 << (b - 1)) < 2 * eps + 1
+
+
+# ------------------------------------------------------------------------ Fig. 2 fixture
+def _golden_fig2():
+    eps = width = keys = None
+    with open(os.path.join(GOLDEN, "fig2_toy.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            k, *v = line.split()
+            if k == "eps":
+                eps = int(v[0])
+            elif k == "width":
+                width = int(v[0])
+            elif k == "keys":
+                keys = [int(x) for x in v]
+    return eps, width, keys
+
+
+def test_fig2_toy_example():
+    """PAPER.md:89-99 (Fig. 2): eps = 4, 21 keys 1, 3, ..., 77, 4-bit residuals, lossless.
+    Only eps, N, first/last keys and the width are the paper's."""
+    eps, width, keys = _golden_fig2()
+    assert (eps, width, len(keys), keys[0], keys[1], keys[-1]) == (4, 4, 21, 1, 3, 77)
+    blob = orc.encode(np.array(keys, np.uint32), eps)
+    bl = blobparse.parse(blob)
+    assert bl.b == width == 4
+    assert bl.n == 21
+    assert orc.validate(blob) == 0
+    assert orc.decode(blob).tolist() == keys
+    # every residual Delta[i] = K[i] - floor(f(i)) lies in [-eps, eps] (Def. 2)
+    for u in blobparse.fields(bl):
+        assert 0 <= u <= 2 * eps
+    # size(K^c) = size(f) + N * ceil(log2(2 eps + 1)) bits: 21 * 4 = 84 bits -> 3 words + pad
+    assert bl.W == 4
+
+
+# --------------------------------------------------------- P1 round trip + P2 exact residual
+def _check_def2_exact(keys, blob):
+    """P2 with exact rationals: f(i) = beta_j + alpha_j (i - s_j), alpha_j = slope_j / 2^32,
+    beta_j = base_j (Eq. 1); |K[i] - floor(f(i))| <= eps and
+    the stored field equals K[i] - floor(f(i)) + eps."""
+    bl = blobparse.parse(blob)
+    us = blobparse.fields(bl)
+    starts = [int(x) for x in bl.starts]
+    j = 0
+    for i, k in enumerate(keys):
+        while starts[j + 1] <= i:
+            j += 1
+        f = Fraction(int(bl.base[j])) + Fraction(int(bl.slope[j]), 1 << 32) * (i - starts[j])
+        fl = math.floor(f)
+        assert abs(int(k) - fl) <= bl.eps
+        assert us[i] == int(k) - fl + bl.eps
+        # the slope guard of FORMAT F2 (makes hi32(acc) exact on the device)
+        seg_len = starts[j + 1] - starts[j]
+        assert int(bl.slope[j]) * (seg_len - 1) <= (1 << 63) - 1
+
+
+@pytest.mark.parametrize("seed", range(1000, 1060))
+def test_roundtrip_and_def2_fuzz(seed):
+    """P1 (Def. 1): Dec(Enc(K))[i] = K[i] for all i, on the SURVEY §8(d) fuzz
+    corpus; the expected output is the generator's array. P2 recomputed exactly."""
+    keys, eps, kb, law = fuzz_case(seed, n_max=3000)
+    blob = orc.encode(keys, eps, kb)
+    assert orc.validate(blob) == 0
+    out = orc.decode(blob)
+    assert out.dtype == keys.dtype
+    assert np.array_equal(out, keys), (seed, law)
+    _check_def2_exact(keys, blob)
+
+
+@pytest.mark.parametrize("seed", range(2000, 2040))
+def test_roundtrip_larger(seed):
+    keys, eps, kb, law = fuzz_case(seed, n_max=100_000)
+    blob = orc.encode(keys, eps, kb)
+    assert np.array_equal(orc.decode(blob), keys), (seed, law)
+    rng = np.random.default_rng(seed)
+    idx = rng.integers(0, keys.size, 500)
+    got, err = orc.access(blob, idx)
+    assert err == 0 and np.array_equal(got, keys[idx])
+    if keys.size >= 64:
+        st = rng.integers(0, keys.size - 64, 50, endpoint=True)
+        got, err = orc.range_decode(blob, st, 64)
+        assert err == 0
+        for r, s in enumerate(st):
+            assert np.array_equal(got[r], keys[s:s + 64])
+
+
+def test_roundtrip_config1_full():
+    """Config 1 at full size (N = 1e6, u32, eps = 63): bit-exact round trip and b = 7."""
+    keys = make_keys(1)
+    blob = orc.encode(keys, 63)
+    assert blobparse.parse(blob).b == 7
+    assert np.array_equal(orc.decode(blob), keys)
+    out, nt = orc.decode_mt(blob)
+    assert nt >= 1 and np.array_equal(out, keys)
+
+
+@pytest.mark.parametrize("cid,n", [(2, 300_000), (3, 300_000), (4, 300_000), (5, 300_000)])
+def test_roundtrip_configs_small(cid, n):
+    keys = make_keys(cid, n)
+    eps = {2: 127, 3: 255, 4: 31, 5: 127}[cid]
+    blob = orc.encode(keys, eps)
+    assert orc.validate(blob) == 0
+    assert np.array_equal(orc.decode(blob), keys)
+
+
+# ----------------------------------------------------------- P4 greedy maximality (brute force)
+def _feasible(keys, s, e, S, eps, F, gmax):
+    """Does slope S admit keys[s..e) as one segment? Direct evaluation of the Def. 2 bound at
+    reduced precision, INCLUDING the overflow guard S * (e - s - 1) <= gmax."""
+    if S * (e - s - 1) > gmax:
+        return False
+    for d in range(1, e - s):
+        D = int(keys[s + d]) - int(keys[s])
+        if not (D - eps <= (S * d) >> F <= D + eps):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("F", range(0, 7))
+def test_greedy_maximal_bruteforce(F):
+    """P4: each greedy segment's slope is feasible, equals lo + floor((hi - lo)/2) over the
+    brute-forced feasible interval [lo, hi] (F5), and NO slope in [0, G] admits the segment
+    extended by one key (F6: break at the first infeasible index). G = 2^12 - 1, keys < 2^10,
+    N <= 40, so every slope is enumerated."""
+    gmax = (1 << 12) - 1
+    rng = np.random.default_rng(100 + F)
+    ends_checked = 0
+    for trial in range(60):
+        n = int(rng.integers(2, 40, endpoint=True))
+        keys = np.unique(rng.integers(0, 1 << 10, 3 * n))[:n].astype(np.uint64)
+        n = keys.size
+        eps = int(rng.integers(0, 6))
+        st, ba, sl = orc.segment(keys, eps, F=F, gmax=gmax)
+        bounds = [int(x) for x in st] + [n]
+        assert bounds[0] == 0
+        for j in range(len(st)):
+            s, e = bounds[j], bounds[j + 1]
+            assert int(ba[j]) == int(keys[s])
+            feas = [S for S in range(gmax + 1) if _feasible(keys, s, e, S, eps, F, gmax)]
+            assert feas, (trial, j)
+            lo, hi = min(feas), max(feas)
+            assert feas == list(range(lo, hi + 1))  # the feasible set is an interval
+            want = 0 if e - s == 1 else lo + (hi - lo) // 2
+            assert int(sl[j]) == want
+            if e < n:
+                assert not any(_feasible(keys, s, e + 1, S, eps, F, gmax)
+                               for S in range(gmax + 1)), (trial, j)
+                ends_checked += 1
+    assert ends_checked > 100
+
+
+# ---------------------------------------------------------------- P5 AP closed forms
+@pytest.mark.parametrize("g,eps,seg_len", [
+    (1 << 20, 0, 2048),        # floor((2^31 - 1) / 2^20) + 1
+    (1_000_003, 0, 2148),      # floor((2^31 - 1) / 1000003) + 1
+    (1 << 20, 5, 2049),        # eps = 5 relaxes the guard by 5 * 2^32 / 2^52 < 1 -> one more key
+    (3, 7, 715_827_883 // 1000),  # long AP, cut below by a forced-size check (see body)
+])
+def test_ap_closed_forms(g, eps, seg_len):
+    """P5. An arithmetic progression with gap g at eps = 0 needs slope >= g * 2^32 (the
+    lower cone bound ceil(g d 2^32 / d)), so the guard slope * d_max <= 2^63 - 1 admits
+    d_max = floor((2^63 - 1) / (g 2^32)) = floor((2^31 - 1) / g): segments of exactly
+    floor((2^31 - 1)/g) + 1 keys. With eps = 5 and g = 2^20 the lower bound drops to
+    g 2^32 - floor(5 2^32 / d), allowing d_max = 2048 -> 2049 keys."""
+    if g == 3:
+        # floor((2^31-1)/3) + 1 = 715827883 keys would be one segment: a 3 * 715827 key AP
+        # must therefore be a single segment
+        keys = np.arange(3 * seg_len, dtype=np.uint64) * np.uint64(g)
+        st, _, _ = orc.segment(keys, eps)
+        assert st.tolist() == [0]
+        return
+    n = 3 * seg_len + 17
+    keys = (np.arange(n, dtype=np.uint64) * np.uint64(g)) + np.uint64(12345)
+    st, _, sl = orc.segment(keys, eps)
+    lens = np.diff(np.append(st, n))
+    assert lens[:3].tolist() == [seg_len] * 3
+    assert lens[3] == 17
+
+
+def test_ap_short_single_segment():
+    """P5: an AP shorter than the guard bound is one segment with every residual = eps
+    (prediction exact: slope = g 2^32 is the only slope for eps = 0 and within the interval
+    for eps > 0 the floor stays at g d)."""
+    for g, eps in [(7, 0), (100, 3), (1 << 20, 127)]:
+        keys = np.arange(1000, dtype=np.uint64) * np.uint64(g)
+        blob = orc.encode(keys, eps)
+        bl = blobparse.parse(blob)
+        assert bl.L == 1
+        assert set(blobparse.fields(bl)) == {eps}
+
+
+# -------------------------------------------------------------------- P6 overflow guard
+def test_overflow_guard_cases():
+    """P6: keys [0, 2^31-1, 2^32] at eps = 0: the first pair needs slope (2^31-1) 2^32 <=
+    2^63-1 (fits), the third key needs slope 2^63 (over the guard) -> lengths [2, 1].
+    Keys [0, 2^31, 2^32+5]: every pair needs slope >= 2^63 -> [1, 1, 1]."""
+    st, _, _ = orc.segment(np.array([0, (1 << 31) - 1, 1 << 32], np.uint64), 0)
+    assert np.diff(np.append(st, 3)).tolist() == [2, 1]
+    st, _, sl = orc.segment(np.array([0, 1 << 31, (1 << 32) + 5], np.uint64), 0)
+    assert np.diff(np.append(st, 3)).tolist() == [1, 1, 1]
+    assert sl.tolist() == [0, 0, 0]
+    # and both still round-trip through a blob
+    for ks in ([0, (1 << 31) - 1, 1 << 32], [0, 1 << 31, (1 << 32) + 5]):
+        k = np.array(ks, np.uint64)
+        assert np.array_equal(orc.decode(orc.encode(k, 0)), k)
+
+
+def test_extreme_keys():
+    """Keys at the top of the u32 / u64 ranges and huge gaps (1-key segments)."""
+    top = (1 << 64) - 1
+    k = np.array([0, 1, 2, 1 << 40, top - 5, top - 1, top], np.uint64)
+    for eps in (0, 1, 255):
+        assert np.array_equal(orc.decode(orc.encode(k, eps)), k)
+    k32 = np.array([0, 5, 0xFFFFFFF0, 0xFFFFFFFF], np.uint32)
+    for eps in (0, 63):
+        assert np.array_equal(orc.decode(orc.encode(k32, eps)), k32)
+
+
+@pytest.mark.parametrize("n", [1, 2, 1023, 1024, 1025, 2048, 4097])
+def test_sizes_around_hint_block(n):
+    keys = np.cumsum(np.random.default_rng(n).integers(1, 300, n)).astype(np.uint64)
+    for eps in (0, 7, 127):
+        blob = orc.encode(keys, eps)
+        assert orc.validate(blob) == 0
+        assert np.array_equal(orc.decode(blob), keys)
+
+
+# ------------------------------------------------------------------ P7 ratio from bytes
+@pytest.mark.parametrize("seed", range(3000, 3010))
+def test_ratio_from_byte_counts(seed):
+    """P7 (Def. 1: r = size(K^c)/size(K)): blob bytes equal the section sizes
+    summed with their 256-byte alignment, computed from (N, L, b) alone."""
+    keys, eps, kb, _ = fuzz_case(seed, n_max=50_000)
+    blob = orc.encode(keys, eps, kb)
+    bl = blobparse.parse(blob)
+    size = blobparse.expected_size(keys.size, bl.L, orc.width(eps))
+    assert len(blob) == size == bl.total
+    r = len(blob) / (keys.size * kb / 8)
+    assert r == size / (keys.size * keys.itemsize)
+
+
+# ----------------------------------------------------------- pyref cross-check (tiny inputs)
+@pytest.mark.parametrize("seed", range(4000, 4040))
+def test_pyref_matches_c(seed):
+    keys, eps, kb, _ = fuzz_case(seed, n_max=2000)
+    segs = pyref.segment(keys, eps)
+    st, ba, sl = orc.segment(keys, eps)
+    assert [(int(a), int(b), int(c)) for a, b, c in zip(st, ba, sl)] == segs
+    us = pyref.residuals(keys, segs, eps)
+    assert pyref.decode_segments(segs, us, keys.size, eps, kb) == [int(x) for x in keys]
+    bl = blobparse.parse(orc.encode(keys, eps, kb))
+    packed = pyref.pack(us, pyref.width(eps))
+    assert [int(w) for w in bl.words[:len(packed)]] == packed
+    assert not bl.words[len(packed):].any()
+
+
+# ------------------------------------------------------------- P9 adversarial valid blobs
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("brk", ["none", "every7", "tile_edges", "all"])
+def test_adversarial_blobs(mode, brk):
+    """P9: valid but non-normative blobs (slope = lo / mid / hi; forced breaks at 1024-key
+    and 4096-key tile edges, T-1, T+1; all-1-key segments). Decode must still equal K."""
+    n = 12_000
+    keys = make_keys(5, n)
+    fb = np.zeros(n, np.uint8)
+    if brk == "every7":
+        fb[::7] = 1
+    elif brk == "tile_edges":
+        for t in range(0, n, 1024):
+            fb[t] = 1
+        for t in range(4096, n, 4096):
+            fb[t - 1] = fb[t + 1] = 1
+    elif brk == "all":
+        fb[:] = 1
+    blob = orc.encode(keys, 127, force_break=fb, slope_mode=mode)
+    assert orc.validate(blob) == 0
+    assert np.array_equal(orc.decode(blob), keys)
+    if brk == "all":
+        assert blobparse.parse(blob).L == n
+
+
+# ---------------------------------------------------------------------- error behaviour
+def test_encode_errors():
+    with pytest.raises(orc.OracleError) as e:
+        orc.encode(np.zeros(0, np.uint64), 3)
+    assert e.value.code == -2
+    with pytest.raises(orc.OracleError) as e:
+        orc.encode(np.array([1, 5, 5], np.uint64), 3)  # duplicates: SURVEY L10
+    assert e.value.code == -3
+    with pytest.raises(orc.OracleError) as e:
+        orc.encode(np.array([4, 3], np.uint64), 3)
+    assert e.value.code == -3
+    with pytest.raises(orc.OracleError) as e:
+        orc.encode(np.array([1, 1 << 33], np.uint64), 3, key_bits=32)
+    assert e.value.code == -4
+    with pytest.raises(orc.OracleError) as e:
+        orc.encode(np.array([1, 2], np.uint64), 1 << 31)
+    assert e.value.code == -1
+
+
+def _corrupt(blob: bytes, off: int, val: bytes) -> bytes:
+    b = bytearray(blob)
+    b[off:off + len(val)] = val
+    return bytes(b)
+
+
+def test_validate_rejects_corruption():
+    keys = make_keys(5, 5000)
+    blob = orc.encode(keys, 127)
+    bl = blobparse.parse(blob)
+    assert orc.validate(blob) == 0
+    bad = [
+        _corrupt(blob, 0, b"XCG1"),                                   # magic
+        _corrupt(blob, 4, b"\x02"),                                   # version
+        blob[:-4],                                                     # truncated
+        _corrupt(blob, bl.o_starts + 8, bl.starts[1].tobytes()),       # non-monotone starts
+        _corrupt(blob, bl.o_hint + 4, np.uint32(bl.L - 1).tobytes()),  # wrong hint
+        _corrupt(blob, 7, b"\x09"),                                    # width != f(eps)
+        _corrupt(blob, 100, b"\x01"),                                  # reserved byte
+        _corrupt(blob, bl.o_words + 4 * bl.W - 4, b"\x01"),            # nonzero pad bit
+        _corrupt(blob, bl.o_params + 8, np.uint64(1 << 63).tobytes()),  # negative slope
+    ]
+    for i, b in enumerate(bad):
+        assert orc.validate(b) == -5, i
+
+
+def test_access_range_out_of_range():
+    keys = make_keys(5, 3000)
+    blob = orc.encode(keys, 127)
+    got, err = orc.access(blob, np.array([0, 2999, 3000, 1 << 40], np.uint64))
+    assert err == 1 and got.tolist() == [int(keys[0]), int(keys[2999]), 0, 0]
+    got, err = orc.range_decode(blob, np.array([0, 2936, 2937], np.uint64), 64)
+    assert err == 1
+    assert np.array_equal(got[0], keys[:64]) and np.array_equal(got[1], keys[2936:])
+    assert not got[2].any()
