@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py -- full-decode throughput of the learned-compression decoder on B200.
+
+One step = one lc_decode launch over the whole BASELINE config-2 list (N = 1e8 u64 keys,
+geometric gaps mean 100, eps = 127): read the compressed blob once, write N keys once.
+Metric (BASELINE.json): full-decode GB/s = (compressed bytes + N * 8) / t, plus keys/s and the
+fraction of the measured HBM copy peak; random-access lookups/s and range decodes on config 5.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config 1..5]
+
+Under torchrun (N > 1) every rank decodes its own replica of the workload (weak scaling, no
+collective: the decode shards with no exchange step); the time is the
+max over ranks of the device-timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full-decode GB/s (+keys/s) and % of HBM peak; random-access lookups/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def _ncu_traffic(cid):
+    """dram bytes per launch of the decode kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"config{cid}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampler of SM clock + throttle reasons while the timed region runs."""
+
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+        0x1: "gpu_idle",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _spec(cid):
+    from synth import CONFIGS
+    s = CONFIGS[cid]
+    return s
+
+
+def _workload_name(cid):
+    s = _spec(cid)
+    return f"config{cid}: N={s.n:.0e} u{s.key_bits} keys, {s.desc}, eps={s.eps}"
+
+
+def _env_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle (plain C, OpenMP over 65536-key spans) timed on the host cores: the same
+    metric, config and units as the GPU arm.  Rank 0 only."""
+    ws, rank, _ = _env_dist()
+    if rank != 0:
+        return
+    from oracle import native as orc
+    from synth import make_keys
+    cid = args.config
+    spec = _spec(cid)
+    keys = make_keys(cid)
+    blob = orc.encode(keys, spec.eps)  # oracle's own encoder
+    n = keys.size
+    w = spec.key_bits // 8
+    out = np.empty(n, keys.dtype)
+    # bound each step: decode a prefix of the list sized so the whole run stays ~<= 2 min
+    t0 = time.perf_counter()
+    _, nt = orc.decode_mt(blob, out)
+    t_full = time.perf_counter() - t0
+    total_steps = args.steps + args.warmup
+    frac = min(1.0, 120.0 / max(total_steps * t_full, 1e-9))
+    m = n if frac >= 1.0 else max(65536, int(n * frac) // 1024 * 1024)
+    sample_bytes = (len(blob) * m / n) + m * w
+    span_out = np.empty(m, keys.dtype)
+
+    def step():
+        if m == n:
+            orc.decode_mt(blob, out)
+        else:
+            # prefix decode, all threads, same code path (oracle_decode_span per 65536 keys)
+            import concurrent.futures as cf
+            spans = [(a, min(a + 65536, m)) for a in range(0, m, 65536)]
+            with cf.ThreadPoolExecutor(nt) as ex:
+                for a, b_ in spans:
+                    ex.submit(lambda a=a, b_=b_: span_out.__setitem__(
+                        slice(a, b_), orc.decode_span(blob, a, b_)))
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    if m == n:
+        assert np.array_equal(out, keys)
+    t = sum(ts) / len(ts)
+    value = sample_bytes / t / 1e9
+    sample = (f"oracle_decode_mt over {'the whole list' if m == n else f'the first {m} keys'} "
+              f"of {_workload_name(cid)}, per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": _workload_name(cid), "n": n, "eps": spec.eps,
+                   "blob_bytes": len(blob), "sample_keys": m},
+        "keys_per_s": m / t,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nt, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------- GPU arm
+def _cpu_baseline(blob, keys, reps=3):
+    from oracle import native as orc
+    out = np.empty_like(keys)
+    ts, nt = [], 1
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, nt = orc.decode_mt(blob, out)
+        ts.append(time.perf_counter() - t0)
+    assert np.array_equal(out, keys)
+    t = statistics.median(ts)
+    return t, nt
+
+
+def _time_launches(fn, stream, steps, warmup):
+    """W untimed + K timed launches of fn on `stream`; per-launch CUDA events. Returns
+    (total seconds of the timed region, per-launch seconds list)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(stream)
+    for k in range(steps):
+        fn()
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [evs[k].elapsed_time(evs[k + 1]) / 1e3 for k in range(steps)]
+    return evs[0].elapsed_time(evs[-1]) / 1e3, per
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_10770_b200 import lc
+    from synth import make_keys, make_queries
+
+    ws, rank, local = _env_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(dev)
+    cid = args.config
+    spec = _spec(cid)
+
+    # ---- inputs (host generation + host encode: not timed)
+    keys = make_keys(cid)
+    n = keys.size
+    w = spec.key_bits // 8
+    blob = lc.encode(keys, spec.eps)
+    h = lc.header(blob)
+    view = lc.View(blob, device=dev)
+    out = view.out_tensor(n)
+    alg_bytes = len(blob) + n * w  # compressed read once + keys written once
+
+    def step():
+        lc.decode(view, out, stream=stream)
+
+    peak, peak_src = _peaks()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    c0 = lc.launch_count()
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+        total, per = _time_launches(step, stream, args.steps, args.warmup)
+    launches = lc.launch_count() - c0 - args.warmup
+    if ws > 1:
+        dist.barrier()
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    # correctness of what was timed: every key, on device, against the generator's array
+    ref = torch.from_numpy(keys.view(np.int64) if w == 8 else keys.view(np.int32)).to(dev)
+    ok = torch.equal(out, ref)
+    del ref
+    if not ok:
+        raise SystemExit(f"rank {rank}: decoded keys differ from the input keys")
+
+    ms = t_max / args.steps * 1e3
+    value = ws * alg_bytes * args.steps / t_max / 1e9
+    kern = statistics.mean(per)
+    achieved = alg_bytes / kern / 1e9
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
+    d_blob = torch.empty(len(blob), dtype=torch.uint8, device=dev)
+    h_out = torch.empty(n, dtype=out.dtype).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        lc.decode_host(h_blob, d_blob, out, h_out, stream=stream)
+
+    e2e_total, _ = _time_launches(e2e_step, stream, e2e_steps, 1)
+    if not np.array_equal(h_out.numpy().view(keys.dtype), keys):
+        raise SystemExit("e2e decode mismatch")
+    e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = ws * alg_bytes * e2e_steps / float(e2e_t.item()) / 1e9
+    del h_blob, d_blob, h_out
+
+    # ---- random access + range decodes (config 5), reported beside the headline
+    access = None
+    if not args.no_access:
+        k5, idx, rs = make_queries()
+        b5 = lc.encode(k5, 127)
+        v5 = lc.View(b5, device=dev)
+        d_idx = torch.from_numpy(idx.view(np.int64)).to(dev)
+        a_out = torch.empty(idx.size, dtype=torch.int64, device=dev)
+        d_rs = torch.from_numpy(rs.view(np.int64)).to(dev)
+        r_out = torch.empty(rs.size * 64, dtype=torch.int64, device=dev)
+        with torch.cuda.stream(stream):
+            ta, pa = _time_launches(lambda: lc.access(v5, d_idx, a_out, stream=stream), stream,
+                                    max(3, min(args.steps, 20)), 2)
+            tr, pr = _time_launches(lambda: lc.range_decode(v5, d_rs, 64, r_out, stream=stream),
+                                    stream, max(3, min(args.steps, 20)), 2)
+        d5 = torch.from_numpy(k5.view(np.int64)).to(dev)
+        ok_a = torch.equal(a_out, d5[d_idx])
+        sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
+        ok_r = torch.equal(r_out, d5[sel])
+        del d5, sel
+        access = {
+            "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
+                        "lookups; 1e7 ranges x 64 keys",
+            "lookups_per_s": ws * idx.size / statistics.mean(pa),
+            "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
+            "ranges_per_s": ws * rs.size / statistics.mean(pr),
+            "range_keys_per_s": ws * rs.size * 64 / statistics.mean(pr),
+            "range_out_GBps": rs.size * 64 * 8 / statistics.mean(pr) / 1e9,
+            "bit_exact": bool(ok_a and ok_r),
+            "blob_bytes": len(b5),
+        }
+        if not (ok_a and ok_r):
+            raise SystemExit("access/range mismatch")
+        del v5, d_idx, a_out, d_rs, r_out
+
+    if ws > 1:
+        dist.barrier()
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    t_cpu, cores = _cpu_baseline(blob, keys) if ws == 1 and not args.no_cpu else (None, None)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64" if w == 8 else "u32", "data": "synthetic",
+        "config": {"workload": _workload_name(cid), "n": n, "key_bits": spec.key_bits,
+                   "eps": spec.eps, "res_bits": int(h.res_bits), "segments": int(h.n_seg),
+                   "blob_bytes": len(blob), "bits_per_int": 8 * len(blob) / n,
+                   "ratio_r": len(blob) / (n * w), "bytes_per_step": alg_bytes,
+                   "l2": "no flush: every step reads+writes %.2f GB >> 126 MB L2" % (alg_bytes / 1e9),
+                   "parallelism": f"replica x{ws} (weak)"},
+        "keys_per_s": ws * n * args.steps / t_max,
+        "hbm_frac": value / ws / peak,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _ncu_traffic(cid),
+                     "kernel": "lc_decode_kernel<true>", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": len(blob),
+                "d2h_bytes_per_step": n * w, "api": "lc_decode_host (pinned host blob -> "
+                "device -> decode -> pinned host keys)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "access": access,
+    }
+    if t_cpu is not None:
+        line["cpu_baseline"] = {
+            "value": alg_bytes / t_cpu / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle_decode_mt of the full {_workload_name(cid)} (median of 3)",
+            "keys_per_s": n / t_cpu}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--no-access", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

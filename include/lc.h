@@ -1,0 +1,135 @@
+/*
+ * lc.h -- C ABI of the B200-native learned-compression decoder (arxiv 2412.10770).
+ *
+ * The method (Def. 2 / Eq. 1, §II-A): a sorted key list K is stored as an
+ * eps-PLA f (segments (s_j, alpha_j, beta_j)) plus residuals Delta[i] = K[i] - floor(f(i)) in
+ * ceil(log2(2 eps + 1)) bits; decompression is K[i] = floor(f(i)) + Delta[i] (
+ * Fig. 2 decoding stage).  The byte format "LCG1" is frozen in FORMAT.md.
+ *
+ * Conventions for every entry point
+ *  - Return value: int32_t status, LC_OK (0) or a negative LC_ERR_* code; never aborts.
+ *  - Pointers prefixed d_ are DEVICE pointers owned by the caller (e.g. torch CUDA tensors);
+ *    the library never allocates, frees or synchronizes device memory in the device calls.
+ *  - Device calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *    Host-detectable argument problems are returned immediately; per-query index problems
+ *    are reported on the device through *d_err (see lc_access).
+ *  - The library is stateless: any number of concurrent calls on distinct streams may read
+ *    the same blob.
+ */
+#ifndef LC_H_
+#define LC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (names follow SPEC.md:113,164,174,184,465 error kinds). */
+enum {
+    LC_OK = 0,
+    LC_ERR_ARG = -1,       /* null/misaligned pointer, bad size, eps > 2^31-1, key_bits != 32|64 */
+    LC_ERR_EMPTY = -2,     /* n == 0 (EmptyInput) */
+    LC_ERR_UNSORTED = -3,  /* keys not strictly increasing, duplicates included (UnsortedInput) */
+    LC_ERR_TOO_LARGE = -4, /* n >= 2^32, or a key >= 2^32 with key_bits == 32 */
+    LC_ERR_FORMAT = -5,    /* bad magic/version/offsets, truncated or non-monotone blob */
+    LC_ERR_ALLOC = -6,     /* host allocation failed */
+    LC_ERR_CUDA = -7       /* a CUDA launch or copy failed (cudaGetLastError) */
+};
+
+/* FORMAT F1: the first 128 bytes of every blob, little-endian. */
+typedef struct lc_header {
+    char magic[4];        /* "LCG1" */
+    uint16_t version;     /* 1 */
+    uint8_t key_bits;     /* 32 | 64 */
+    uint8_t res_bits;     /* b = ceil(log2(2 eps + 1)) */
+    uint32_t eps;         /* error bound of the eps-PLA */
+    uint32_t hint_log2;   /* 10: one segment hint every 1024 keys */
+    uint64_t n;           /* N keys */
+    uint64_t n_seg;       /* L segments */
+    uint64_t n_hint;      /* H + 1, H = ceil(N / 1024) */
+    uint64_t n_words;     /* W residual words */
+    uint64_t off_starts, off_params, off_hint, off_words, total_bytes;
+    uint8_t reserved[40];
+} lc_header;
+
+/* A blob resident in device memory: a host copy of its header plus the device pointer.
+ * d_blob must be 256-byte aligned (torch / cudaMalloc allocations are). */
+typedef struct lc_view {
+    lc_header h;
+    const void* d_blob;
+} lc_view;
+
+/* A CUDA stream (binary-compatible with cudaStream_t / CUstream). */
+typedef struct CUstream_st* lc_stream;
+
+/* ----------------------------------------------------------------------------- host side */
+
+/* Build an LCG1 blob from n sorted keys (FORMAT F4 greedy anchored cone, the eps-PLA of Def. 2
+ * PAPER.md:171-181; residual packing PAPER.md:184-186).  NOT on the hot path.
+ *   keys:      host array of n keys, uint32_t if key_bits == 32 else uint64_t
+ *   eps:       error bound, 0 <= eps <= 2^31 - 1
+ *   *blob:     receives a host buffer of *blob_bytes bytes owned by the caller; release it
+ *              with lc_free.
+ * Errors: LC_ERR_EMPTY (n == 0), LC_ERR_UNSORTED, LC_ERR_TOO_LARGE, LC_ERR_ARG, LC_ERR_ALLOC. */
+int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps, void** blob,
+                  uint64_t* blob_bytes);
+
+/* Release a blob returned by lc_encode (NULL is a no-op). */
+void lc_free(void* blob);
+
+/* Full validation of a HOST copy of a blob (header, offsets, monotone starts, slope guard,
+ * hint array, residual range, zero padding).  LC_OK or LC_ERR_FORMAT / LC_ERR_ARG. */
+int32_t lc_validate(const void* blob, uint64_t blob_bytes);
+
+/* Fill *v from the blob's 128-byte header (a host copy) and the device pointer of the same blob
+ * (blob_bytes bytes).  Checks the header fields only (LC_ERR_FORMAT) and d_blob alignment
+ * (LC_ERR_ARG). */
+int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
+                     uint64_t blob_bytes);
+
+/* ---------------------------------------------------------------------------- device side */
+
+/* Full decompression Dec(K^c) (Def. 1): d_out[i] = K[i] for i in [0, n), each
+ * key_bits/8 bytes (d_out 16-byte aligned).  One kernel launch, asynchronous on stream. */
+int32_t lc_decode(const lc_view* v, void* d_out, lc_stream stream);
+
+/* Decode the key span [i0, i1) into d_out[0 .. i1-i0): the shard of a multi-GPU decode
+ * (SURVEY §8(e)).  i0 must be a multiple of 1024; i1 <= n.  LC_ERR_ARG otherwise. */
+int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out,
+                       lc_stream stream);
+
+/* Batched random access Dec(K^c)[i] ("f(j) + Delta[j]"; Table I caption
+ * PAPER.md:309, binary search for the segment).  d_idx: q uint64 indices (device);
+ * d_out: q keys of key_bits/8 bytes.  An index >= n yields 0 in its slot and sets bit 0 of
+ * *d_err (atomicOr) when d_err is not NULL.  q == 0 is a no-op. */
+int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_out,
+                  uint32_t* d_err, lc_stream stream);
+
+/* Range decode: d_out[r*len + k] = K[d_start[r] + k] for r < q, k < len (BASELINE config 5:
+ * 10^7 ranges of 64 keys).  A range with start + len > n yields zeros and sets bit 0 of
+ * *d_err.  1 <= len <= 2^20; q == 0 is a no-op. */
+int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
+                        void* d_out, uint32_t* d_err, lc_stream stream);
+
+/* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
+ * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
+ * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out
+ * (>= n*key_bits/8 bytes) and copies the keys to h_out.  Work is split into spans so that
+ * the device->host copy of one span overlaps the decode of the next.  Asynchronous: the
+ * caller synchronizes the stream before reading h_out. */
+int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, void* d_out,
+                       void* h_out, lc_stream stream);
+
+/* Human-readable name of a status code (static string). */
+const char* lc_status_str(int32_t status);
+
+/* Number of device kernels the previous calls on this thread have launched (monotone
+ * counter; used by bench.py to report gpu_launches). */
+uint64_t lc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LC_H_ */

@@ -1,0 +1,209 @@
+"""Thin ctypes binding of the C ABI in include/lc.h (argument marshalling only).
+
+Every step of the decode path runs inside liblc.so (host encoder in C++, decode / access /
+range kernels in CUDA for sm_100a).  PyTorch is used only for device memory and streams.
+There is no fallback: if liblc.so is missing this module raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; "
+                      "g.build()'` (nvcc, sm_100a)")
+
+_lib = C.CDLL(LIB_PATH)
+
+LC_OK, LC_ERR_ARG, LC_ERR_EMPTY, LC_ERR_UNSORTED = 0, -1, -2, -3
+LC_ERR_TOO_LARGE, LC_ERR_FORMAT, LC_ERR_ALLOC, LC_ERR_CUDA = -4, -5, -6, -7
+
+
+class lc_header(C.Structure):
+    _fields_ = [
+        ("magic", C.c_char * 4), ("version", C.c_uint16), ("key_bits", C.c_uint8),
+        ("res_bits", C.c_uint8), ("eps", C.c_uint32), ("hint_log2", C.c_uint32),
+        ("n", C.c_uint64), ("n_seg", C.c_uint64), ("n_hint", C.c_uint64), ("n_words", C.c_uint64),
+        ("off_starts", C.c_uint64), ("off_params", C.c_uint64), ("off_hint", C.c_uint64),
+        ("off_words", C.c_uint64), ("total_bytes", C.c_uint64), ("reserved", C.c_uint8 * 40),
+    ]
+
+
+assert C.sizeof(lc_header) == 128
+
+
+class lc_view(C.Structure):
+    _fields_ = [("h", lc_header), ("d_blob", C.c_void_p)]
+
+
+_p, _u64, _u32, _i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32
+_sig = {
+    "lc_encode": ([_p, _u64, _u32, _u32, C.POINTER(_p), C.POINTER(_u64)], _i32),
+    "lc_free": ([_p], None),
+    "lc_validate": ([_p, _u64], _i32),
+    "lc_view_init": ([C.POINTER(lc_view), _p, _p, _u64], _i32),
+    "lc_decode": ([C.POINTER(lc_view), _p, _p], _i32),
+    "lc_decode_span": ([C.POINTER(lc_view), _u64, _u64, _p, _p], _i32),
+    "lc_access": ([C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
+    "lc_range_decode": ([C.POINTER(lc_view), _p, _u64, _u32, _p, _p, _p], _i32),
+    "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
+    "lc_status_str": ([_i32], C.c_char_p),
+    "lc_launch_count": ([], _u64),
+}
+for _name, (_args, _res) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTS = tuple(_sig)
+
+
+class LcError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {_lib.lc_status_str(code).decode()} ({code})")
+        self.code = code
+
+
+def _check(code: int, what: str) -> None:
+    if code != LC_OK:
+        raise LcError(code, what)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def launch_count() -> int:
+    """Kernels launched by liblc.so so far (process-wide counter)."""
+    return int(_lib.lc_launch_count())
+
+
+# ---------------------------------------------------------------------------- host side
+def encode(keys: np.ndarray, eps: int, key_bits: int | None = None) -> bytes:
+    """lc_encode: host blob (FORMAT F1-F6) of sorted keys (uint32 or uint64 numpy array)."""
+    k = np.asarray(keys)
+    if key_bits is None:
+        key_bits = 32 if k.dtype == np.uint32 else 64
+    if key_bits == 32 and k.dtype != np.uint32:
+        if k.size and int(k.max()) > 0xFFFFFFFF:
+            raise LcError(LC_ERR_TOO_LARGE, "lc_encode")
+    k = np.ascontiguousarray(k, dtype=np.uint32 if key_bits == 32 else np.uint64)
+    out, nb = C.c_void_p(), C.c_uint64()
+    _check(_lib.lc_encode(k.ctypes.data if k.size else None, k.size, key_bits, eps,
+                          C.byref(out), C.byref(nb)), "lc_encode")
+    try:
+        return C.string_at(out.value, nb.value)
+    finally:
+        _lib.lc_free(out)
+
+
+def _host_ptr(blob) -> tuple[int, int, object]:
+    if isinstance(blob, (bytes, bytearray)):
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob) if isinstance(blob, bytes) else \
+            (C.c_char * len(blob)).from_buffer(blob)
+        return C.addressof(buf), len(blob), buf
+    if isinstance(blob, np.ndarray):
+        return blob.ctypes.data, blob.nbytes, blob
+    # torch CPU tensor
+    return blob.data_ptr(), blob.numel() * blob.element_size(), blob
+
+
+def validate(blob) -> int:
+    """lc_validate: 0 (LC_OK) or a negative status."""
+    p, n, _keep = _host_ptr(blob)
+    return int(_lib.lc_validate(p, n))
+
+
+def header(blob) -> lc_header:
+    p, n, _keep = _host_ptr(blob)
+    if n < 128:
+        raise LcError(LC_ERR_FORMAT, "header")
+    return lc_header.from_buffer_copy(C.string_at(p, 128))
+
+
+# -------------------------------------------------------------------------- device side
+class View:
+    """A blob resident on the GPU: lc_view (host header + device pointer) plus the tensor."""
+
+    def __init__(self, blob, device="cuda", d_blob=None):
+        import torch
+        raw = bytes(blob) if not isinstance(blob, (bytes, np.ndarray)) else blob
+        host = np.frombuffer(raw, np.uint8) if isinstance(raw, bytes) else raw.view(np.uint8)
+        if d_blob is None:
+            d_blob = torch.from_numpy(host.copy()).to(device)
+        self.d_blob = d_blob
+        self.v = lc_view()
+        _check(_lib.lc_view_init(C.byref(self.v), host.ctypes.data, d_blob.data_ptr(),
+                                 host.nbytes), "lc_view_init")
+
+    @property
+    def n(self) -> int:
+        return int(self.v.h.n)
+
+    @property
+    def key_bits(self) -> int:
+        return int(self.v.h.key_bits)
+
+    @property
+    def torch_dtype(self):
+        import torch
+        return torch.int64 if self.key_bits == 64 else torch.int32
+
+    def out_tensor(self, count: int):
+        import torch
+        return torch.empty(count, dtype=self.torch_dtype, device=self.d_blob.device)
+
+
+def decode(view: View, out=None, stream=None):
+    """lc_decode: all N keys into a device tensor (int64/int32 storage of u64/u32 keys)."""
+    if out is None:
+        out = view.out_tensor(view.n)
+    _check(_lib.lc_decode(C.byref(view.v), out.data_ptr(), _stream(stream)), "lc_decode")
+    return out
+
+
+def decode_span(view: View, i0: int, i1: int, out=None, stream=None):
+    if out is None:
+        out = view.out_tensor(max(i1 - i0, 0))
+    _check(_lib.lc_decode_span(C.byref(view.v), i0, i1, out.data_ptr() if out.numel() else None,
+                               _stream(stream)), "lc_decode_span")
+    return out
+
+
+def access(view: View, idx, out=None, err=None, stream=None):
+    """lc_access: Dec(K^c)[idx] for a device int64 tensor of indices."""
+    q = idx.numel()
+    if out is None:
+        out = view.out_tensor(q)
+    _check(_lib.lc_access(C.byref(view.v), idx.data_ptr() if q else None, q,
+                          out.data_ptr() if q else None,
+                          err.data_ptr() if err is not None else None, _stream(stream)),
+           "lc_access")
+    return out
+
+
+def range_decode(view: View, starts, length: int, out=None, err=None, stream=None):
+    """lc_range_decode: out[r, k] = K[starts[r] + k]."""
+    q = starts.numel()
+    if out is None:
+        out = view.out_tensor(q * length)
+    _check(_lib.lc_range_decode(C.byref(view.v), starts.data_ptr() if q else None, q, length,
+                                out.data_ptr() if q else None,
+                                err.data_ptr() if err is not None else None, _stream(stream)),
+           "lc_range_decode")
+    return out.view(q, length)
+
+
+def decode_host(h_blob, d_blob, d_out, h_out, stream=None) -> None:
+    """lc_decode_host: pinned host blob -> device -> decode -> pinned host keys (async)."""
+    _check(_lib.lc_decode_host(h_blob.data_ptr(), h_blob.numel(), d_blob.data_ptr(),
+                               d_out.data_ptr(), h_out.data_ptr(), _stream(stream)),
+           "lc_decode_host")

@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the CPU oracle and the
+generators' own key arrays (bit-exact; integer path, zero tolerance).
+
+Expected values never come from the CUDA path: they are the synthetic key arrays themselves
+(Def. 1: Dec(K^c) = K) and the oracle's decode / access / range of the same blob.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import native as orc  # noqa: E402
+from synth import CONFIGS, fuzz_case, make_keys, make_queries  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lc():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    from paper_2412_10770_b200 import lc as m
+    return m
+
+
+DEV = "cuda:0"
+
+
+def _dev(a: np.ndarray):
+    a = np.ascontiguousarray(a)
+    v = a.view(np.int64) if a.dtype.itemsize == 8 else a.view(np.int32)
+    return torch.from_numpy(v).to(DEV)
+
+
+def _host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+def _decode_equal(lc, blob, keys):
+    view = lc.View(blob, device=DEV)
+    out = lc.decode(view)
+    torch.cuda.synchronize()
+    return torch.equal(out, _dev(keys))
+
+
+# ------------------------------------------------------------------------- full decode
+@pytest.mark.parametrize("seed", range(1000, 1300))
+def test_decode_fuzz(lc, seed):
+    keys, eps, kb, law = fuzz_case(seed, n_max=100_000)
+    blob = lc.encode(keys, eps, kb)
+    assert _decode_equal(lc, blob, keys), (seed, law, keys.size, eps)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [2, 1023, 1024, 1025, 33_000, 262_145])
+def test_decode_configs_small(lc, cid, n):
+    keys = make_keys(cid, n)
+    eps = CONFIGS[cid].eps
+    blob = lc.encode(keys, eps)
+    view = lc.View(blob, device=DEV)
+    out = lc.decode(view)
+    torch.cuda.synchronize()
+    want = orc.decode(blob)
+    assert np.array_equal(want, keys)
+    assert np.array_equal(_host(out, keys.dtype), want)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("brk", ["every3", "tile_edges", "all", "dense_runs"])
+def test_decode_adversarial_blobs(lc, mode, brk):
+    """P9: valid non-normative blobs from the oracle's test-only builder (lo/mid/hi slopes,
+    forced breaks at 1024-key edges, T-1, T+1, all-1-key segments over whole chunks — the
+    worst case for the staged segment pages)."""
+    n = 40_000
+    keys = make_keys(5, n)
+    fb = np.zeros(n, np.uint8)
+    if brk == "every3":
+        fb[::3] = 1
+    elif brk == "tile_edges":
+        fb[::1024] = 1
+        for t in range(4096, n - 1, 4096):
+            fb[t - 1] = fb[t + 1] = 1
+    elif brk == "all":
+        fb[:] = 1
+    else:  # alternating dense and sparse chunks
+        for c in range(0, n, 2048):
+            fb[c:c + 1024] = 1
+    blob = orc.encode(keys, 127, force_break=fb, slope_mode=mode)
+    assert orc.validate(blob) == 0
+    assert _decode_equal(lc, blob, keys)
+
+
+@pytest.mark.parametrize("eps", [0, 1, 2, 3, 7, 100, 4095, 65535, (1 << 31) - 1])
+def test_decode_eps_extremes(lc, eps):
+    """b from 0 (no residual words read) up to 32 bits (eps = 2^31 - 1)."""
+    rng = np.random.default_rng(eps)
+    keys = np.cumsum(rng.integers(1, 1 << 20, 50_000)).astype(np.uint64)
+    blob = lc.encode(keys, eps)
+    assert _decode_equal(lc, blob, keys)
+
+
+def test_decode_top_of_range(lc):
+    for kb, top in ((32, (1 << 32) - 1), (64, (1 << 64) - 1)):
+        n = 5000
+        gaps = np.random.default_rng(kb).integers(1, 1000, n - 1).astype(np.uint64)
+        span = int(gaps.sum())
+        keys = np.empty(n, np.uint64)
+        keys[0] = top - span
+        keys[1:] = np.uint64(top - span) + np.cumsum(gaps, dtype=np.uint64)
+        keys = keys.astype(np.uint32) if kb == 32 else keys
+        for eps in (0, 63, 255):
+            assert _decode_equal(lc, lc.encode(keys, eps), keys)
+
+
+def test_decode_single_key(lc):
+    for dt in (np.uint32, np.uint64):
+        keys = np.array([123456], dt)
+        assert _decode_equal(lc, lc.encode(keys, 5), keys)
+
+
+def test_decode_span_shards(lc):
+    """Multi-GPU shard decode: spans at multiples of 1024 tile the output."""
+    keys = make_keys(2, 300_000)
+    blob = lc.encode(keys, 127)
+    view = lc.View(blob, device=DEV)
+    cuts = [0, 1024, 50 * 1024, 100 * 1024, 200 * 1024, 300_000]
+    parts = [lc.decode_span(view, a, b) for a, b in zip(cuts, cuts[1:])]
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts), _dev(keys))
+    with pytest.raises(lc.LcError):
+        lc.decode_span(view, 1000, 2000)
+    with pytest.raises(lc.LcError):
+        lc.decode_span(view, 0, 300_001)
+
+
+def test_decode_host_e2e(lc):
+    keys = make_keys(2, 1_000_003)
+    blob = lc.encode(keys, 127)
+    h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
+    d_blob = torch.empty(len(blob), dtype=torch.uint8, device=DEV)
+    d_out = torch.empty(keys.size, dtype=torch.int64, device=DEV)
+    h_out = torch.empty(keys.size, dtype=torch.int64).pin_memory()
+    lc.decode_host(h_blob, d_blob, d_out, h_out)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_out.numpy().view(np.uint64), keys)
+
+
+# -------------------------------------------------------------- access and range (config 5)
+def test_access_and_range_small(lc):
+    keys, idx, rs = make_queries(n=500_000, q=200_000, r=20_000)
+    blob = lc.encode(keys, 127)
+    view = lc.View(blob, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    got = lc.access(view, _dev(idx), err=err)
+    rg = lc.range_decode(view, _dev(rs), 64, err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert np.array_equal(_host(got, np.uint64), keys[idx.astype(np.int64)])
+    want_r, e = orc.range_decode(blob, rs, 64)
+    assert e == 0 and np.array_equal(_host(rg, np.uint64), want_r)
+
+
+@pytest.mark.parametrize("length", [1, 31, 32, 33, 64, 1000])
+def test_range_lengths(lc, length):
+    keys = make_keys(3, 100_000)
+    blob = lc.encode(keys, 255)
+    view = lc.View(blob, device=DEV)
+    rs = np.random.default_rng(length).integers(0, keys.size - length, 3000,
+                                                endpoint=True).astype(np.uint64)
+    rg = lc.range_decode(view, _dev(rs), length)
+    want, _ = orc.range_decode(blob, rs, length)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(rg, np.uint64), want)
+
+
+def test_access_range_errors(lc):
+    keys = make_keys(5, 5000)
+    blob = lc.encode(keys, 127)
+    view = lc.View(blob, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    idx = np.array([0, 4999, 5000, 1 << 40], np.uint64)
+    got = lc.access(view, _dev(idx), err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
+    assert _host(got, np.uint64).tolist() == [int(keys[0]), int(keys[4999]), 0, 0]
+    err.zero_()
+    rs = np.array([0, 4936, 4937], np.uint64)
+    rg = lc.range_decode(view, _dev(rs), 64, err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
+    h = _host(rg, np.uint64)
+    assert np.array_equal(h[0], keys[:64]) and np.array_equal(h[1], keys[4936:])
+    assert not h[2].any()
+    # q == 0 is a no-op
+    lc.access(view, torch.empty(0, dtype=torch.int64, device=DEV))
+
+
+def test_access_u32_keys(lc):
+    keys = make_keys(1, 300_000)
+    blob = lc.encode(keys, 63)
+    view = lc.View(blob, device=DEV)
+    idx = np.random.default_rng(1).integers(0, keys.size, 10_000).astype(np.uint64)
+    got = lc.access(view, _dev(idx))
+    rg = lc.range_decode(view, _dev(idx[:100] % np.uint64(keys.size - 64)), 64)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(got, np.uint32), keys[idx.astype(np.int64)])
+    want, _ = orc.range_decode(blob, idx[:100] % np.uint64(keys.size - 64), 64)
+    assert np.array_equal(_host(rg, np.uint32), want)
+
+
+# ------------------------------------------------------------- full-size configs (bench sizes)
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_full_config(lc, cid):
+    """Each BASELINE config at its full size, in the launch configuration bench.py times:
+    decode == the generator's keys (every element, on device); sampled indices == oracle
+    access computed one by one on the same blob."""
+    keys = make_keys(cid)
+    eps = CONFIGS[cid].eps
+    blob = lc.encode(keys, eps)
+    view = lc.View(blob, device=DEV)
+    out = lc.decode(view)
+    ref = _dev(keys)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    rng = np.random.default_rng(cid)
+    idx = np.unique(np.concatenate([rng.integers(0, keys.size, 20_000),
+                                    [0, keys.size - 1]])).astype(np.uint64)
+    want, err = orc.access(blob, idx)
+    assert err == 0
+    assert np.array_equal(_host(out[torch.from_numpy(idx.view(np.int64)).to(DEV)], keys.dtype),
+                          want)
+
+
+def test_full_config5_access_range(lc):
+    keys, idx, rs = make_queries()
+    blob = lc.encode(keys, 127)
+    view = lc.View(blob, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    d_keys = _dev(keys)
+    d_idx = _dev(idx)
+    got = lc.access(view, d_idx, err=err)
+    assert torch.equal(got, d_keys[d_idx])
+    del got
+    d_rs = _dev(rs)
+    rg = lc.range_decode(view, d_rs, 64, err=err)
+    ar = d_rs[:, None] + torch.arange(64, device=DEV)[None, :]
+    assert torch.equal(rg, d_keys[ar])
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    # sampled against the oracle one by one
+    s_idx = idx[:5000]
+    want, _ = orc.access(blob, s_idx)
+    assert np.array_equal(_host(lc.access(view, _dev(s_idx)), np.uint64), want)

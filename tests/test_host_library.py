@@ -1,0 +1,156 @@
+"""Host-side tests of the product library (no GPU): C-ABI exports, the C++ encoder's byte
+equality with the oracle, the validator, error codes, and the oracle/product
+boundary."""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import native as orc
+from synth import fuzz_case, make_keys
+from tests import blobparse
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lc():
+    from paper_2412_10770_b200 import _build
+    _build.build()
+    from paper_2412_10770_b200 import lc as m
+    return m
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "lc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lc):
+    names = _declared_functions()
+    assert "lc_decode" in names and "lc_access" in names and "lc_range_decode" in names
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lc.LIB_PATH], text=True)
+    exported = set(re.findall(r"\bT (lc_[a-z_0-9]+)$", out, flags=re.M))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert set(names) == set(lc.EXPORTS)
+
+
+def test_library_is_sm100a(lc):
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lc.LIB_PATH],
+                                  text=True)
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("seed", range(5000, 5150))
+def test_blob_equals_oracle_fuzz(lc, seed):
+    """P8: the product encoder and the oracle emit identical bytes (FORMAT F4/F5 are normative)."""
+    keys, eps, kb, law = fuzz_case(seed, n_max=20_000)
+    a = lc.encode(keys, eps, kb)
+    b = orc.encode(keys, eps, kb)
+    assert a == b, (seed, law)
+    assert lc.validate(a) == 0
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_blob_equals_oracle_configs_small(lc, cid):
+    keys = make_keys(cid, 200_000 if cid != 1 else None)
+    eps = {1: 63, 2: 127, 3: 255, 4: 31, 5: 127}[cid]
+    a = lc.encode(keys, eps)
+    assert a == orc.encode(keys, eps)
+    bl = blobparse.parse(a)
+    assert len(a) == blobparse.expected_size(keys.size, bl.L, bl.b)
+
+
+def test_overflow_and_extremes_equal(lc):
+    cases = [
+        (np.array([0, (1 << 31) - 1, 1 << 32], np.uint64), 0),
+        (np.array([0, 1 << 31, (1 << 32) + 5], np.uint64), 0),
+        (np.array([0, 1, 2, 1 << 40, (1 << 64) - 6, (1 << 64) - 2, (1 << 64) - 1], np.uint64), 255),
+        (np.array([5], np.uint64), 3),
+        (np.array([0xFFFFFFFF], np.uint32), 0),
+        (np.arange(5000, dtype=np.uint64) * np.uint64(1 << 20), 0),
+        (np.arange(5000, dtype=np.uint64) * np.uint64(1 << 20), (1 << 31) - 1),
+    ]
+    for keys, eps in cases:
+        assert lc.encode(keys, eps) == orc.encode(keys, eps), (keys[:3], eps)
+
+
+def test_encode_errors(lc):
+    def code(fn):
+        with pytest.raises(lc.LcError) as e:
+            fn()
+        return e.value.code
+    assert code(lambda: lc.encode(np.zeros(0, np.uint64), 3)) == lc.LC_ERR_EMPTY
+    assert code(lambda: lc.encode(np.array([1, 5, 5], np.uint64), 3)) == lc.LC_ERR_UNSORTED
+    assert code(lambda: lc.encode(np.array([9, 3], np.uint64), 3)) == lc.LC_ERR_UNSORTED
+    assert code(lambda: lc.encode(np.array([1, 2], np.uint64), 1 << 31)) == lc.LC_ERR_ARG
+    assert code(lambda: lc.encode(np.array([1, 1 << 33], np.uint64), 3, 32)) == lc.LC_ERR_TOO_LARGE
+    assert code(lambda: lc.encode(np.array([1, 2], np.uint64), 3, 16)) == lc.LC_ERR_ARG
+
+
+def test_validator_agrees_with_oracle(lc):
+    keys = make_keys(5, 7000)
+    blob = lc.encode(keys, 127)
+    bl = blobparse.parse(blob)
+
+    def put(off, val):
+        b = bytearray(blob)
+        b[off:off + len(val)] = val
+        return bytes(b)
+
+    variants = [
+        blob, blob[:-4], put(0, b"ZZZZ"), put(4, b"\x07"), put(7, b"\x03"), put(12, b"\x0b"),
+        put(bl.o_starts + 4, np.uint32(0).tobytes()),
+        put(bl.o_starts + 4 * bl.L, np.uint32(keys.size + 1).tobytes()),
+        put(bl.o_hint, np.uint32(3).tobytes()),
+        put(bl.o_params + 24, np.uint64((1 << 63) - 1).tobytes()),
+        put(bl.o_words, np.uint32(0xFFFFFFFF).tobytes()),
+        put(bl.o_words + 4 * bl.W - 4, b"\x80"),
+        put(200, b"\x01"),
+    ]
+    for i, v in enumerate(variants):
+        want = orc.validate(v)
+        got = lc.validate(v)
+        assert (got == 0) == (want == 0), (i, got, want)
+        if want:
+            assert got == lc.LC_ERR_FORMAT, i
+
+
+def test_header_struct_matches_format(lc):
+    keys = make_keys(1, 5000)
+    blob = lc.encode(keys, 63)
+    h = lc.header(blob)
+    bl = blobparse.parse(blob)
+    assert h.magic == b"LCG1" and h.version == 1 and h.key_bits == 32 and h.res_bits == 7
+    assert (h.n, h.n_seg, h.n_hint, h.n_words) == (bl.n, bl.L, bl.n_hint, bl.W)
+    assert (h.off_starts, h.off_params, h.off_hint, h.off_words, h.total_bytes) == (
+        bl.o_starts, bl.o_params, bl.o_hint, bl.o_words, len(blob))
+
+
+def test_product_never_touches_oracle():
+    """The product path must not import, load or call anything under oracle/ (task ②/③)."""
+    pkg = os.path.join(ROOT, "paper_2412_10770_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                src = open(os.path.join(dirpath, f), errors="ignore").read()
+                bad = re.findall(r"import oracle|from oracle|liblc_oracle|lc_oracle|"
+                                 r"oracle_[a-z_]+\(|oracle\.native|oracle\.pyref", src)
+                assert not bad, (f, bad)
+
+
+def test_oracle_never_touches_product():
+    for dirpath, _, files in os.walk(os.path.join(ROOT, "oracle")):
+        for f in files:
+            if f.endswith((".py", ".c", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import paper_2412_10770_b200" not in src
+                assert "from paper_2412_10770_b200" not in src
+                assert "liblc.so" not in src
+                assert "lc_kernels" not in src
