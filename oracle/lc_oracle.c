@@ -453,6 +453,9 @@ int32_t oracle_validate(const uint8_t* B, uint64_t bytes) {
     /* residual fields in [0, 2 eps]; stream bits past n*b are zero */
     for (uint64_t i = 0; i < h.n; i++)
         if (field_at(B + h.o_words, i, h.b) > 2ULL * h.eps) return OR_ERR_FORMAT;
+    /* anchor: the field at every segment start is eps (base_j = K[s_j]) */
+    for (uint64_t j = 0; j < h.L; j++)
+        if (field_at(B + h.o_words, rd32(B + h.o_starts + 4 * j), h.b) != h.eps) return OR_ERR_FORMAT;
     for (uint64_t p = h.n * h.b; p < 32 * h.W; p++)
         if (bit_at(B + h.o_words, p)) return OR_ERR_FORMAT;
     /* decoded keys strictly increasing and within key_bits (corruption detector) */

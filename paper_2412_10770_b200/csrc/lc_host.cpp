@@ -272,6 +272,7 @@ int32_t lc_validate(const void* blob, uint64_t blob_bytes) {
                 u = (two >> (p & 31)) & ((1ULL << b) - 1);
             }
             if (u > 2 * eps) return LC_ERR_FORMAT;
+            if (i == S[j] && u != eps) return LC_ERR_FORMAT;  // anchor: base_j = K[s_j]
             const u128 full = (u128)base + (run >> 32) + u;
             if (full < eps || full - eps > kmax) return LC_ERR_FORMAT;
             const uint64_t key = (uint64_t)(full - eps);

@@ -22,9 +22,11 @@
 //    scheme reading through L1.
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <utility>
 
 #include "lc.h"
 #include "lc_internal.h"
@@ -115,90 +117,127 @@ struct DecodeArgs {
     uint32_t i0, i1;   // i0 % 1024 == 0
     uint32_t chunk0;   // i0 / 1024
     uint32_t nchunks;  // ceil((i1 - i0) / 1024)
-    uint32_t b, eps, mask;
+    uint32_t eps;
     uint32_t warp_bytes;  // shared memory per warp
 };
 
+// Per-warp shared-memory page: [mbarrier | starts (kSegCap+4) | params kSegCap | words]
 __host__ __device__ constexpr uint32_t page_starts_off() { return 16; }
 __host__ __device__ constexpr uint32_t page_params_off() { return 16 + 4 * (kSegCap + 4); }
 __host__ __device__ constexpr uint32_t page_words_off() { return page_params_off() + 16 * kSegCap; }
+__host__ __device__ constexpr uint32_t warp_bytes_for(uint32_t b) {
+    return (page_words_off() + 4 * (b ? 32 * b + 4 : 0) + 127) & ~127u;
+}
 
-template <bool K64>
+struct Page {
+    uint64_t* bar;
+    uint32_t* sS;         // starts[pj .. pj + cs)
+    ulonglong2* sP;       // params[pj .. pj + cp)
+    uint32_t* sW;         // the chunk's residual words
+    uint32_t pj, cp;
+    uint32_t phase;
+};
+
+// Stage starts[pj, pj + cs) and params[pj, pj + cp) (plus, when wbytes != 0, the chunk's words)
+// with TMA bulk copies; cs covers one start past the params so every window candidate
+// (clamped at jlast + 1) is a real start.  Lane 0 issues, the warp waits on the mbarrier.
+__device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t from, uint32_t jlast,
+                                      const uint32_t* wsrc, uint32_t wbytes, uint32_t lane) {
+    __syncwarp();  // every lane is done reading the previous contents
+    pg.pj = from & ~3u;
+    pg.cp = min(kSegCap, jlast + 1 - pg.pj);
+    if (lane == 0) {
+        const uint32_t cs = min(kSegCap + 4, jlast + 2 - pg.pj);
+        const uint32_t sbytes = ((cs + 3) & ~3u) * 4, pbytes = pg.cp * 16;
+        mbar_expect_tx(pg.bar, sbytes + pbytes + wbytes);
+        bulk_g2s(pg.sS, sec.starts + pg.pj, sbytes, pg.bar);
+        bulk_g2s(pg.sP, sec.params + pg.pj, pbytes, pg.bar);
+        if (wbytes) bulk_g2s(pg.sW, wsrc, wbytes, pg.bar);
+    }
+    mbar_wait(pg.bar, pg.phase);
+    pg.phase ^= 1;
+}
+
+// Decode one 32-key window [wb, wb + 32) of a chunk, lane = key.  w is the window index in
+// the chunk (selects the residual words).  Segment j of each lane: boundaries inside the
+// window form a bitmask (REDUX.OR over the next 32 segment starts); popc/clz give the
+// segment and the offset d = i - s_j with no search.  key = base + t with
+// t = floor(slope d / 2^32) + u - eps = K[i] - K[s_j] in [0, 2^32) (FORMAT F2 anchor + guard).
+template <bool K64, uint32_t B, bool FULL>
+__device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
+                                              uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                              uint32_t w, uint32_t lane, uint32_t lmask,
+                                              uint32_t lw, uint32_t ls, uint32_t eps,
+                                              void* outw, uint32_t valid) {
+    if (min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[cand - pg.pj] - wb;  // > 0: position of the next start
+    const uint32_t P = __reduce_or_sync(kFull, x < 32 ? (1u << x) : 0u);
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
+    const uint32_t m = P & lmask;  // boundaries at or before this lane's key
+    const uint32_t seg = jb + __popc(m);
+    const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
+    const ulonglong2 pr = pg.sP[seg - pg.pj];
+    uint32_t u = 0;
+    if (B) {
+        constexpr uint32_t mask = B >= 32 ? 0xffffffffu : ((1u << (B & 31)) - 1);
+        const uint32_t* wp = pg.sW + w * B + lw;
+        u = __funnelshift_r(wp[0], wp[1], ls) & mask;
+    }
+    const uint32_t t = pred_delta(pr.y, d) + u - eps;  // = K[i] - base, exact mod 2^32
+    if (FULL || lane < valid) {
+        if (K64) __stcs((unsigned long long*)outw + lane, (unsigned long long)(pr.x + t));
+        else __stcs((unsigned int*)outw + lane, (unsigned int)pr.x + t);
+    }
+    jb += adv;
+    sb = pg.sS[jb - pg.pj];
+}
+
+template <bool K64, uint32_t B>
 __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* page = smem + warp * a.warp_bytes;
-    uint64_t* bar = (uint64_t*)page;
-    uint32_t* sS = (uint32_t*)(page + page_starts_off());
-    const ulonglong2* sP = (const ulonglong2*)(page + page_params_off());
-    uint32_t* sW = (uint32_t*)(page + page_words_off());
-    if (lane == 0) mbar_init(bar);
+    uint8_t* base = smem + warp * a.warp_bytes;
+    Page pg;
+    pg.bar = (uint64_t*)base;
+    pg.sS = (uint32_t*)(base + page_starts_off());
+    pg.sP = (ulonglong2*)(base + page_params_off());
+    pg.sW = (uint32_t*)(base + page_words_off());
+    pg.phase = 0;
+    if (lane == 0) mbar_init(pg.bar);
     __syncwarp();
-    uint32_t phase = 0;
 
-    const uint32_t b = a.b;
-    const uint32_t lw = (lane * b) >> 5, ls = (lane * b) & 31;  // lane's field in a window
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lw = (lane * B) >> 5, ls = (lane * B) & 31;  // lane's field in a window
     const uint32_t lmask = lanemask_le();
     const uint32_t nwarps = gridDim.x * kWarpsPerCta;
+    const Sections sec = a.sec;
 
     for (uint32_t c = blockIdx.x * kWarpsPerCta + warp; c < a.nchunks; c += nwarps) {
         const uint32_t h = a.chunk0 + c;
         const uint32_t key0 = h << 10;
         const uint32_t nk = min(1024u, a.i1 - key0);
-        const uint32_t j0 = __ldg(a.sec.hint + h);
-        const uint32_t jlast = __ldg(a.sec.hint + h + 1);  // last segment the chunk can touch
-        uint32_t pj = j0 & ~3u;                             // page = segments [pj, pj + cnt)
-        uint32_t cnt = min(kSegCap, jlast + 1 - pj);
-        __syncwarp();  // all lanes are done with the previous chunk's page
-        if (lane == 0) {
-            const uint32_t sbytes = ((cnt + 3) & ~3u) * 4, pbytes = cnt * 16;
-            const uint32_t wbytes = b ? ((((nk * b + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
-            mbar_expect_tx(bar, sbytes + pbytes + wbytes);
-            bulk_g2s(sS, a.sec.starts + pj, sbytes, bar);
-            bulk_g2s((void*)sP, a.sec.params + pj, pbytes, bar);
-            if (wbytes) bulk_g2s(sW, a.sec.words + (size_t)h * 32 * b, wbytes, bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-
-        uint32_t jb = j0;              // segment holding the window's first key
-        uint32_t sb = sS[j0 - pj];     // its start
-        const uint32_t nwin = (nk + 31) >> 5;
-        for (uint32_t w = 0; w < nwin; ++w) {
-            const uint32_t wb = key0 + (w << 5);
-            const uint32_t need = min(jb + 32, jlast);
-            if (need >= pj + cnt) {  // warp-uniform: re-page a dense chunk
-                __syncwarp();
-                pj = jb & ~3u;
-                cnt = min(kSegCap, jlast + 1 - pj);
-                if (lane == 0) {
-                    const uint32_t sbytes = ((cnt + 3) & ~3u) * 4, pbytes = cnt * 16;
-                    mbar_expect_tx(bar, sbytes + pbytes);
-                    bulk_g2s(sS, a.sec.starts + pj, sbytes, bar);
-                    bulk_g2s((void*)sP, a.sec.params + pj, pbytes, bar);
-                }
-                mbar_wait(bar, phase);
-                phase ^= 1;
+        const uint32_t j0 = __ldg(sec.hint + h);
+        const uint32_t jlast = __ldg(sec.hint + h + 1);  // last segment the chunk can touch
+        const uint32_t wbytes = B ? ((((nk * B + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
+        stage(pg, sec, j0, jlast, sec.words + (size_t)h * 32 * B, wbytes, lane);
+        uint32_t jb = j0;                // segment holding the window's first key
+        uint32_t sb = pg.sS[j0 - pg.pj];  // its start
+        uint8_t* out = (uint8_t*)a.out + (size_t)(key0 - a.i0) * kw;
+        if (nk == 1024) {
+#pragma unroll 1
+            for (uint32_t g = 0; g < 32; g += 8) {
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k)
+                    decode_window<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 32 * (g + k), g + k,
+                                                lane, lmask, lw, ls, a.eps,
+                                                out + 32 * kw * (g + k), 32);
             }
-            // segment starts inside (wb, wb + 32] -> bitmask over the window
-            const uint32_t cand = jb + 1 + lane;
-            const uint32_t x = (cand <= jlast) ? sS[cand - pj] - wb : kFull;
-            const uint32_t P = __reduce_or_sync(kFull, x < 32 ? (1u << x) : 0u);
-            const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
-            const uint32_t m = P & lmask;  // boundaries at or before this lane's key
-            const uint32_t seg = jb + __popc(m);
-            const uint32_t d = m ? lane - (31 - __clz(m)) : wb + lane - sb;
-            const ulonglong2 pr = sP[seg - pj];
-            const uint32_t delta = pred_delta(pr.y, d);
-            uint32_t u = 0;
-            if (b) {
-                const uint32_t wi = w * b + lw;
-                u = __funnelshift_r(sW[wi], sW[wi + 1], ls) & a.mask;
-            }
-            const uint32_t i = wb + lane;
-            if (i < a.i1) store_key<K64>(a.out, i - a.i0, pr.x, delta, u, a.eps);
-            jb += adv;
-            if (adv) sb = sS[jb - pj];
+        } else {  // ragged tail chunk
+            for (uint32_t w = 0; 32 * w < nk; ++w)
+                decode_window<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane, lmask,
+                                             lw, ls, a.eps, out + 32 * kw * w, nk - 32 * w);
         }
     }
 }
@@ -313,15 +352,27 @@ uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
 
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? LC_OK : LC_ERR_CUDA; }
 
+using DecodeFn = void (*)(DecodeArgs);
+
+template <bool K64, uint32_t... Bs>
+constexpr std::array<DecodeFn, sizeof...(Bs)> decode_table(std::integer_sequence<uint32_t, Bs...>) {
+    return {{&lc_decode_kernel<K64, Bs>...}};
+}
+// one instantiation per residual width b = 0..32 (compile-time field offsets and masks)
+const std::array<DecodeFn, 33> kDecode[2] = {
+    decode_table<false>(std::make_integer_sequence<uint32_t, 33>{}),
+    decode_table<true>(std::make_integer_sequence<uint32_t, 33>{})};
+
 struct GridCache {
     std::mutex mu;
     int dev = -1;
     int sms = 0;
-    int occ[2][64] = {};  // [K64][warp_bytes / 256] -> CTAs per SM
+    int occ[2][33] = {};  // [K64][res_bits] -> resident CTAs per SM
 };
 GridCache g_grid;
 
-int persistent_grid(bool k64, uint32_t smem_bytes, uint32_t warp_bytes) {
+// persistent grid size for the decode kernel: SMs x resident CTAs at this smem footprint
+int persistent_grid(bool k64, uint32_t b) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_grid.mu);
@@ -330,12 +381,12 @@ int persistent_grid(bool k64, uint32_t smem_bytes, uint32_t warp_bytes) {
         cudaDeviceGetAttribute(&g_grid.sms, cudaDevAttrMultiProcessorCount, dev);
         std::memset(g_grid.occ, 0, sizeof g_grid.occ);
     }
-    const uint32_t slot = (warp_bytes / 256) & 63;
-    int& occ = g_grid.occ[k64][slot];
+    int& occ = g_grid.occ[k64][b];
     if (occ == 0) {
-        const void* fn = k64 ? (const void*)lc_decode_kernel<true> : (const void*)lc_decode_kernel<false>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem_bytes);
+        const void* fn = (const void*)kDecode[k64][b];
+        const int smem = (int)(warp_bytes_for(b) * kWarpsPerCta);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
         if (occ < 1) occ = 1;
     }
     return occ * g_grid.sms;
@@ -349,18 +400,15 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     a.i1 = (uint32_t)i1;
     a.chunk0 = (uint32_t)(i0 >> 10);
     a.nchunks = (uint32_t)((i1 - i0 + 1023) >> 10);
-    a.b = v->h.res_bits;
     a.eps = v->h.eps;
-    a.mask = mask_of(a.b);
-    const uint32_t words_cap = a.b ? 32 * a.b + 4 : 0;
-    a.warp_bytes = (page_words_off() + 4 * words_cap + 127) & ~127u;
+    const uint32_t b = v->h.res_bits;
+    a.warp_bytes = warp_bytes_for(b);
     const uint32_t smem = a.warp_bytes * kWarpsPerCta;
     const bool k64 = v->h.key_bits == 64;
-    const int full = persistent_grid(k64, smem, a.warp_bytes);
+    const int full = persistent_grid(k64, b);
     const uint32_t need = (a.nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const uint32_t grid = need < (uint32_t)full ? need : (uint32_t)full;
-    if (k64) lc_decode_kernel<true><<<grid, kThreads, smem, st>>>(a);
-    else lc_decode_kernel<false><<<grid, kThreads, smem, st>>>(a);
+    kDecode[k64][b]<<<grid, kThreads, smem, st>>>(a);
     lc_detail::count_launch(1);
     return cuda_status();
 }

@@ -113,6 +113,8 @@ def test_validator_agrees_with_oracle(lc):
         put(bl.o_words, np.uint32(0xFFFFFFFF).tobytes()),
         put(bl.o_words + 4 * bl.W - 4, b"\x80"),
         put(200, b"\x01"),
+        put(bl.o_words, np.uint32(int(bl.words[0]) ^ 1).tobytes()),  # anchor field u_0 != eps
+        put(bl.o_params, np.uint64(int(bl.base[0]) + 1).tobytes()),  # shifted base: still valid
     ]
     for i, v in enumerate(variants):
         want = orc.validate(v)

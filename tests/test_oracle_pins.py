@@ -359,6 +359,7 @@ def test_validate_rejects_corruption():
         _corrupt(blob, 100, b"\x01"),                                  # reserved byte
         _corrupt(blob, bl.o_words + 4 * bl.W - 4, b"\x01"),            # nonzero pad bit
         _corrupt(blob, bl.o_params + 8, np.uint64(1 << 63).tobytes()),  # negative slope
+        _corrupt(blob, bl.o_words, np.uint32(int(bl.words[0]) ^ 1).tobytes()),  # u_0 != eps
     ]
     for i, b in enumerate(bad):
         assert orc.validate(b) == -5, i
