@@ -99,6 +99,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ uint32_t pred_delta(uint64_t slope, uint32_t d) {
     return __umulhi((uint32_t)slope, d) + (uint32_t)(slope >> 32) * d;
 }
+// t = floor(slope * d / 2^32) + v  (v = u - eps): mul.hi + mad.lo + add, kept as 3 ops
+__device__ __forceinline__ uint32_t pred_plus(uint64_t slope, uint32_t d, uint32_t v) {
+    uint32_t t;
+    asm("{\n.reg .u32 h;\nmul.hi.u32 h, %1, %2;\nmad.lo.u32 h, %3, %2, h;\nadd.u32 %0, h, %4;\n}"
+        : "=r"(t)
+        : "r"((uint32_t)slope), "r"(d), "r"((uint32_t)(slope >> 32)), "r"(v));
+    return t;
+}
 
 template <bool K64>
 __device__ __forceinline__ void store_key(void* out, uint64_t pos, uint64_t base, uint32_t delta,
@@ -163,33 +171,85 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
 // window form a bitmask (REDUX.OR over the next 32 segment starts); popc/clz give the
 // segment and the offset d = i - s_j with no search.  key = base + t with
 // t = floor(slope d / 2^32) + u - eps = K[i] - K[s_j] in [0, 2^32) (FORMAT F2 anchor + guard).
-template <bool K64, uint32_t B, bool FULL>
+template <uint32_t B>
+__device__ __forceinline__ uint32_t field(const uint32_t* sW, uint32_t w, uint32_t lw, uint32_t ls) {
+    if (!B) return 0;
+    constexpr uint32_t mask = B >= 32 ? 0xffffffffu : ((1u << (B & 31)) - 1);
+    const uint32_t* wp = sW + w * B + lw;
+    return __funnelshift_r(wp[0], wp[1], ls) & mask;
+}
+
+template <bool K64>
+__device__ __forceinline__ void put(void* outl, uint64_t base, uint32_t t) {  // outl: lane's slot
+    if (K64) __stcs((unsigned long long*)outl, (unsigned long long)(base + t));
+    else __stcs((unsigned int*)outl, (unsigned int)base + t);
+}
+
+__device__ __forceinline__ uint32_t bit_or_zero(uint32_t x) {  // 1 << x, 0 when x >= 32
+    uint32_t r;
+    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
+template <bool K64, uint32_t B, bool CHECK, bool FULL>
 __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
                                               uint32_t& sb, uint32_t jlast, uint32_t wb,
                                               uint32_t w, uint32_t lane, uint32_t lmask,
                                               uint32_t lw, uint32_t ls, uint32_t eps,
                                               void* outw, uint32_t valid) {
-    if (min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[cand - pg.pj] - wb;  // > 0: position of the next start
-    const uint32_t P = __reduce_or_sync(kFull, x < 32 ? (1u << x) : 0u);
+    const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x));
     const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
     const uint32_t m = P & lmask;  // boundaries at or before this lane's key
     const uint32_t seg = jb + __popc(m);
     const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
     const ulonglong2 pr = pg.sP[seg - pg.pj];
-    uint32_t u = 0;
-    if (B) {
-        constexpr uint32_t mask = B >= 32 ? 0xffffffffu : ((1u << (B & 31)) - 1);
-        const uint32_t* wp = pg.sW + w * B + lw;
-        u = __funnelshift_r(wp[0], wp[1], ls) & mask;
+    const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - eps);
+    if (FULL || lane < valid) put<K64>(outw, pr.x, t);
+    jb += adv;
+    sb = pg.sS[jb - pg.pj];
+}
+
+// Two windows at once: keys [wb, wb + 64), lane handles wb + lane and wb + 32 + lane.  One
+// candidate load / vote serves both halves when fewer than 32 segment starts fall inside;
+// otherwise it falls back to two single windows.  w2 = pair index (windows 2 w2, 2 w2 + 1).
+template <bool K64, uint32_t B, bool CHECK>
+__device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint32_t& jb,
+                                            uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                            uint32_t w2, uint32_t lane, uint32_t lmask,
+                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[cand - pg.pj] - wb;
+    const uint32_t inside = __ballot_sync(kFull, x < 64);
+    if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
+        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
+                                           ls, eps, outw, 32);
+        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
+                                           lmask, lw, ls, eps, (uint8_t*)outw + 32 * kw, 32);
+        return;
     }
-    const uint32_t t = pred_delta(pr.y, d) + u - eps;  // = K[i] - base, exact mod 2^32
-    if (FULL || lane < valid) {
-        if (K64) __stcs((unsigned long long*)outw + lane, (unsigned long long)(pr.x + t));
-        else __stcs((unsigned int*)outw + lane, (unsigned int)pr.x + t);
-    }
+    const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));       // starts in (wb, wb+32)
+    const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));  // starts in [wb+32, wb+64)
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
+    const uint32_t off0 = wb - sb;                                      // uniform
+    const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;               // uniform
+    const uint32_t jB = jb + __popc(PA);                                // uniform
+    const uint32_t mA = PA & lmask;
+    const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+    const ulonglong2 pA = pg.sP[jb + __popc(mA) - pg.pj];
+    const uint32_t mB = PB & lmask;
+    const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+    const ulonglong2 pB = pg.sP[jB + __popc(mB) - pg.pj];
+    const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - eps);
+    const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps);
+    put<K64>(outw, pA.x, tA);
+    put<K64>((uint8_t*)outw + 32 * kw, pB.x, tB);
     jb += adv;
     sb = pg.sS[jb - pg.pj];
 }
@@ -214,30 +274,49 @@ __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a)
     const uint32_t nwarps = gridDim.x * kWarpsPerCta;
     const Sections sec = a.sec;
 
-    for (uint32_t c = blockIdx.x * kWarpsPerCta + warp; c < a.nchunks; c += nwarps) {
+    uint32_t c = blockIdx.x * kWarpsPerCta + warp;
+    // hint pair of the warp's next chunk, loaded one chunk ahead (hides a DRAM round trip)
+    uint32_t nj0 = 0, njl = 0;
+    if (c < a.nchunks) {
+        nj0 = __ldg(sec.hint + a.chunk0 + c);
+        njl = __ldg(sec.hint + a.chunk0 + c + 1);
+    }
+    for (; c < a.nchunks; c += nwarps) {
         const uint32_t h = a.chunk0 + c;
         const uint32_t key0 = h << 10;
         const uint32_t nk = min(1024u, a.i1 - key0);
-        const uint32_t j0 = __ldg(sec.hint + h);
-        const uint32_t jlast = __ldg(sec.hint + h + 1);  // last segment the chunk can touch
+        const uint32_t j0 = nj0;
+        const uint32_t jlast = njl;  // last segment the chunk can touch
+        if (c + nwarps < a.nchunks) {
+            nj0 = __ldg(sec.hint + h + nwarps);
+            njl = __ldg(sec.hint + h + nwarps + 1);
+        }
         const uint32_t wbytes = B ? ((((nk * B + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
         stage(pg, sec, j0, jlast, sec.words + (size_t)h * 32 * B, wbytes, lane);
         uint32_t jb = j0;                // segment holding the window's first key
         uint32_t sb = pg.sS[j0 - pg.pj];  // its start
-        uint8_t* out = (uint8_t*)a.out + (size_t)(key0 - a.i0) * kw;
-        if (nk == 1024) {
+        uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
+        if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
 #pragma unroll 1
-            for (uint32_t g = 0; g < 32; g += 8) {
+            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
 #pragma unroll
-                for (uint32_t k = 0; k < 8; ++k)
-                    decode_window<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 32 * (g + k), g + k,
-                                                lane, lmask, lw, ls, a.eps,
-                                                out + 32 * kw * (g + k), 32);
+                for (uint32_t k = 0; k < 4; ++k)
+                    decode_pair<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
+                                               lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
+            }
+        } else if (nk == 1024) {  // dense chunk: paged
+#pragma unroll 1
+            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    decode_pair<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
+                                              lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
             }
         } else {  // ragged tail chunk
             for (uint32_t w = 0; 32 * w < nk; ++w)
-                decode_window<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane, lmask,
-                                             lw, ls, a.eps, out + 32 * kw * w, nk - 32 * w);
+                decode_window<K64, B, true, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane,
+                                                   lmask, lw, ls, a.eps, outl + 32 * kw * w,
+                                                   nk - 32 * w);
         }
     }
 }

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblc.so")
+# LC_LIB: developer override to A/B another build of the same sources (tools/ only)
+LIB_PATH = os.environ.get("LC_LIB") or os.path.join(_PKG, "liblc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; "
