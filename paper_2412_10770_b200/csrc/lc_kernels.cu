@@ -82,6 +82,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+// TMA bulk prefetch of [src, src + bytes) into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     do {
@@ -95,11 +99,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
-// floor(slope * d / 2^32) for slope * d < 2^63 (FORMAT F2 guard): exact in 32 bits.
-__device__ __forceinline__ uint32_t pred_delta(uint64_t slope, uint32_t d) {
-    return __umulhi((uint32_t)slope, d) + (uint32_t)(slope >> 32) * d;
-}
-// t = floor(slope * d / 2^32) + v  (v = u - eps): mul.hi + mad.lo + add, kept as 3 ops
+// t = floor(slope * d / 2^32) + v  (v = u - eps), with floor(slope * d / 2^32) =
+// umulhi(slope_lo, d) + slope_hi * d exact in 32 bits because slope * d < 2^63 (FORMAT F2
+// guard): mul.hi + mad.lo + add, kept as 3 ops
 __device__ __forceinline__ uint32_t pred_plus(uint64_t slope, uint32_t d, uint32_t v) {
     uint32_t t;
     asm("{\n.reg .u32 h;\nmul.hi.u32 h, %1, %2;\nmad.lo.u32 h, %3, %2, h;\nadd.u32 %0, h, %4;\n}"
@@ -127,6 +129,7 @@ struct DecodeArgs {
     uint32_t nchunks;  // ceil((i1 - i0) / 1024)
     uint32_t eps;
     uint32_t warp_bytes;  // shared memory per warp
+    uint32_t nwords;      // W (words section length)
 };
 
 // Per-warp shared-memory page: [mbarrier | starts (kSegCap+4) | params kSegCap | words]
@@ -293,6 +296,10 @@ __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a)
         }
         const uint32_t wbytes = B ? ((((nk * B + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
         stage(pg, sec, j0, jlast, sec.words + (size_t)h * 32 * B, wbytes, lane);
+        const bool has_next = c + nwarps < a.nchunks;
+        if (B && has_next && lane == 0)  // next chunk's residual words -> L2 now
+            bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
+                             min(32 * B * 4 + 16, (a.nwords - (h + nwarps) * 32 * B) * 4));
         uint32_t jb = j0;                // segment holding the window's first key
         uint32_t sb = pg.sS[j0 - pg.pj];  // its start
         uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
@@ -303,6 +310,12 @@ __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a)
                 for (uint32_t k = 0; k < 4; ++k)
                     decode_pair<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
                                                lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
+                if (g == 4 && has_next && lane == 0) {  // next chunk's hint pair has landed:
+                    const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
+                    const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
+                    bulk_prefetch_l2(sec.starts + npj, ((ncs + 3) & ~3u) * 4);
+                    bulk_prefetch_l2(sec.params + npj, min(kSegCap, njl + 1 - npj) * 16);
+                }
             }
         } else if (nk == 1024) {  // dense chunk: paged
 #pragma unroll 1
@@ -321,45 +334,6 @@ __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a)
     }
 }
 
-// ------------------------------------------------------------------------- random access
-struct AccessArgs {
-    Sections sec;
-    const uint64_t* idx;
-    void* out;
-    uint32_t* err;
-    uint64_t q;
-    uint32_t n, b, eps, mask;
-};
-
-template <bool K64>
-__global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
-    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-    if (t >= a.q) return;
-    const uint64_t i64 = __ldcs(a.idx + t);
-    if (i64 >= a.n) {
-        if (a.err) atomicOr(a.err, 1u);
-        if (K64) __stcs((unsigned long long*)a.out + t, 0ull);
-        else __stcs((unsigned int*)a.out + t, 0u);
-        return;
-    }
-    const uint32_t i = (uint32_t)i64;
-    uint32_t lo = __ldg(a.sec.hint + (i >> 10)), hi = __ldg(a.sec.hint + (i >> 10) + 1);
-    while (lo < hi) {  // j = max{t in [lo, hi] : starts[t] <= i}
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(a.sec.starts + mid) <= i) lo = mid;
-        else hi = mid - 1;
-    }
-    const uint32_t s = __ldg(a.sec.starts + lo);
-    const ulonglong2 pr = __ldg(a.sec.params + lo);
-    uint32_t u = 0;
-    if (a.b) {
-        const uint64_t bit = (uint64_t)i * a.b;
-        const uint32_t* wp = a.sec.words + (bit >> 5);
-        u = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & a.mask;
-    }
-    store_key<K64>(a.out, t, pr.x, pred_delta(pr.y, i - s), u, a.eps);
-}
-
 // -------------------------------------------------------------------------- range decode
 struct RangeArgs {
     Sections sec;
@@ -370,59 +344,213 @@ struct RangeArgs {
     uint32_t len, n, L, b, eps, mask;
 };
 
+// j = max{t in [hint[i>>10], hint[(i>>10)+1]] : starts[t] <= i} (Table I caption)
+__device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i) {
+    uint32_t lo = __ldg(sec.hint + (i >> 10)), hi = __ldg(sec.hint + (i >> 10) + 1);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(sec.starts + mid) <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// residual field of key i read from global words (two loads + funnel shift)
+__device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b) {
+    const uint64_t bit = (uint64_t)i * b;
+    const uint32_t* wp = sec.words + (bit >> 5);
+    return make_uint2(__ldg(wp), __ldg(wp + 1));
+}
+__device__ __forceinline__ uint32_t field_of(uint2 w, uint32_t i, uint32_t b, uint32_t mask) {
+    return __funnelshift_r(w.x, w.y, (i * b) & 31) & mask;
+}
+
+// One warp decodes 32 ranges.  Phase 1: lane r binary-searches the segment of range r's first
+// key (32 independent searches in flight).  Phase 2: the warp decodes the ranges one after
+// another with the window scheme of the full decode (64 keys per step, 2 keys per lane),
+// prefetching the next range's candidate starts and residual words so that each step waits
+// on a single dependent load (the params gather).
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
-    const uint64_t r = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    constexpr uint32_t kw = K64 ? 8 : 4;
     const uint32_t lane = threadIdx.x & 31;
-    if (r >= a.q) return;  // warp-uniform
-    const uint64_t rs64 = __ldg(a.start + r);
-    const uint64_t obase = r * a.len;
-    if (rs64 > a.n || a.len > a.n - rs64) {
-        if (lane == 0 && a.err) atomicOr(a.err, 1u);
-        for (uint32_t k = lane; k < a.len; k += 32) store_key<K64>(a.out, obase + k, 0, 0, 0, 0);
-        return;
-    }
-    const uint32_t rs = (uint32_t)rs64;
-    // warp-cooperative search for j = max{t : starts[t] <= rs} inside the hint bracket
-    uint32_t lo = __ldg(a.sec.hint + (rs >> 10)), hi = __ldg(a.sec.hint + (rs >> 10) + 1);
-    while (hi - lo + 1 > 32) {
-        const uint32_t step = (hi - lo + 32) >> 5;  // ceil((hi - lo + 1) / 32)
-        const uint32_t p = lo + lane * step;
-        const bool ok = p <= hi && __ldg(a.sec.starts + p) <= rs;
-        const uint32_t c = __popc(__ballot_sync(kFull, ok));  // >= 1: starts[lo] <= rs
-        lo += (c - 1) * step;
-        hi = min(hi, lo + step - 1);
-    }
-    {
-        const uint32_t p = lo + lane;
-        const bool ok = p <= hi && __ldg(a.sec.starts + p) <= rs;
-        lo += __popc(__ballot_sync(kFull, ok)) - 1;
-    }
-    uint32_t jb = lo, sb = __ldg(a.sec.starts + lo);
+    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    if (r0 >= a.q) return;  // warp-uniform
+    const Sections sec = a.sec;
+    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L;
     const uint32_t lmask = lanemask_le();
-    const uint32_t jmax = a.L - 1;
-    for (uint32_t w0 = 0; w0 < a.len; w0 += 32) {
-        const uint32_t wb = rs + w0;
-        const uint32_t cand = jb + 1 + lane;
-        const uint32_t x = (cand <= jmax) ? __ldg(a.sec.starts + cand) - wb : kFull;
-        const uint32_t P = __reduce_or_sync(kFull, x < 32 ? (1u << x) : 0u);
-        const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
-        const uint32_t m = P & lmask;
-        const uint32_t seg = jb + __popc(m);
-        const uint32_t d = m ? lane - (31 - __clz(m)) : wb + lane - sb;
-        const uint32_t k = w0 + lane;
-        if (k < a.len) {
-            const ulonglong2 pr = __ldg(a.sec.params + seg);
-            uint32_t u = 0;
-            if (a.b) {
-                const uint64_t bit = (uint64_t)(wb + lane) * a.b;
-                const uint32_t* wp = a.sec.words + (bit >> 5);
-                u = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & a.mask;
-            }
-            store_key<K64>(a.out, obase + k, pr.x, pred_delta(pr.y, d), u, a.eps);
+
+    // ---- phase 1: lane-parallel search
+    uint32_t rs = 0, j = 0, sj = 0, ok = 0;
+    if (r0 + lane < a.q) {
+        const uint64_t s64 = __ldg(a.start + r0 + lane);
+        if (s64 <= a.n && len <= a.n - s64) {
+            ok = 1;
+            rs = (uint32_t)s64;
+            j = seg_search(sec, rs);
+            sj = __ldg(sec.starts + j);
+        } else if (a.err) {
+            atomicOr(a.err, 1u);
         }
-        jb += adv;
-        if (adv) sb = __ldg(a.sec.starts + jb);
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+
+    // prefetch for range k: candidate start and the first pair's words
+    auto prefetch = [&](uint32_t k, uint32_t& cand_s, uint2& wA, uint2& wB) {
+        const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
+        cand_s = __ldg(sec.starts + min(jk + 1 + lane, L));
+        if (b && len >= 64) {
+            wA = field_words(sec, rk + lane, b);
+            wB = field_words(sec, rk + 32 + lane, b);
+        }
+    };
+    uint32_t pc = 0;
+    uint2 pwA = make_uint2(0, 0), pwB = make_uint2(0, 0);
+    prefetch(0, pc, pwA, pwB);
+
+    for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t rk = __shfl_sync(kFull, rs, k);
+        uint32_t jb = __shfl_sync(kFull, j, k);
+        uint32_t sb = __shfl_sync(kFull, sj, k);
+        const uint32_t okk = __shfl_sync(kFull, ok, k);
+        uint32_t cand_s = pc;
+        uint2 wA = pwA, wB = pwB;
+        if (k + 1 < nr) prefetch(k + 1, pc, pwA, pwB);
+        uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * len * kw;
+        if (!okk) {
+            for (uint32_t e = lane; e < len; e += 32) {
+                if (K64) __stcs((unsigned long long*)outk + e, 0ull);
+                else __stcs((unsigned int*)outk + e, 0u);
+            }
+            continue;
+        }
+        uint32_t w0 = 0;
+        bool first = true;
+        while (w0 < len) {
+            const uint32_t wb = rk + w0;
+            const uint32_t rem = len - w0;
+            if (!first) cand_s = __ldg(sec.starts + min(jb + 1 + lane, L));
+            const uint32_t x = cand_s - wb;
+            if (rem >= 64 && __ballot_sync(kFull, x < 64) != kFull) {
+                if (!first && b) {
+                    wA = field_words(sec, wb + lane, b);
+                    wB = field_words(sec, wb + 32 + lane, b);
+                }
+                const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
+                const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
+                const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
+                const uint32_t off0 = wb - sb;
+                const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
+                const uint32_t mA = PA & lmask, mB = PB & lmask;
+                const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+                const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+                const ulonglong2 pA = __ldg(sec.params + jb + __popc(mA));
+                const ulonglong2 pB = __ldg(sec.params + jb + __popc(PA) + __popc(mB));
+                const uint32_t uA = b ? field_of(wA, wb + lane, b, mask) : 0;
+                const uint32_t uB = b ? field_of(wB, wb + 32 + lane, b, mask) : 0;
+                put<K64>(outk + (w0 + lane) * kw, pA.x, pred_plus(pA.y, dA, uA - a.eps));
+                put<K64>(outk + (w0 + 32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - a.eps));
+                jb += adv;
+                sb = __ldg(sec.starts + jb);
+                w0 += 64;
+            } else {  // a single 32-key window (tail, or >= 32 boundaries in 64 keys)
+                const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x));
+                const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
+                const uint32_t m = P & lmask;
+                const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sb + lane;
+                if (lane < rem) {
+                    const ulonglong2 pr = __ldg(sec.params + jb + __popc(m));
+                    const uint32_t u = b ? field_of(field_words(sec, wb + lane, b), wb + lane, b, mask) : 0;
+                    put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - a.eps));
+                }
+                jb += adv;
+                sb = __ldg(sec.starts + min(jb, L));
+                w0 += 32;
+            }
+            first = false;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------- random access
+struct AccessArgs {
+    Sections sec;
+    const uint64_t* idx;
+    void* out;
+    uint32_t* err;
+    uint64_t q;
+    uint32_t n, b, eps, mask;
+};
+
+constexpr uint32_t kAccessPerThread = 2;
+
+// Dec(K^c)[i] per query (Table I): hint bracket, binary search
+// over starts, one params gather, one residual field.  Each thread serves kAccessPerThread
+// queries whose dependent load chains are interleaved; the residual words do not depend on
+// the segment and are fetched before the search.
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
+    const uint64_t t0 = (uint64_t)blockIdx.x * (256 * kAccessPerThread) + threadIdx.x;
+    const Sections sec = a.sec;
+    uint32_t i[kAccessPerThread], lo[kAccessPerThread], hi[kAccessPerThread];
+    bool live[kAccessPerThread];
+    uint2 w[kAccessPerThread];
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        const uint64_t t = t0 + 256 * k;
+        live[k] = false;
+        i[k] = 0;
+        lo[k] = hi[k] = 0;
+        w[k] = make_uint2(0, 0);
+        if (t < a.q) {
+            const uint64_t i64 = __ldcs(a.idx + t);
+            if (i64 < a.n) {
+                live[k] = true;
+                i[k] = (uint32_t)i64;
+            } else {
+                if (a.err) atomicOr(a.err, 1u);
+                if (K64) __stcs((unsigned long long*)a.out + t, 0ull);
+                else __stcs((unsigned int*)a.out + t, 0u);
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        if (live[k]) {
+            lo[k] = __ldg(sec.hint + (i[k] >> 10));
+            hi[k] = __ldg(sec.hint + (i[k] >> 10) + 1);
+            if (a.b) w[k] = field_words(sec, i[k], a.b);
+        }
+    }
+    for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
+        bool any = false;
+        uint32_t mid[kAccessPerThread], v[kAccessPerThread];
+#pragma unroll
+        for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+            mid[k] = (lo[k] + hi[k] + 1) >> 1;
+            v[k] = 0;
+            if (lo[k] < hi[k]) {
+                v[k] = __ldg(sec.starts + mid[k]);
+                any = true;
+            }
+        }
+        if (!any) break;
+#pragma unroll
+        for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+            if (lo[k] < hi[k]) {
+                if (v[k] <= i[k]) lo[k] = mid[k];
+                else hi[k] = mid[k] - 1;
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        if (!live[k]) continue;
+        const uint32_t s = __ldg(sec.starts + lo[k]);
+        const ulonglong2 pr = __ldg(sec.params + lo[k]);
+        const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
+        const uint64_t t = t0 + 256 * k;
+        put<K64>((uint8_t*)a.out + t * (K64 ? 8 : 4), pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
     }
 }
 
@@ -480,6 +608,7 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     a.chunk0 = (uint32_t)(i0 >> 10);
     a.nchunks = (uint32_t)((i1 - i0 + 1023) >> 10);
     a.eps = v->h.eps;
+    a.nwords = (uint32_t)v->h.n_words;
     const uint32_t b = v->h.res_bits;
     a.warp_bytes = warp_bytes_for(b);
     const uint32_t smem = a.warp_bytes * kWarpsPerCta;
@@ -492,13 +621,41 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     return cuda_status();
 }
 
+// lc_decode_host pipeline resources, created once per device: an H2D and a D2H copy stream and
+// one event per span and stage.
+constexpr uint32_t kMaxSpans = 64;
 struct HostPipe {
     std::mutex mu;
     int dev = -1;
-    cudaStream_t copy = nullptr;
-    cudaEvent_t ev[17] = {};
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t up[kMaxSpans] = {}, dec[kMaxSpans] = {}, done = nullptr;
 };
 HostPipe g_pipe;
+
+int32_t pipe_init() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_pipe.dev == dev) return LC_OK;
+    if (cudaStreamCreateWithFlags(&g_pipe.h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g_pipe.d2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_pipe.done, cudaEventDisableTiming) != cudaSuccess)
+        return LC_ERR_CUDA;
+    for (uint32_t k = 0; k < kMaxSpans; ++k)
+        if (cudaEventCreateWithFlags(&g_pipe.up[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g_pipe.dec[k], cudaEventDisableTiming) != cudaSuccess)
+            return LC_ERR_CUDA;
+    g_pipe.dev = dev;
+    return LC_OK;
+}
+
+// host->device copy of blob bytes [a, b) (same offsets on both sides)
+int32_t up_bytes(const void* h, void* d, uint64_t a, uint64_t b, cudaStream_t st) {
+    if (b <= a) return LC_OK;
+    return cudaMemcpyAsync((uint8_t*)d + a, (const uint8_t*)h + a, b - a, cudaMemcpyHostToDevice,
+                           st) == cudaSuccess
+               ? LC_OK
+               : LC_ERR_CUDA;
+}
 
 }  // namespace
 
@@ -532,7 +689,7 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
     a.b = v->h.res_bits;
     a.eps = v->h.eps;
     a.mask = mask_of(a.b);
-    const uint64_t grid = (q + 255) / 256;
+    const uint64_t grid = (q + 256 * kAccessPerThread - 1) / (256 * kAccessPerThread);
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     if (v->h.key_bits == 64)
         lc_access_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
@@ -560,7 +717,7 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     a.b = v->h.res_bits;
     a.eps = v->h.eps;
     a.mask = mask_of(a.b);
-    const uint64_t grid = (q + 7) / 8;
+    const uint64_t grid = (q + 255) / 256;  // 8 warps x 32 ranges per CTA
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     if (v->h.key_bits == 64)
         lc_range_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
@@ -578,36 +735,51 @@ int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, vo
     int32_t st = lc_view_init(&v, h_blob, d_blob, blob_bytes);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemcpyAsync(d_blob, h_blob, v.h.total_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return LC_ERR_CUDA;
-    // decode in spans; each span's device->host copy runs on a side stream and overlaps the
-    // next span's decode
-    int dev = 0;
-    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_pipe.mu);
-    if (g_pipe.dev != dev) {
-        if (cudaStreamCreateWithFlags(&g_pipe.copy, cudaStreamNonBlocking) != cudaSuccess)
-            return LC_ERR_CUDA;
-        for (auto& e : g_pipe.ev)
-            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return LC_ERR_CUDA;
-        g_pipe.dev = dev;
-    }
-    const uint64_t n = v.h.n, w = v.h.key_bits / 8;
-    const uint64_t spans = 16;
-    const uint64_t per = ((n + spans - 1) / spans + 1023) & ~1023ULL;
+    if ((st = pipe_init())) return st;
+    // order the pipeline after whatever the caller queued on its stream
+    cudaEventRecord(g_pipe.done, s);
+    cudaStreamWaitEvent(g_pipe.h2d, g_pipe.done, 0);
+    cudaStreamWaitEvent(g_pipe.d2h, g_pipe.done, 0);
+
+    const lc_header& h = v.h;
+    const uint8_t* B = (const uint8_t*)h_blob;
+    const uint32_t* hint = (const uint32_t*)(B + h.off_hint);
+    const uint64_t n = h.n, w = h.key_bits / 8, L = h.n_seg, b = h.res_bits;
+    const uint64_t H = h.n_hint - 1;
+    // spans of >= 4 Mi keys (multiples of 1024), at most kMaxSpans
+    uint64_t per = (n + kMaxSpans - 1) / kMaxSpans;
+    if (per < (4u << 20)) per = 4u << 20;
+    per = (per + 1023) & ~1023ULL;
     uint32_t k = 0;
     for (uint64_t i0 = 0; i0 < n; i0 += per, ++k) {
         const uint64_t i1 = i0 + per < n ? i0 + per : n;
-        st = launch_decode(&v, i0, i1, (uint8_t*)d_out + i0 * w, s);
-        if (st) return st;
-        cudaEventRecord(g_pipe.ev[k], s);
-        cudaStreamWaitEvent(g_pipe.copy, g_pipe.ev[k], 0);
+        const uint64_t c0 = i0 >> 10, c1 = (i1 + 1023) >> 10;  // chunks [c0, c1)
+        const uint64_t j0 = hint[c0], j1 = hint[c1 < H ? c1 : H];
+        // exactly the slices the span's kernel stages (FORMAT F2 sections, 16-byte rounded)
+        const uint64_t s_lo = (j0 & ~3ULL), s_hi = ((j1 + 2 + 3) & ~3ULL) < ((L + 1 + 3) & ~3ULL)
+                                                     ? ((j1 + 2 + 3) & ~3ULL)
+                                                     : ((L + 1 + 3) & ~3ULL);
+        const uint64_t w_lo = c0 * 32 * b, w_hi = (c1 * 32 * b + 4) < h.n_words ? c1 * 32 * b + 4
+                                                                                  : h.n_words;
+        if ((st = up_bytes(B, d_blob, h.off_hint + 4 * c0, h.off_hint + 4 * (c1 + 1), g_pipe.h2d)) ||
+            (st = up_bytes(B, d_blob, h.off_starts + 4 * s_lo, h.off_starts + 4 * s_hi, g_pipe.h2d)) ||
+            (st = up_bytes(B, d_blob, h.off_params + 16 * (j0 & ~3ULL), h.off_params + 16 * (j1 + 1),
+                           g_pipe.h2d)) ||
+            (b && (st = up_bytes(B, d_blob, h.off_words + 4 * w_lo, h.off_words + 4 * w_hi,
+                                 g_pipe.h2d))))
+            return st;
+        cudaEventRecord(g_pipe.up[k], g_pipe.h2d);
+        cudaStreamWaitEvent(s, g_pipe.up[k], 0);
+        if ((st = launch_decode(&v, i0, i1, (uint8_t*)d_out + i0 * w, s))) return st;
+        cudaEventRecord(g_pipe.dec[k], s);
+        cudaStreamWaitEvent(g_pipe.d2h, g_pipe.dec[k], 0);
         if (cudaMemcpyAsync((uint8_t*)h_out + i0 * w, (uint8_t*)d_out + i0 * w, (i1 - i0) * w,
-                            cudaMemcpyDeviceToHost, g_pipe.copy) != cudaSuccess)
+                            cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
             return LC_ERR_CUDA;
     }
-    cudaEventRecord(g_pipe.ev[16], g_pipe.copy);
-    cudaStreamWaitEvent(s, g_pipe.ev[16], 0);
+    cudaEventRecord(g_pipe.done, g_pipe.d2h);
+    cudaStreamWaitEvent(s, g_pipe.done, 0);
     return cuda_status();
 }
 
