@@ -95,7 +95,8 @@ int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
 int32_t lc_decode(const lc_view* v, void* d_out, lc_stream stream);
 
 /* Decode the key span [i0, i1) into d_out[0 .. i1-i0): the shard of a multi-GPU decode
- * (SURVEY §8(e)).  i0 must be a multiple of 1024; i1 <= n.  LC_ERR_ARG otherwise. */
+ * (SURVEY §8(e)).  i0 must be a multiple of 1024 (unless i0 == i1: an empty span is a no-op);
+ * i1 <= n.  LC_ERR_ARG otherwise. */
 int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out,
                        lc_stream stream);
 
@@ -124,8 +125,8 @@ int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, vo
 /* Human-readable name of a status code (static string). */
 const char* lc_status_str(int32_t status);
 
-/* Number of device kernels the previous calls on this thread have launched (monotone
- * counter; used by bench.py to report gpu_launches). */
+/* Number of device kernels launched by this library in this process so far (monotone,
+ * thread-safe counter; bench.py reports its delta over the timed region as gpu_launches). */
 uint64_t lc_launch_count(void);
 
 #ifdef __cplusplus

@@ -82,6 +82,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+// L2 cache policies for the gather kernels: the search structures (hint, starts: 0.4 + 30 MB
+// on config 5) stay resident (evict_last) while the one-touch params/words gathers are
+// marked evict_first, so the binary-search probes keep hitting L2.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t ldh(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ldh(const ulonglong2* p, uint64_t pol) {
+    ulonglong2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 // TMA bulk prefetch of [src, src + bytes) into L2 (no shared memory, no completion tracking)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -157,6 +183,9 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
     __syncwarp();  // every lane is done reading the previous contents
     pg.pj = from & ~3u;
     pg.cp = min(kSegCap, jlast + 1 - pg.pj);
+#ifdef LC_EXP_NO_STAGE  // experiment build only
+    return;
+#endif
     if (lane == 0) {
         const uint32_t cs = min(kSegCap + 4, jlast + 2 - pg.pj);
         const uint32_t sbytes = ((cs + 3) & ~3u) * 4, pbytes = pg.cp * 16;
@@ -225,6 +254,15 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
                                             uint32_t w2, uint32_t lane, uint32_t lmask,
                                             uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
     constexpr uint32_t kw = K64 ? 8 : 4;
+#ifdef LC_EXP_STORE_ONLY  // experiment build only: memory pattern without the decode math
+    put<K64>(outw, jb, lane);
+    put<K64>((uint8_t*)outw + 32 * kw, jb, lane);
+    return;
+#endif
+#ifdef LC_EXP_STAGE_ONLY  // experiment build only: staging reads, no decode, no stores
+    if (jb == 0xffffffffu) put<K64>(outw, jb, lane);
+    return;
+#endif
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
@@ -345,21 +383,22 @@ struct RangeArgs {
 };
 
 // j = max{t in [hint[i>>10], hint[(i>>10)+1]] : starts[t] <= i} (Table I caption)
-__device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i) {
-    uint32_t lo = __ldg(sec.hint + (i >> 10)), hi = __ldg(sec.hint + (i >> 10) + 1);
+__device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i, uint64_t keep) {
+    uint32_t lo = ldh(sec.hint + (i >> 10), keep), hi = ldh(sec.hint + (i >> 10) + 1, keep);
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(sec.starts + mid) <= i) lo = mid;
+        if (ldh(sec.starts + mid, keep) <= i) lo = mid;
         else hi = mid - 1;
     }
     return lo;
 }
 
 // residual field of key i read from global words (two loads + funnel shift)
-__device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b) {
+__device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b,
+                                             uint64_t pol) {
     const uint64_t bit = (uint64_t)i * b;
     const uint32_t* wp = sec.words + (bit >> 5);
-    return make_uint2(__ldg(wp), __ldg(wp + 1));
+    return make_uint2(ldh(wp, pol), ldh(wp + 1, pol));
 }
 __device__ __forceinline__ uint32_t field_of(uint2 w, uint32_t i, uint32_t b, uint32_t mask) {
     return __funnelshift_r(w.x, w.y, (i * b) & 31) & mask;
@@ -367,9 +406,9 @@ __device__ __forceinline__ uint32_t field_of(uint2 w, uint32_t i, uint32_t b, ui
 
 // One warp decodes 32 ranges.  Phase 1: lane r binary-searches the segment of range r's first
 // key (32 independent searches in flight).  Phase 2: the warp decodes the ranges one after
-// another with the window scheme of the full decode (64 keys per step, 2 keys per lane),
-// prefetching the next range's candidate starts and residual words so that each step waits
-// on a single dependent load (the params gather).
+// another with the window scheme of the full decode (64 keys per step, 2 keys per lane); the
+// next range's candidate starts and residual words are fetched while the current range is
+// decoded, so each range waits on a single dependent load (the params gather).
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
     constexpr uint32_t kw = K64 ? 8 : 4;
@@ -377,8 +416,9 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
     const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
-    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L;
+    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L, eps = a.eps;
     const uint32_t lmask = lanemask_le();
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
 
     // ---- phase 1: lane-parallel search
     uint32_t rs = 0, j = 0, sj = 0, ok = 0;
@@ -387,35 +427,34 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
         if (s64 <= a.n && len <= a.n - s64) {
             ok = 1;
             rs = (uint32_t)s64;
-            j = seg_search(sec, rs);
-            sj = __ldg(sec.starts + j);
+            j = seg_search(sec, rs, keep);
+            sj = ldh(sec.starts + j, keep);
         } else if (a.err) {
             atomicOr(a.err, 1u);
         }
     }
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
 
-    // prefetch for range k: candidate start and the first pair's words
-    auto prefetch = [&](uint32_t k, uint32_t& cand_s, uint2& wA, uint2& wB) {
+    // candidate starts and first-step residual words of range k
+    uint32_t nx;
+    uint2 nwA = make_uint2(0, 0), nwB = make_uint2(0, 0);
+    auto fetch = [&](uint32_t k) {
         const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
-        cand_s = __ldg(sec.starts + min(jk + 1 + lane, L));
+        nx = ldh(sec.starts + min(jk + 1 + lane, L), keep) - rk;
         if (b && len >= 64) {
-            wA = field_words(sec, rk + lane, b);
-            wB = field_words(sec, rk + 32 + lane, b);
+            nwA = field_words(sec, rk + lane, b, once);
+            nwB = field_words(sec, rk + 32 + lane, b, once);
         }
     };
-    uint32_t pc = 0;
-    uint2 pwA = make_uint2(0, 0), pwB = make_uint2(0, 0);
-    prefetch(0, pc, pwA, pwB);
-
+    fetch(0);
     for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t rk = __shfl_sync(kFull, rs, k);
         uint32_t jb = __shfl_sync(kFull, j, k);
         uint32_t sb = __shfl_sync(kFull, sj, k);
         const uint32_t okk = __shfl_sync(kFull, ok, k);
-        uint32_t cand_s = pc;
-        uint2 wA = pwA, wB = pwB;
-        if (k + 1 < nr) prefetch(k + 1, pc, pwA, pwB);
+        const uint32_t x = nx;
+        const uint2 wA = nwA, wB = nwB;
+        if (k + 1 < nr) fetch(k + 1);
         uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * len * kw;
         if (!okk) {
             for (uint32_t e = lane; e < len; e += 32) {
@@ -425,49 +464,43 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
             continue;
         }
         uint32_t w0 = 0;
-        bool first = true;
-        while (w0 < len) {
-            const uint32_t wb = rk + w0;
-            const uint32_t rem = len - w0;
-            if (!first) cand_s = __ldg(sec.starts + min(jb + 1 + lane, L));
-            const uint32_t x = cand_s - wb;
-            if (rem >= 64 && __ballot_sync(kFull, x < 64) != kFull) {
-                if (!first && b) {
-                    wA = field_words(sec, wb + lane, b);
-                    wB = field_words(sec, wb + 32 + lane, b);
-                }
-                const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
-                const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
-                const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
-                const uint32_t off0 = wb - sb;
-                const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
-                const uint32_t mA = PA & lmask, mB = PB & lmask;
-                const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
-                const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
-                const ulonglong2 pA = __ldg(sec.params + jb + __popc(mA));
-                const ulonglong2 pB = __ldg(sec.params + jb + __popc(PA) + __popc(mB));
-                const uint32_t uA = b ? field_of(wA, wb + lane, b, mask) : 0;
-                const uint32_t uB = b ? field_of(wB, wb + 32 + lane, b, mask) : 0;
-                put<K64>(outk + (w0 + lane) * kw, pA.x, pred_plus(pA.y, dA, uA - a.eps));
-                put<K64>(outk + (w0 + 32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - a.eps));
-                jb += adv;
-                sb = __ldg(sec.starts + jb);
-                w0 += 64;
-            } else {  // a single 32-key window (tail, or >= 32 boundaries in 64 keys)
-                const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x));
-                const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
-                const uint32_t m = P & lmask;
-                const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sb + lane;
-                if (lane < rem) {
-                    const ulonglong2 pr = __ldg(sec.params + jb + __popc(m));
-                    const uint32_t u = b ? field_of(field_words(sec, wb + lane, b), wb + lane, b, mask) : 0;
-                    put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - a.eps));
-                }
-                jb += adv;
-                sb = __ldg(sec.starts + min(jb, L));
-                w0 += 32;
+        // first 64 keys as one pair step, from the prefetched candidates and words
+        if (len >= 64 && __ballot_sync(kFull, x < 64) != kFull) {
+            const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
+            const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
+            const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
+            const uint32_t off0 = rk - sb;
+            const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
+            const uint32_t mA = PA & lmask, mB = PB & lmask;
+            const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+            const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+            const ulonglong2 pA = ldh(sec.params + jb + __popc(mA), once);
+            const ulonglong2 pB = ldh(sec.params + jb + __popc(PA) + __popc(mB), once);
+            const uint32_t uA = b ? field_of(wA, rk + lane, b, mask) : 0;
+            const uint32_t uB = b ? field_of(wB, rk + 32 + lane, b, mask) : 0;
+            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
+            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+            if (len == 64) continue;
+            jb += adv;
+            sb = ldh(sec.starts + min(jb, L), keep);
+            w0 = 64;
+        }
+        while (w0 < len) {  // remaining keys: 32-key windows through L1/L2
+            const uint32_t wb = rk + w0, rem = len - w0;
+            const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
+            const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(xw));
+            const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
+            const uint32_t m = P & lmask;
+            const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sb + lane;
+            if (lane < rem) {
+                const ulonglong2 pr = ldh(sec.params + jb + __popc(m), once);
+                const uint32_t u =
+                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
             }
-            first = false;
+            jb += adv;
+            sb = ldh(sec.starts + min(jb, L), keep);
+            w0 += 32;
         }
     }
 }
@@ -492,6 +525,7 @@ template <bool K64>
 __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
     const uint64_t t0 = (uint64_t)blockIdx.x * (256 * kAccessPerThread) + threadIdx.x;
     const Sections sec = a.sec;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
     uint32_t i[kAccessPerThread], lo[kAccessPerThread], hi[kAccessPerThread];
     bool live[kAccessPerThread];
     uint2 w[kAccessPerThread];
@@ -517,9 +551,9 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
 #pragma unroll
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {
         if (live[k]) {
-            lo[k] = __ldg(sec.hint + (i[k] >> 10));
-            hi[k] = __ldg(sec.hint + (i[k] >> 10) + 1);
-            if (a.b) w[k] = field_words(sec, i[k], a.b);
+            lo[k] = ldh(sec.hint + (i[k] >> 10), keep);
+            hi[k] = ldh(sec.hint + (i[k] >> 10) + 1, keep);
+            if (a.b) w[k] = field_words(sec, i[k], a.b, once);
         }
     }
     for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
@@ -530,7 +564,7 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
             mid[k] = (lo[k] + hi[k] + 1) >> 1;
             v[k] = 0;
             if (lo[k] < hi[k]) {
-                v[k] = __ldg(sec.starts + mid[k]);
+                v[k] = ldh(sec.starts + mid[k], keep);
                 any = true;
             }
         }
@@ -546,8 +580,8 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
 #pragma unroll
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {
         if (!live[k]) continue;
-        const uint32_t s = __ldg(sec.starts + lo[k]);
-        const ulonglong2 pr = __ldg(sec.params + lo[k]);
+        const uint32_t s = ldh(sec.starts + lo[k], keep);
+        const ulonglong2 pr = ldh(sec.params + lo[k], once);
         const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
         const uint64_t t = t0 + 256 * k;
         put<K64>((uint8_t*)a.out + t * (K64 ? 8 : 4), pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
@@ -663,8 +697,9 @@ extern "C" {
 
 int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, lc_stream stream) {
     if (!v || !v->d_blob) return LC_ERR_ARG;
-    if (i0 > i1 || i1 > v->h.n || (i0 & 1023)) return LC_ERR_ARG;
-    if (i0 == i1) return LC_OK;
+    if (i0 > i1 || i1 > v->h.n) return LC_ERR_ARG;
+    if (i0 == i1) return LC_OK;  // an empty span (e.g. a shard past the end) is a no-op
+    if (i0 & 1023) return LC_ERR_ARG;
     if (!d_out || ((uintptr_t)d_out & 15)) return LC_ERR_ARG;
     return launch_decode(v, i0, i1, d_out, (cudaStream_t)stream);
 }

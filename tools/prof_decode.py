@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--access", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="experiment builds (LC_LIB)")
     args = ap.parse_args()
     import torch
 
@@ -52,10 +53,24 @@ def main():
         gbs = (len(blob) + keys.size * keys.itemsize) / ms / 1e6
         print(f"decode rep {r}: {ms:.4f} ms  {gbs:.1f} GB/s", flush=True)
         if args.access:
+            ev[0].record()
             lc.access(view, d_idx, a_out)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms = ev[0].elapsed_time(ev[1])
+            print(f"access rep {r}: {ms:.4f} ms  {idx.size / ms / 1e6:.3e} lookups/s", flush=True)
+            ev[0].record()
             lc.range_decode(view, d_rs, 64, r_out)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms = ev[0].elapsed_time(ev[1])
+            print(f"range rep {r}: {ms:.4f} ms  {rs.size / ms / 1e6:.3e} ranges/s", flush=True)
     ref = torch.from_numpy(keys.view(np.int64) if keys.itemsize == 8 else keys.view(np.int32)).cuda()
-    assert torch.equal(out, ref), "decode mismatch"
+    assert args.no_check or torch.equal(out, ref), "decode mismatch"
+    if args.access and not args.no_check:
+        assert torch.equal(a_out, ref[d_idx]), "access mismatch"
+        sel = (d_rs[:, None] + torch.arange(64, device="cuda")[None, :]).reshape(-1)
+        assert torch.equal(r_out, ref[sel]), "range mismatch"
     print("ok", flush=True)
 
 
