@@ -81,7 +81,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self._nv:
@@ -343,6 +343,9 @@ def run_gpu(args):
         "hbm_frac": value / ws / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic(cid),
+                     "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes of one "
+                                       "ncu --set full launch; L2 keeps part of the output dirty "
+                                       "at kernel end)",
                      "kernel": "lc_decode_kernel<true>", "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": len(blob),
@@ -365,7 +368,7 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
