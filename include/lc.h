@@ -113,6 +113,17 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
                         void* d_out, uint32_t* d_err, lc_stream stream);
 
+/* Quantiles (§III-C, Table I): d_out[t] = the k_t-th q-quantile of the
+ * list, K[min(floor(N * k_t / q), N - 1)], for t < m (d_k: m uint64 ranks, 0 <= k_t <= q).
+ *   exact != 0: the exact key, f(i) + Delta[i] (one segment search + residual per quantile);
+ *   exact == 0: the segments-only approximation floor(f(i)) with no residual read; its error
+ *               is at most eps (approximate query processing); it saturates
+ *               at 2^key_bits - 1 when the prediction overshoots the key width.
+ * 1 <= q <= 2^32 - 1 (LC_ERR_ARG otherwise).  A rank k_t > q yields 0 and sets bit 0 of *d_err.
+ * m == 0 is a no-op. */
+int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t q, int32_t exact,
+                    void* d_out, uint32_t* d_err, lc_stream stream);
+
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
  * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out

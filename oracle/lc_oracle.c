@@ -391,6 +391,34 @@ int32_t oracle_access(const uint8_t* B, uint64_t bytes, const uint64_t* idx, uin
     return OR_OK;
 }
 
+/* Segments-only prediction floor(f(i)) = base_j + floor(slope_j (i - s_j) / 2^32) (Eq. 1;
+ * omitting the residuals gives approximate answers with error <= eps),
+ * saturated at the key width's maximum (reading L24).  Out-of-range i: out = 0 and
+ * *err |= 1. */
+int32_t oracle_predict(const uint8_t* B, uint64_t bytes, const uint64_t* idx, uint64_t q,
+                       void* out, uint32_t* err) {
+    or_hdr h;
+    int32_t st = or_read_hdr(B, bytes, &h);
+    if (st) return st;
+    uint32_t e = 0;
+    for (uint64_t t = 0; t < q; t++) {
+        uint64_t i = idx[t];
+        if (i >= h.n) {
+            put_key(out, h.key_bits, t, 0);
+            e |= 1u;
+            continue;
+        }
+        uint64_t j = seg_of(B, &h, i);
+        uint64_t s = rd32(B + h.o_starts + 4 * j);
+        uint64_t slope = rd64(B + h.o_params + 16 * j + 8);
+        u128 f = (u128)rd64(B + h.o_params + 16 * j) + (((u128)slope * (i - s)) >> 32);
+        u128 top = h.key_bits == 32 ? (u128)0xffffffffULL : (u128)0xffffffffffffffffULL;
+        put_key(out, h.key_bits, t, (uint64_t)(f > top ? top : f)); /* saturate (DESIGN L24) */
+    }
+    if (err) *err |= e;
+    return OR_OK;
+}
+
 /* Range decode: out[len*r + k] = K[start_r + k], k < len.  start_r + len > n: the range's
  * slots are 0 and *err |= 1. */
 int32_t oracle_range(const uint8_t* B, uint64_t bytes, const uint64_t* start, uint64_t q,

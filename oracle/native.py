@@ -52,6 +52,8 @@ def lib():
         L.oracle_decode_mt.restype = i32
         L.oracle_access.argtypes = [p, u64, p, u64, p, C.POINTER(u32)]
         L.oracle_access.restype = i32
+        L.oracle_predict.argtypes = [p, u64, p, u64, p, C.POINTER(u32)]
+        L.oracle_predict.restype = i32
         L.oracle_range.argtypes = [p, u64, p, u64, u32, p, C.POINTER(u32)]
         L.oracle_range.restype = i32
         L.oracle_validate.argtypes = [p, u64]
@@ -181,6 +183,24 @@ def access(blob: bytes, idx) -> tuple[np.ndarray, int]:
     if st != 0:
         raise OracleError(st, "access")
     return out, int(err.value)
+
+
+def predict(blob: bytes, idx) -> tuple[np.ndarray, int]:
+    """Segments-only prediction floor(f(i)) for each index (approximate quantiles)."""
+    h = header(blob)
+    ix = np.ascontiguousarray(idx, dtype=np.uint64)
+    out = np.empty(ix.size, _dtype(h))
+    err = C.c_uint32(0)
+    st = lib().oracle_predict(blob, len(blob), _ptr(ix) if ix.size else None, ix.size,
+                              _ptr(out) if out.size else None, C.byref(err))
+    if st != 0:
+        raise OracleError(st, "predict")
+    return out, int(err.value)
+
+
+def quantile_index(n: int, k: int, q: int) -> int:
+    """Index of the k-th q-quantile, min(floor(N k / q), N - 1)."""
+    return min((n * k) // q, n - 1)
 
 
 def range_decode(blob: bytes, starts, length: int) -> tuple[np.ndarray, int]:

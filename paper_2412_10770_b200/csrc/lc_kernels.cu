@@ -268,6 +268,18 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[cand - pg.pj] - wb;
     const uint32_t inside = __ballot_sync(kFull, x < 64);
+    if (inside == 0) {  // no boundary inside: all 64 keys in segment jb (sparse segments)
+        const ulonglong2 pr = pg.sP[jb - pg.pj];
+        const uint32_t off0 = wb - sb + lane;
+        put<K64>(outw, pr.x, pred_plus(pr.y, off0, field<B>(pg.sW, 2 * w2, lw, ls) - eps));
+        put<K64>((uint8_t*)outw + 32 * kw, pr.x,
+                 pred_plus(pr.y, off0 + 32, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps));
+        if (__ballot_sync(kFull, x == 64)) {  // a segment starts exactly at wb + 64
+            ++jb;
+            sb = wb + 64;
+        }
+        return;
+    }
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
         decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
                                            ls, eps, outw, 32);
@@ -588,6 +600,47 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
     }
 }
 
+// ----------------------------------------------------------------------------- quantiles
+struct QuantArgs {
+    Sections sec;
+    const uint64_t* k;
+    void* out;
+    uint32_t* err;
+    uint64_t m, q;
+    uint32_t n, b, eps, mask;
+};
+
+// The k-th q-quantile K[min(floor(N k / q), N - 1)] (§III-C; Table I): exact =
+// f(i) + Delta[i] through the hint bracket + binary search; approximate (EXACT = false) =
+// floor(f(i)) from the segment alone, no residual read, error <= eps.
+template <bool K64, bool EXACT>
+__global__ void __launch_bounds__(256) lc_quantile_kernel(const QuantArgs a) {
+    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (t >= a.m) return;
+    const Sections sec = a.sec;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    const uint64_t k = __ldg(a.k + t);
+    uint8_t* o = (uint8_t*)a.out + t * (K64 ? 8 : 4);
+    if (k > a.q) {
+        if (a.err) atomicOr(a.err, 1u);
+        put<K64>(o, 0, 0);
+        return;
+    }
+    const uint32_t i = (uint32_t)min((uint64_t)a.n * k / a.q, (uint64_t)a.n - 1);  // N k < 2^64
+    const uint32_t j = seg_search(sec, i, keep);
+    const uint32_t s = ldh(sec.starts + j, keep);
+    const ulonglong2 pr = ldh(sec.params + j, once);
+    if (EXACT) {
+        const uint32_t v = (a.b ? field_of(field_words(sec, i, a.b, once), i, a.b, a.mask) : 0) - a.eps;
+        put<K64>(o, pr.x, pred_plus(pr.y, i - s, v));
+    } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
+        const uint32_t t = pred_plus(pr.y, i - s, 0);
+        const uint64_t f = pr.x + t;
+        if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
+        else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
 uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
 
@@ -758,6 +811,38 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
         lc_range_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
     else
         lc_range_kernel<false><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    lc_detail::count_launch(1);
+    return cuda_status();
+}
+
+int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t q,
+                    int32_t exact, void* d_out, uint32_t* d_err, lc_stream stream) {
+    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (q == 0 || q > 0xffffffffULL) return LC_ERR_ARG;
+    if (m == 0) return LC_OK;
+    if (!d_k || !d_out) return LC_ERR_ARG;
+    QuantArgs a;
+    a.sec = sections_of(v);
+    a.k = d_k;
+    a.out = d_out;
+    a.err = d_err;
+    a.m = m;
+    a.q = q;
+    a.n = (uint32_t)v->h.n;
+    a.b = v->h.res_bits;
+    a.eps = v->h.eps;
+    a.mask = mask_of(a.b);
+    const uint64_t grid = (m + 255) / 256;
+    if (grid > 0x7fffffffULL) return LC_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool k64 = v->h.key_bits == 64;
+    if (exact) {
+        if (k64) lc_quantile_kernel<true, true><<<(unsigned)grid, 256, 0, st>>>(a);
+        else lc_quantile_kernel<false, true><<<(unsigned)grid, 256, 0, st>>>(a);
+    } else {
+        if (k64) lc_quantile_kernel<true, false><<<(unsigned)grid, 256, 0, st>>>(a);
+        else lc_quantile_kernel<false, false><<<(unsigned)grid, 256, 0, st>>>(a);
+    }
     lc_detail::count_launch(1);
     return cuda_status();
 }

@@ -52,6 +52,7 @@ _sig = {
     "lc_decode_span": ([C.POINTER(lc_view), _u64, _u64, _p, _p], _i32),
     "lc_access": ([C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_range_decode": ([C.POINTER(lc_view), _p, _u64, _u32, _p, _p, _p], _i32),
+    "lc_quantile": ([C.POINTER(lc_view), _p, _u64, _u64, _i32, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
@@ -201,6 +202,18 @@ def range_decode(view: View, starts, length: int, out=None, err=None, stream=Non
                                 err.data_ptr() if err is not None else None, _stream(stream)),
            "lc_range_decode")
     return out.view(q, length)
+
+
+def quantile(view: View, ranks, q: int, exact: bool = True, out=None, err=None, stream=None):
+    """lc_quantile: the ranks[t]-th q-quantiles (exact, or the segments-only approximation)."""
+    m = ranks.numel()
+    if out is None:
+        out = view.out_tensor(m)
+    _check(_lib.lc_quantile(C.byref(view.v), ranks.data_ptr() if m else None, m, q,
+                            1 if exact else 0, out.data_ptr() if m else None,
+                            err.data_ptr() if err is not None else None, _stream(stream)),
+           "lc_quantile")
+    return out
 
 
 def decode_host(h_blob, d_blob, d_out, h_out, stream=None) -> None:

@@ -252,3 +252,40 @@ def test_full_config5_access_range(lc):
     s_idx = idx[:5000]
     want, _ = orc.access(blob, s_idx)
     assert np.array_equal(_host(lc.access(view, _dev(s_idx)), np.uint64), want)
+
+
+# ------------------------------------------------------------------ NEXT-1: quantiles
+@pytest.mark.parametrize("cid,n", [(1, 300_000), (2, 1_000_003), (3, 500_000), (4, 700_001)])
+def test_quantiles(lc, cid, n):
+    keys = make_keys(cid, n)
+    eps = CONFIGS[cid].eps
+    blob = lc.encode(keys, eps)
+    view = lc.View(blob, device=DEV)
+    rng = np.random.default_rng(cid)
+    for q in (1, 2, 100, 1_000_003, (1 << 32) - 1):
+        ranks = np.unique(np.concatenate([rng.integers(0, q, 2000, endpoint=True), [0, q]]))
+        ranks = ranks.astype(np.uint64)
+        idx = np.array([orc.quantile_index(keys.size, int(k), q) for k in ranks], np.uint64)
+        ex = lc.quantile(view, _dev(ranks), q, exact=True)
+        ap = lc.quantile(view, _dev(ranks), q, exact=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(ex, keys.dtype), keys[idx.astype(np.int64)])
+        want_ap, err = orc.predict(blob, idx)
+        assert err == 0
+        got_ap = _host(ap, keys.dtype)
+        assert np.array_equal(got_ap, want_ap)
+        diff = got_ap.astype(np.int64) - keys[idx.astype(np.int64)].astype(np.int64)
+        assert np.abs(diff).max() <= eps
+
+
+def test_quantile_errors(lc):
+    keys = make_keys(5, 5000)
+    view = lc.View(lc.encode(keys, 127), device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    out = lc.quantile(view, _dev(np.array([0, 5, 11], np.uint64)), 10, err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1 and int(_host(out, np.uint64)[2]) == 0
+    with pytest.raises(lc.LcError):
+        lc.quantile(view, _dev(np.array([0], np.uint64)), 0)
+    with pytest.raises(lc.LcError):
+        lc.quantile(view, _dev(np.array([0], np.uint64)), 1 << 32)

@@ -374,3 +374,34 @@ def test_access_range_out_of_range():
     assert err == 1
     assert np.array_equal(got[0], keys[:64]) and np.array_equal(got[1], keys[2936:])
     assert not got[2].any()
+
+
+# ------------------------------------------------------------ NEXT-1: quantiles (AQP bound)
+@pytest.mark.parametrize("seed", range(6000, 6030))
+def test_predict_within_eps(seed):
+    """dropping the residuals leaves floor(f(i)) with |K[i] - floor(f(i))|
+    <= eps (the eps-PLA bound of Def. 2), checked at every index; the value is
+    also recomputed with exact rationals from the blob's segment (saturated at 2^w - 1)."""
+    keys, eps, kb, _ = fuzz_case(seed, n_max=5000)
+    blob = orc.encode(keys, eps, kb)
+    idx = np.arange(keys.size, dtype=np.uint64)
+    pred, err = orc.predict(blob, idx)
+    assert err == 0
+    diff = pred.astype(object) - keys.astype(object)
+    assert all(abs(int(d)) <= eps for d in diff)
+    bl = blobparse.parse(blob)
+    starts = [int(x) for x in bl.starts]
+    for i in np.random.default_rng(seed).integers(0, keys.size, 50):
+        j = int(np.searchsorted(bl.starts[:-1], i, side="right")) - 1
+        f = Fraction(int(bl.base[j])) + Fraction(int(bl.slope[j]), 1 << 32) * (int(i) - starts[j])
+        assert int(pred[i]) == min(math.floor(f), (1 << kb) - 1)  # saturated (DESIGN L24)
+
+
+def test_quantile_index_definition():
+    """The k-th q-quantile of a sorted list is K[floor(N k / q)], clipped to N-1
+    for k = q; the median of an odd list is its middle element."""
+    keys = np.arange(0, 1001, dtype=np.uint64) * np.uint64(3)
+    assert int(keys[orc.quantile_index(keys.size, 1, 2)]) == 1500  # median of 0, 3, ..., 3000
+    assert orc.quantile_index(keys.size, 0, 4) == 0
+    assert orc.quantile_index(keys.size, 4, 4) == keys.size - 1
+    assert orc.quantile_index(10, 1, 4) == 2
