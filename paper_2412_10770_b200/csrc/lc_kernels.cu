@@ -268,18 +268,6 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[cand - pg.pj] - wb;
     const uint32_t inside = __ballot_sync(kFull, x < 64);
-    if (inside == 0) {  // no boundary inside: all 64 keys in segment jb (sparse segments)
-        const ulonglong2 pr = pg.sP[jb - pg.pj];
-        const uint32_t off0 = wb - sb + lane;
-        put<K64>(outw, pr.x, pred_plus(pr.y, off0, field<B>(pg.sW, 2 * w2, lw, ls) - eps));
-        put<K64>((uint8_t*)outw + 32 * kw, pr.x,
-                 pred_plus(pr.y, off0 + 32, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps));
-        if (__ballot_sync(kFull, x == 64)) {  // a segment starts exactly at wb + 64
-            ++jb;
-            sb = wb + 64;
-        }
-        return;
-    }
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
         decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
                                            ls, eps, outw, 32);
