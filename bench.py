@@ -307,9 +307,46 @@ def run_gpu(args):
         sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
         ok_r = torch.equal(r_out, d5[sel])
         del d5, sel
+        # NEXT-1 quantiles and NEXT-2 successor search / intersection on the same list
+        qrng = np.random.default_rng(55)
+        mq = 10_000_000
+        d_ranks = torch.from_numpy(qrng.integers(0, (1 << 32) - 1, mq, endpoint=True)
+                                   .astype(np.uint64).view(np.int64)).to(dev)
+        q_out = torch.empty(mq, dtype=torch.int64, device=dev)
+        d_probe = torch.from_numpy(qrng.integers(0, int(k5[-1]), mq, dtype=np.uint64)
+                                   .view(np.int64)).to(dev)
+        p_idx = torch.empty(mq, dtype=torch.int64, device=dev)
+        p_key = torch.empty(mq, dtype=torch.int64, device=dev)
+        na = 1_000_000
+        a_keys = np.unique(np.concatenate([
+            k5[np.sort(qrng.choice(k5.size, na // 2, replace=False))],
+            qrng.integers(0, int(k5[-1]), na // 2, dtype=np.uint64)]))
+        va = lc.View(lc.encode(a_keys, 127), device=dev)
+        i_scr = torch.empty(lc.intersect_scratch_bytes(va), dtype=torch.uint8, device=dev)
+        i_out = va.out_tensor(va.n)
+        i_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        reps = max(3, min(args.steps, 20))
+        with torch.cuda.stream(stream):
+            _, pqe = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, True, q_out,
+                                                        stream=stream), stream, reps, 2)
+            _, pqa = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, False, q_out,
+                                                        stream=stream), stream, reps, 2)
+            _, png = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx, p_key, stream=stream),
+                                    stream, reps, 2)
+            _, pis = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt,
+                                                         stream=stream), stream, reps, 2)
+        want_cnt = int(np.intersect1d(a_keys, k5, assume_unique=True).size)
+        if int(i_cnt.item()) != want_cnt:
+            raise SystemExit("intersection count mismatch")
         access = {
             "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
                         "lookups; 1e7 ranges x 64 keys",
+            "quantiles_exact_per_s": mq / statistics.mean(pqe),
+            "quantiles_approx_per_s": mq / statistics.mean(pqa),
+            "next_geq_per_s": mq / statistics.mean(png),
+            "intersect": {"a_keys": int(a_keys.size), "b_keys": int(k5.size),
+                          "matches": want_cnt, "ms": statistics.mean(pis) * 1e3,
+                          "a_keys_per_s": a_keys.size / statistics.mean(pis)},
             "lookups_per_s": ws * idx.size / statistics.mean(pa),
             "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
             "ranges_per_s": ws * rs.size / statistics.mean(pr),
@@ -320,7 +357,7 @@ def run_gpu(args):
         }
         if not (ok_a and ok_r):
             raise SystemExit("access/range mismatch")
-        del v5, d_idx, a_out, d_rs, r_out
+        del v5, d_idx, a_out, d_rs, r_out, va, i_scr, i_out, d_ranks, q_out, d_probe, p_idx, p_key
 
     if ws > 1:
         dist.barrier()

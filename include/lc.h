@@ -124,6 +124,27 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
 int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t q, int32_t exact,
                     void* d_out, uint32_t* d_err, lc_stream stream);
 
+/* Successor search (NEXT-2; segments as skip pointers, Fig. 4b): for t < m,
+ * d_out_idx[t] = min{i : K[i] >= x_t} (n if none) and d_out_key[t] = that key (0 if none).
+ * d_x: m uint64 probe keys (for a 32-bit list a probe >= 2^32 is past every key).  Either
+ * output pointer may be NULL (not both).  m == 0 is a no-op.  Uses the anchor invariant
+ * base_j = K[s_j] (FORMAT F2): binary search over the segment bases, then inside one segment. */
+int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,
+                    void* d_out_key, lc_stream stream);
+
+/* Device scratch bytes lc_intersect needs for list a (its decoded keys, a match bitmap and
+ * per-CTA offsets). */
+uint64_t lc_intersect_scratch_bytes(const lc_view* a);
+
+/* Intersection of two compressed lists, the AND query of inverted-index processing
+ * (§III-A): d_out receives the sorted keys present in both lists and
+ * *d_count (device uint64) their number.  a is decoded into d_scratch (>=
+ * lc_intersect_scratch_bytes(a) bytes, 256-byte aligned) and each of its keys is searched in b
+ * with next_geq, so segments of b that hold none of a's keys are never read: pass the shorter
+ * list as a.  d_out capacity: a->h.n keys.  Both lists must have the same key_bits. */
+int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
+                     void* d_out, uint64_t* d_count, lc_stream stream);
+
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
  * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out

@@ -629,6 +629,183 @@ __global__ void __launch_bounds__(256) lc_quantile_kernel(const QuantArgs a) {
     }
 }
 
+// ------------------------------------------------------ successor search and intersection
+// Key-space search uses the segments as skip pointers (Fig. 4b): with the
+// FORMAT F2 anchor, base_j = K[s_j] and the bases are strictly increasing, so segment j covers
+// exactly the keys [base_j, base_{j+1}).  next_geq(x) = binary search over the bases, then a
+// binary search inside the one segment, decoding only the probed keys (never a whole segment).
+__device__ __forceinline__ uint64_t key_at(const Sections& sec, uint32_t i, uint32_t s,
+                                           ulonglong2 pr, uint32_t b, uint32_t mask, uint32_t eps,
+                                           uint64_t once) {
+    const uint32_t u = b ? field_of(field_words(sec, i, b, once), i, b, mask) : 0;
+    return pr.x + pred_plus(pr.y, i - s, u - eps);
+}
+
+struct SuccResult {
+    uint32_t idx;  // first index with K[idx] >= x, n if none
+    uint64_t key;  // K[idx], 0 if none
+};
+
+__device__ SuccResult next_geq_one(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
+                                   uint32_t mask, uint32_t eps, uint64_t x, uint64_t keep,
+                                   uint64_t once) {
+    const uint64_t* bases = (const uint64_t*)sec.params;  // base_j at bases[2 j]
+    const uint64_t b0 = __ldg(bases);
+    if (x <= b0) return {0u, b0};
+    uint32_t lo = 0, hi = L - 1;  // max{j : base_j <= x}
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(bases + 2 * (size_t)mid) <= x) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint32_t j = lo;
+    const uint32_t s = ldh(sec.starts + j, keep), e = ldh(sec.starts + j + 1, keep);
+    const ulonglong2 pr = ldh(sec.params + j, once);
+    uint32_t l = s + 1, r = e;  // K[s] = base_j <= x; answer in (s, e]
+    if (pr.x == x) return {s, x};
+    uint64_t kr = 0;
+    bool have = false;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        const uint64_t km = key_at(sec, mid, s, pr, b, mask, eps, once);
+        if (km >= x) {
+            r = mid;
+            kr = km;
+            have = true;
+        } else {
+            l = mid + 1;
+        }
+    }
+    if (l < e) {
+        if (!have || r != l) kr = key_at(sec, l, s, pr, b, mask, eps, once);
+        return {l, kr};
+    }
+    if (e >= n) return {n, 0};
+    return {e, __ldg(bases + 2 * (size_t)(j + 1))};  // K[e] = base_{j+1} > x
+}
+
+struct SuccArgs {
+    Sections sec;
+    const uint64_t* x;
+    uint64_t* out_idx;
+    void* out_key;
+    uint64_t m;
+    uint32_t n, L, b, eps, mask;
+};
+
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
+    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (t >= a.m) return;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    const uint64_t x = __ldg(a.x + t);
+    SuccResult r;
+    if (!K64 && x > 0xffffffffull) r = {a.n, 0};
+    else r = next_geq_one(a.sec, a.n, a.L, a.b, a.mask, a.eps, x, keep, once);
+    if (a.out_idx) a.out_idx[t] = r.idx;
+    if (a.out_key) put<K64>((uint8_t*)a.out_key + t * (K64 ? 8 : 4), r.key, 0);
+}
+
+// Intersection A ∩ B (AND query): A is decoded into scratch, each key of A is looked up in B
+// with next_geq (segments of B holding no key of A are never touched), matches are flagged
+// with warp ballots and compacted in order (per-CTA counts, one-CTA scan, scatter).
+struct IsectArgs {
+    Sections sb;            // list B (searched)
+    const void* a_keys;     // decoded list A
+    uint32_t* flags;        // ceil(na / 32) match bitmap
+    uint32_t* counts;       // per-CTA match counts, then exclusive offsets; [nblk] = total
+    void* out;
+    uint64_t* d_count;
+    uint32_t na, nb, Lb, b, eps, mask, nblk;
+};
+
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
+    __shared__ uint32_t warp_cnt[8];
+    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    bool hit = false;
+    if (t < a.na) {
+        const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
+        const SuccResult r = next_geq_one(a.sb, a.nb, a.Lb, a.b, a.mask, a.eps, x, keep, once);
+        hit = r.idx < a.nb && r.key == x;
+    }
+    const uint32_t bal = __ballot_sync(kFull, hit);
+    if (lane == 0) {
+        if (t < a.na) a.flags[t >> 5] = bal;
+        warp_cnt[warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (int w = 0; w < 8; ++w) c += warp_cnt[w];
+        a.counts[blockIdx.x] = c;
+    }
+}
+
+// exclusive scan of the per-CTA counts in one CTA of 1024 threads; counts[nblk] = total
+__global__ void __launch_bounds__(1024) lc_isect_scan_kernel(const IsectArgs a) {
+    __shared__ uint32_t part[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t base = 0; base < a.nblk; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < a.nblk ? a.counts[i] : 0;
+        uint32_t x = v;  // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) part[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t p = part[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, p, o);
+                if (lane >= (uint32_t)o) p += y;
+            }
+            part[lane] = p;  // inclusive over warps
+        }
+        __syncthreads();
+        const uint32_t excl = carry + (warp ? part[warp - 1] : 0) + x - v;
+        if (i < a.nblk) a.counts[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.counts[a.nblk] = carry;
+        *a.d_count = carry;
+    }
+}
+
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) {
+    __shared__ uint32_t warp_off[8];
+    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t bal = t < a.na ? a.flags[t >> 5] : 0;  // whole warp reads the same word
+    if (lane == 0) warp_off[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = a.counts[blockIdx.x];
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t v = warp_off[w];
+            warp_off[w] = c;
+            c += v;
+        }
+    }
+    __syncthreads();
+    if ((bal >> lane) & 1) {
+        const uint32_t pos = warp_off[warp] + __popc(bal & ((1u << lane) - 1));
+        if (K64) ((uint64_t*)a.out)[pos] = ((const uint64_t*)a.a_keys)[t];
+        else ((uint32_t*)a.out)[pos] = ((const uint32_t*)a.a_keys)[t];
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
 uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
 
@@ -832,6 +1009,72 @@ int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t 
         else lc_quantile_kernel<false, false><<<(unsigned)grid, 256, 0, st>>>(a);
     }
     lc_detail::count_launch(1);
+    return cuda_status();
+}
+
+int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,
+                    void* d_out_key, lc_stream stream) {
+    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (m == 0) return LC_OK;
+    if (!d_x || (!d_out_idx && !d_out_key)) return LC_ERR_ARG;
+    SuccArgs a;
+    a.sec = sections_of(v);
+    a.x = d_x;
+    a.out_idx = d_out_idx;
+    a.out_key = d_out_key;
+    a.m = m;
+    a.n = (uint32_t)v->h.n;
+    a.L = (uint32_t)v->h.n_seg;
+    a.b = v->h.res_bits;
+    a.eps = v->h.eps;
+    a.mask = mask_of(a.b);
+    const uint64_t grid = (m + 255) / 256;
+    if (grid > 0x7fffffffULL) return LC_ERR_ARG;
+    if (v->h.key_bits == 64) lc_next_geq_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    else lc_next_geq_kernel<false><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    lc_detail::count_launch(1);
+    return cuda_status();
+}
+
+uint64_t lc_intersect_scratch_bytes(const lc_view* a) {
+    if (!a) return 0;
+    const uint64_t na = a->h.n, kw = a->h.key_bits / 8;
+    const uint64_t nblk = (na + 255) / 256;
+    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
+    return r256(na * kw) + r256(4 * ((na + 31) / 32)) + r256(4 * (nblk + 1));
+}
+
+int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
+                     void* d_out, uint64_t* d_count, lc_stream stream) {
+    if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
+    if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
+    if (scratch_bytes < lc_intersect_scratch_bytes(a) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
+    const uint64_t na = a->h.n, kw = a->h.key_bits / 8;
+    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
+    uint8_t* sc = (uint8_t*)d_scratch;
+    IsectArgs g;
+    g.sb = sections_of(b);
+    g.a_keys = sc;
+    g.flags = (uint32_t*)(sc + r256(na * kw));
+    g.counts = (uint32_t*)(sc + r256(na * kw) + r256(4 * ((na + 31) / 32)));
+    g.out = d_out;
+    g.d_count = d_count;
+    g.na = (uint32_t)na;
+    g.nb = (uint32_t)b->h.n;
+    g.Lb = (uint32_t)b->h.n_seg;
+    g.b = b->h.res_bits;
+    g.eps = b->h.eps;
+    g.mask = mask_of(g.b);
+    g.nblk = (uint32_t)((na + 255) / 256);
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t rc = launch_decode(a, 0, na, sc, st);
+    if (rc) return rc;
+    if (kw == 8) lc_isect_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g);
+    else lc_isect_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g);
+    lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
+    if (kw == 8) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
+    else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
+    lc_detail::count_launch(3);
     return cuda_status();
 }
 

@@ -53,6 +53,9 @@ _sig = {
     "lc_access": ([C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_range_decode": ([C.POINTER(lc_view), _p, _u64, _u32, _p, _p, _p], _i32),
     "lc_quantile": ([C.POINTER(lc_view), _p, _u64, _u64, _i32, _p, _p, _p], _i32),
+    "lc_next_geq": ([C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
+    "lc_intersect_scratch_bytes": ([C.POINTER(lc_view)], _u64),
+    "lc_intersect": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
@@ -214,6 +217,42 @@ def quantile(view: View, ranks, q: int, exact: bool = True, out=None, err=None, 
                             err.data_ptr() if err is not None else None, _stream(stream)),
            "lc_quantile")
     return out
+
+
+def next_geq(view: View, x, out_idx=None, out_key=None, stream=None):
+    """lc_next_geq: (first index with K[i] >= x_t, that key) for a device int64 tensor of probes."""
+    import torch
+    m = x.numel()
+    if out_idx is None:
+        out_idx = torch.empty(m, dtype=torch.int64, device=x.device)
+    if out_key is None:
+        out_key = view.out_tensor(m)
+    _check(_lib.lc_next_geq(C.byref(view.v), x.data_ptr() if m else None, m,
+                            out_idx.data_ptr() if m else None, out_key.data_ptr() if m else None,
+                            _stream(stream)), "lc_next_geq")
+    return out_idx, out_key
+
+
+def intersect_scratch_bytes(a: View) -> int:
+    return int(_lib.lc_intersect_scratch_bytes(C.byref(a.v)))
+
+
+def intersect(a: View, b: View, scratch=None, out=None, count=None, stream=None):
+    """lc_intersect: keys in both lists (pass the shorter list as `a`).  Returns (out, count)
+    where out[:count] holds the intersection (count is a device tensor)."""
+    import torch
+    dev = a.d_blob.device
+    need = int(_lib.lc_intersect_scratch_bytes(C.byref(a.v)))
+    if scratch is None:
+        scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+    if out is None:
+        out = a.out_tensor(a.n)
+    if count is None:
+        count = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.lc_intersect(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
+                             scratch.numel() * scratch.element_size(), out.data_ptr(),
+                             count.data_ptr(), _stream(stream)), "lc_intersect")
+    return out, count
 
 
 def decode_host(h_blob, d_blob, d_out, h_out, stream=None) -> None:

@@ -289,3 +289,81 @@ def test_quantile_errors(lc):
         lc.quantile(view, _dev(np.array([0], np.uint64)), 0)
     with pytest.raises(lc.LcError):
         lc.quantile(view, _dev(np.array([0], np.uint64)), 1 << 32)
+
+
+# ------------------------------------------------ NEXT-2: successor search and intersection
+from oracle import setops  # noqa: E402
+
+
+def _probes(keys, rng, m):
+    k = keys.astype(np.uint64)
+    hits = k[rng.integers(0, k.size, m // 2)]
+    lo, hi = int(k[0]), int(k[-1])
+    top = (1 << 32) - 1 if keys.dtype == np.uint32 else (1 << 64) - 1
+    a, b = max(lo - 10, 0), min(hi + 10, top)
+    between = rng.integers(a, max(b, a + 1), m - m // 2, dtype=np.uint64, endpoint=True)
+    return np.concatenate([hits, between, np.array([0, lo, hi, (1 << 64) - 1], np.uint64)])
+
+
+@pytest.mark.parametrize("cid,n", [(1, 200_000), (2, 500_000), (3, 400_000), (4, 300_000), (5, 300_000)])
+def test_next_geq(lc, cid, n):
+    keys = make_keys(cid, n)
+    view = lc.View(lc.encode(keys, CONFIGS[cid].eps), device=DEV)
+    x = _probes(keys, np.random.default_rng(cid), 20_000)
+    idx, key = lc.next_geq(view, _dev(x))
+    torch.cuda.synchronize()
+    want_i, want_k = setops.next_geq(keys, x)
+    assert np.array_equal(_host(idx, np.uint64), want_i)
+    assert np.array_equal(_host(key, keys.dtype), want_k)
+
+
+@pytest.mark.parametrize("seed", range(3000, 3040))
+def test_next_geq_fuzz(lc, seed):
+    keys, eps, kb, law = fuzz_case(seed, n_max=50_000)
+    view = lc.View(lc.encode(keys, eps, kb), device=DEV)
+    x = _probes(keys, np.random.default_rng(seed), 2000)
+    idx, key = lc.next_geq(view, _dev(x))
+    torch.cuda.synchronize()
+    want_i, want_k = setops.next_geq(keys, x)
+    assert np.array_equal(_host(idx, np.uint64), want_i), (seed, law)
+    assert np.array_equal(_host(key, keys.dtype), want_k), (seed, law)
+
+
+def _isect_case(lc, a, b, eps_a, eps_b):
+    va = lc.View(lc.encode(a, eps_a), device=DEV)
+    vb = lc.View(lc.encode(b, eps_b), device=DEV)
+    out, cnt = lc.intersect(va, vb)
+    torch.cuda.synchronize()
+    c = int(cnt.item())
+    want = setops.intersect(a, b)
+    assert c == want.size
+    assert np.array_equal(_host(out[:c], a.dtype), want)
+
+
+@pytest.mark.parametrize("na", [1, 1000, 33_333, 300_000])
+def test_intersect_subset_plus_noise(lc, na):
+    b = make_keys(2, 1_000_000)
+    rng = np.random.default_rng(na)
+    pick = b[np.sort(rng.choice(b.size, na // 2 + 1, replace=False))]
+    noise = rng.integers(0, int(b[-1]) + 1000, na, dtype=np.uint64)
+    a = np.unique(np.concatenate([pick, noise]))[:na]
+    _isect_case(lc, a, b, 63, 127)
+
+
+def test_intersect_closed_form_and_edges(lc):
+    M = 3_000_000
+    a = np.arange(0, M, 6, dtype=np.uint64)
+    b = np.arange(0, M, 10, dtype=np.uint64)
+    _isect_case(lc, a, b, 0, 31)                     # multiples of 30
+    _isect_case(lc, b, b, 127, 127)                  # identical lists
+    _isect_case(lc, a + np.uint64(1), a, 7, 7)       # disjoint
+    a32 = np.arange(5, 2_000_000, 3, dtype=np.uint32)
+    b32 = make_keys(1, 1_000_000)
+    _isect_case(lc, a32, b32, 15, 63)                # u32 lists, a longer than b
+
+
+def test_intersect_key_width_mismatch(lc):
+    va = lc.View(lc.encode(np.arange(10, dtype=np.uint32), 1), device=DEV)
+    vb = lc.View(lc.encode(np.arange(10, dtype=np.uint64), 1), device=DEV)
+    with pytest.raises(lc.LcError):
+        lc.intersect(va, vb)

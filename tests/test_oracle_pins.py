@@ -405,3 +405,38 @@ def test_quantile_index_definition():
     assert orc.quantile_index(keys.size, 0, 4) == 0
     assert orc.quantile_index(keys.size, 4, 4) == keys.size - 1
     assert orc.quantile_index(10, 1, 4) == 2
+
+
+# ------------------------------------------------- NEXT-2: successor search and intersection
+from oracle import setops  # noqa: E402
+
+
+def test_setops_bruteforce_tiny():
+    """next_geq and intersect against Python loops over tiny lists (the definitions by hand)."""
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        a = np.unique(rng.integers(0, 300, rng.integers(1, 40))).astype(np.uint64)
+        b = np.unique(rng.integers(0, 300, rng.integers(1, 40))).astype(np.uint64)
+        xs = rng.integers(0, 320, 30).astype(np.uint64)
+        idx, key = setops.next_geq(a, xs)
+        for x, i, k in zip(xs, idx, key):
+            want = next((t for t, v in enumerate(a) if v >= x), len(a))
+            assert int(i) == want
+            assert int(k) == (int(a[want]) if want < len(a) else 0)
+        assert setops.intersect(a, b).tolist() == sorted(set(a.tolist()) & set(b.tolist()))
+
+
+def test_intersect_lcm_closed_form():
+    """Multiples of p below M intersect multiples of q in exactly the multiples of lcm(p, q)."""
+    for p, q in [(6, 10), (7, 13), (12, 18), (1, 5)]:
+        M = 100_000
+        a = np.arange(0, M, p, dtype=np.uint64)
+        b = np.arange(0, M, q, dtype=np.uint64)
+        l = p * q // math.gcd(p, q)
+        assert np.array_equal(setops.intersect(a, b), np.arange(0, M, l, dtype=np.uint64))
+
+
+def test_next_geq_u32_probe_above_range():
+    a = np.array([1, 5, 0xFFFFFFFF], np.uint32)
+    idx, key = setops.next_geq(a, np.array([0, 5, 6, 0xFFFFFFFF, 1 << 32], np.uint64))
+    assert idx.tolist() == [0, 1, 2, 2, 3] and key.tolist() == [1, 5, 0xFFFFFFFF, 0xFFFFFFFF, 0]
