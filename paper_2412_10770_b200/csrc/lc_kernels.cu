@@ -380,6 +380,7 @@ struct RangeArgs {
     uint32_t* err;
     uint64_t q;
     uint32_t len, n, L, b, eps, mask;
+    uint32_t nwords;  // W
 };
 
 // j = max{t in [hint[i>>10], hint[(i>>10)+1]] : starts[t] <= i} (Table I caption)
@@ -503,6 +504,152 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
             w0 += 32;
         }
     }
+}
+
+// ---------------------------------------------------------------- range decode, len == 64
+// cp.async (LDGSTS) 16-byte copy with zero fill when `valid` is false
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+constexpr uint32_t kR64Segs = 12;   // params staged per range (>= 1 + boundaries in 64 keys)
+#ifndef LC_R64_SLOTS
+#define LC_R64_SLOTS 4
+#endif
+constexpr uint32_t kR64Slots = LC_R64_SLOTS;  // ring depth per warp (ranges gathered ahead)
+__host__ __device__ constexpr uint32_t r64_words(uint32_t b) {  // staged residual words
+    return ((((64 * b + 31) >> 5) + 2 + 3) + 3) & ~3u;
+}
+__host__ __device__ constexpr uint32_t r64_bytes(uint32_t b) {  // per slot: params|starts|words
+    return 16 * kR64Segs + 4 * 20 + 4 * r64_words(b);
+}
+
+// 64-key ranges (BASELINE config 5).  Phase 1: lane r binary-searches range r's first segment
+// (32 independent searches).  Phase 2: the warp walks its 32 ranges through a 4-slot shared-
+// memory ring: the lanes gather range k+3's params[j..j+12), starts[j+1..j+17) and residual
+// words with cp.async (one or two 16-byte copies per lane) while range k is decoded from smem
+// with the pair-window scheme, so the decode never waits on a dependent global load.  A range
+// crossing more than 11 segment starts is decoded through L2 instead.
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
+    if (r0 >= a.q) return;  // warp-uniform
+    const Sections sec = a.sec;
+    const uint32_t b = a.b, mask = a.mask, L = a.L, eps = a.eps;
+    const uint32_t RB = r64_bytes(b), nw16 = r64_words(b) / 4;
+    uint8_t* ring = smem + warp * kR64Slots * RB;
+    const uint32_t lmask = lanemask_le();
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+
+    // ---- phase 1: lane-parallel search
+    uint32_t rs = 0, j = 0, sj = 0, ok = 0;
+    if (r0 + lane < a.q) {
+        const uint64_t s64 = __ldg(a.start + r0 + lane);
+        if (s64 <= a.n && 64 <= a.n - s64) {
+            ok = 1;
+            rs = (uint32_t)s64;
+            j = seg_search(sec, rs, keep);
+            sj = ldh(sec.starts + j, keep);
+        } else if (a.err) {
+            atomicOr(a.err, 1u);
+        }
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+
+    // gather range k into ring slot k % kR64Slots: groups 0..11 params, 12..16 starts, then words
+    const uint32_t ngroups = kR64Segs + 5 + nw16;
+    auto issue = [&](uint32_t k) {
+        if (k < nr) {
+            const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
+            const uint32_t okk = __shfl_sync(kFull, ok, k);
+            uint8_t* slot = ring + (k % kR64Slots) * RB;
+            if (okk) {
+                const uint32_t s0 = (jk + 1) & ~3u;
+                const uint32_t w0 = (uint32_t)(((uint64_t)rk * b) >> 5) & ~3u;
+                for (uint32_t g = lane; g < ngroups; g += 32) {
+                    if (g < kR64Segs) {
+                        cp16(slot + 16 * g, sec.params + jk + g, jk + g < L);
+                    } else if (g < kR64Segs + 5) {
+                        const uint32_t t = g - kR64Segs;
+                        cp16(slot + 16 * kR64Segs + 16 * t, sec.starts + s0 + 4 * t, true);
+                    } else {
+                        const uint32_t t = g - kR64Segs - 5;
+                        cp16(slot + 16 * kR64Segs + 80 + 16 * t, sec.words + w0 + 4 * t,
+                             w0 + 4 * t + 4 <= a.nwords);
+                    }
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
+    };
+    for (uint32_t k = 0; k + 1 < kR64Slots; ++k) issue(k);
+
+    for (uint32_t k = 0; k < nr; ++k) {
+        issue(k + kR64Slots - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kR64Slots - 1) : "memory");
+        __syncwarp();
+        const uint32_t rk = __shfl_sync(kFull, rs, k);
+        const uint32_t jk = __shfl_sync(kFull, j, k);
+        const uint32_t sb = __shfl_sync(kFull, sj, k);
+        const uint32_t okk = __shfl_sync(kFull, ok, k);
+        uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * 64 * kw;
+        if (!okk) {
+            put<K64>(outk + lane * kw, 0, 0);
+            put<K64>(outk + (32 + lane) * kw, 0, 0);
+            __syncwarp();
+            continue;
+        }
+        const uint8_t* rsm = ring + (k % kR64Slots) * RB;
+        const ulonglong2* P = (const ulonglong2*)rsm;
+        const uint32_t* S = (const uint32_t*)(rsm + 16 * kR64Segs) + ((jk + 1) & 3);  // starts[jk+1+t]
+        const uint32_t x = (lane < 16 && jk + 1 + lane <= L) ? S[lane] - rk : kFull;
+        const uint32_t inside = __ballot_sync(kFull, x < 64);
+        if (__popc(inside) < kR64Segs) {
+            const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
+            const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
+            const uint32_t off0 = rk - sb;
+            const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
+            const uint32_t mA = PA & lmask, mB = PB & lmask;
+            const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+            const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+            const ulonglong2 pA = P[__popc(mA)];
+            const ulonglong2 pB = P[__popc(PA) + __popc(mB)];
+            uint32_t uA = 0, uB = 0;
+            if (b) {
+                const uint32_t* Wd = (const uint32_t*)(rsm + 16 * kR64Segs + 80);
+                const uint64_t wbase = ((((uint64_t)rk * b) >> 5) & ~3ull) << 5;
+                const uint32_t bA = (uint32_t)((uint64_t)(rk + lane) * b - wbase);
+                const uint32_t bB = bA + 32 * b;
+                uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
+                uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
+            }
+            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
+            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+        } else {  // dense range: two 32-key windows through L2
+            uint32_t jb = jk, sbw = sb;
+            for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
+                const uint32_t wb = rk + w0;
+                const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
+                const uint32_t Pm = __reduce_or_sync(kFull, bit_or_zero(xw));
+                const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
+                const uint32_t m = Pm & lmask;
+                const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
+                const ulonglong2 pr = ldh(sec.params + jb + __popc(m), once);
+                const uint32_t u =
+                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
+                jb += adv;
+                sbw = ldh(sec.starts + min(jb, L), keep);
+            }
+        }
+        __syncwarp();  // the slot is refilled by the next issue()
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------- random access
@@ -970,12 +1117,24 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     a.b = v->h.res_bits;
     a.eps = v->h.eps;
     a.mask = mask_of(a.b);
+    a.nwords = (uint32_t)v->h.n_words;
     const uint64_t grid = (q + 255) / 256;  // 8 warps x 32 ranges per CTA
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
-    if (v->h.key_bits == 64)
-        lc_range_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
-    else
-        lc_range_kernel<false><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    const bool k64 = v->h.key_bits == 64;
+    cudaStream_t st = (cudaStream_t)stream;
+#ifndef LC_EXP_NO_RANGE64
+    if (len == 64) {  // the config-5 shape: cp.async ring kernel
+        const uint32_t smem = 8 * kR64Slots * r64_bytes(a.b);
+        const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (k64) lc_range64_kernel<true><<<(unsigned)grid, 256, smem, st>>>(a);
+        else lc_range64_kernel<false><<<(unsigned)grid, 256, smem, st>>>(a);
+        lc_detail::count_launch(1);
+        return cuda_status();
+    }
+#endif
+    if (k64) lc_range_kernel<true><<<(unsigned)grid, 256, 0, st>>>(a);
+    else lc_range_kernel<false><<<(unsigned)grid, 256, 0, st>>>(a);
     lc_detail::count_launch(1);
     return cuda_status();
 }

@@ -6,6 +6,9 @@
 
 #include <cstdint>
 #include <cstdio>
+#ifndef NSRC
+#define NSRC 7500000ull
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(256) gather(const ulonglong2* __restrict__ src,
@@ -48,7 +51,7 @@ __global__ void seq(const ulonglong2* __restrict__ src, uint64_t q, unsigned lon
 }
 
 int main() {
-    const uint64_t nsrc = 7'500'000, q = 100'000'000;  // params-like: 120 MB source
+    const uint64_t nsrc = NSRC, q = 100000000;  // params-like source (NSRC x 16 B)
     ulonglong2* src;
     uint32_t* idx;
     unsigned long long* out;

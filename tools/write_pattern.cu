@@ -165,6 +165,19 @@ __global__ void __launch_bounds__(256) p_mixed(const uint8_t* r0, const uint8_t*
     if (BULKST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// Streaming read:write mix: each thread reads 16 B from src and writes R x 16 B to dst
+// (grid-stride, contiguous streams) -- the decode's ~1:3 byte ratio without its structure.
+template <int R>
+__global__ void p_ratio(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t nsrc) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nsrc;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcs(src + i);
+#pragma unroll
+        for (int r = 0; r < R; ++r) __stcs(dst + (size_t)r * nsrc + i, v);
+    }
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -256,6 +269,22 @@ int main() {
         }
         CK(cudaGetLastError());
         cudaFree(a0); cudaFree(a1); cudaFree(a2); cudaFree(o2);
+    }
+
+    {   // streaming ratio mixes: read 1 GB, write R GB
+        const size_t ns = (1ull << 30) / 16;
+        uint4 *src, *dst;
+        CK(cudaMalloc(&src, ns * 16));
+        CK(cudaMalloc(&dst, 4 * ns * 16));
+        cudaMemset(src, 1, ns * 16);
+        auto gb = [&](float ms, int r) { return (1.0 + r) * ns * 16 / (ms * 1e-3) / 1e9; };
+        for (int g : {4, 8, 16}) {
+            printf(", \"ratio1_1_g%d\": %.1f", g, gb(timeit([&] { p_ratio<1><<<sms * g, 256>>>(src, dst, ns); }), 1));
+            printf(", \"ratio1_2_g%d\": %.1f", g, gb(timeit([&] { p_ratio<2><<<sms * g, 256>>>(src, dst, ns); }), 2));
+            printf(", \"ratio1_3_g%d\": %.1f", g, gb(timeit([&] { p_ratio<3><<<sms * g, 256>>>(src, dst, ns); }), 3));
+            printf(", \"ratio1_4_g%d\": %.1f", g, gb(timeit([&] { p_ratio<4><<<sms * g, 256>>>(src, dst, ns); }), 4));
+        }
+        cudaFree(src); cudaFree(dst);
     }
     CK(cudaGetLastError());
     printf("}\n");
