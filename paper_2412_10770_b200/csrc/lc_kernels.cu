@@ -561,8 +561,33 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     }
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
 
-    // gather range k into ring slot k % kR64Slots: groups 0..11 params, 12..16 starts, then words
+    // gather range k into ring slot k % kR64Slots: copy groups 0..11 = params, 12..16 = starts,
+    // then words; group g is done by lane g % 32.  Each lane's role (source section, offset in
+    // the slot) is fixed, so per range it only adds the range's uniform section offset.
     const uint32_t ngroups = kR64Segs + 5 + nw16;
+    struct Role {
+        const uint8_t* src;  // section base + 16 t
+        uint32_t dst, kind, t;
+    };
+    auto role_of = [&](uint32_t g) {
+        Role r;
+        if (g < kR64Segs) r = {(const uint8_t*)(sec.params + g), 16 * g, 0, g};
+        else if (g < kR64Segs + 5)
+            r = {(const uint8_t*)(sec.starts + 4 * (g - kR64Segs)), 16 * g, 1, g - kR64Segs};
+        else
+            r = {(const uint8_t*)(sec.words + 4 * (g - kR64Segs - 5)), 16 * kR64Segs + 80 +
+                 16 * (g - kR64Segs - 5), 2, g - kR64Segs - 5};
+        return r;
+    };
+    const Role ra = role_of(lane), rb = role_of(lane + 32);
+    const bool has_a = lane < ngroups, has_b = lane + 32 < ngroups;
+    auto copy = [&](const Role& r, uint8_t* slot, uint32_t jk, uint32_t s0, uint32_t w0) {
+        const uint64_t off = r.kind == 0 ? (uint64_t)jk * 16 : r.kind == 1 ? (uint64_t)s0 * 4
+                                                                            : (uint64_t)w0 * 4;
+        const bool valid = r.kind == 0 ? jk + r.t < L
+                                       : (r.kind == 1 || w0 + 4 * r.t + 4 <= a.nwords);
+        cp16(slot + r.dst, r.src + off, valid);
+    };
     auto issue = [&](uint32_t k) {
         if (k < nr) {
             const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
@@ -571,18 +596,8 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             if (okk) {
                 const uint32_t s0 = (jk + 1) & ~3u;
                 const uint32_t w0 = (uint32_t)(((uint64_t)rk * b) >> 5) & ~3u;
-                for (uint32_t g = lane; g < ngroups; g += 32) {
-                    if (g < kR64Segs) {
-                        cp16(slot + 16 * g, sec.params + jk + g, jk + g < L);
-                    } else if (g < kR64Segs + 5) {
-                        const uint32_t t = g - kR64Segs;
-                        cp16(slot + 16 * kR64Segs + 16 * t, sec.starts + s0 + 4 * t, true);
-                    } else {
-                        const uint32_t t = g - kR64Segs - 5;
-                        cp16(slot + 16 * kR64Segs + 80 + 16 * t, sec.words + w0 + 4 * t,
-                             w0 + 4 * t + 4 <= a.nwords);
-                    }
-                }
+                if (has_a) copy(ra, slot, jk, s0, w0);
+                if (has_b) copy(rb, slot, jk, s0, w0);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
