@@ -514,7 +514,13 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
                  : "memory");
 }
 
-constexpr uint32_t kR64Segs = 12;   // params staged per range (>= 1 + boundaries in 64 keys)
+#ifndef LC_R64_SEGS
+#define LC_R64_SEGS 8
+#endif
+// params staged per range: 1 + boundaries in 64 keys is <= 8 for 99.6% of config-5 ranges
+// (max 10); a range needing more is decoded through L2
+constexpr uint32_t kR64Segs = LC_R64_SEGS;
+constexpr uint32_t kR64StartGroups = (kR64Segs + 3 + 3) / 4;  // starts[j+1 .. j+kR64Segs] from a 16-B boundary
 #ifndef LC_R64_SLOTS
 #define LC_R64_SLOTS 4
 #endif
@@ -523,15 +529,15 @@ __host__ __device__ constexpr uint32_t r64_words(uint32_t b) {  // staged residu
     return ((((64 * b + 31) >> 5) + 2 + 3) + 3) & ~3u;
 }
 __host__ __device__ constexpr uint32_t r64_bytes(uint32_t b) {  // per slot: params|starts|words
-    return 16 * kR64Segs + 4 * 20 + 4 * r64_words(b);
+    return 16 * kR64Segs + 16 * kR64StartGroups + 4 * r64_words(b);
 }
 
 // 64-key ranges (BASELINE config 5).  Phase 1: lane r binary-searches range r's first segment
 // (32 independent searches).  Phase 2: the warp walks its 32 ranges through a 4-slot shared-
-// memory ring: the lanes gather range k+3's params[j..j+12), starts[j+1..j+17) and residual
-// words with cp.async (one or two 16-byte copies per lane) while range k is decoded from smem
-// with the pair-window scheme, so the decode never waits on a dependent global load.  A range
-// crossing more than 11 segment starts is decoded through L2 instead.
+// memory ring: the lanes gather range k+3's params[j..j+8), starts[j+1..j+9) and residual
+// words with cp.async (one 16-byte copy per lane) while range k is decoded from smem with the
+// pair-window scheme, so the decode never waits on a dependent global load.  A range crossing
+// more than 7 segment starts is decoded through L2 instead.
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -564,19 +570,19 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     // gather range k into ring slot k % kR64Slots: copy groups 0..11 = params, 12..16 = starts,
     // then words; group g is done by lane g % 32.  Each lane's role (source section, offset in
     // the slot) is fixed, so per range it only adds the range's uniform section offset.
-    const uint32_t ngroups = kR64Segs + 5 + nw16;
+    const uint32_t ngroups = kR64Segs + kR64StartGroups + nw16;
     struct Role {
         const uint8_t* src;  // section base + 16 t
         uint32_t dst, kind, t;
     };
     auto role_of = [&](uint32_t g) {
         Role r;
+        const uint32_t gw = kR64Segs + kR64StartGroups;
         if (g < kR64Segs) r = {(const uint8_t*)(sec.params + g), 16 * g, 0, g};
-        else if (g < kR64Segs + 5)
+        else if (g < gw)
             r = {(const uint8_t*)(sec.starts + 4 * (g - kR64Segs)), 16 * g, 1, g - kR64Segs};
         else
-            r = {(const uint8_t*)(sec.words + 4 * (g - kR64Segs - 5)), 16 * kR64Segs + 80 +
-                 16 * (g - kR64Segs - 5), 2, g - kR64Segs - 5};
+            r = {(const uint8_t*)(sec.words + 4 * (g - gw)), 16 * g, 2, g - gw};
         return r;
     };
     const Role ra = role_of(lane), rb = role_of(lane + 32);
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         const uint8_t* rsm = ring + (k % kR64Slots) * RB;
         const ulonglong2* P = (const ulonglong2*)rsm;
         const uint32_t* S = (const uint32_t*)(rsm + 16 * kR64Segs) + ((jk + 1) & 3);  // starts[jk+1+t]
-        const uint32_t x = (lane < 16 && jk + 1 + lane <= L) ? S[lane] - rk : kFull;
+        const uint32_t x = (lane < kR64Segs && jk + 1 + lane <= L) ? S[lane] - rk : kFull;
         const uint32_t inside = __ballot_sync(kFull, x < 64);
         if (__popc(inside) < kR64Segs) {
             const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
@@ -636,7 +642,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             const ulonglong2 pB = P[__popc(PA) + __popc(mB)];
             uint32_t uA = 0, uB = 0;
             if (b) {
-                const uint32_t* Wd = (const uint32_t*)(rsm + 16 * kR64Segs + 80);
+                const uint32_t* Wd = (const uint32_t*)(rsm + 16 * (kR64Segs + kR64StartGroups));
                 const uint64_t wbase = ((((uint64_t)rk * b) >> 5) & ~3ull) << 5;
                 const uint32_t bA = (uint32_t)((uint64_t)(rk + lane) * b - wbase);
                 const uint32_t bB = bA + 32 * b;
