@@ -4,22 +4,23 @@
 // What is computed (FORMAT F3; PAPER.md:105 K[i] = floor(f(i)) + Delta[i]; Eq. 1):
 //     key_i = base_j + floor(slope_j * (i - s_j) / 2^32) + u_i - eps,  j = max{t : s_t <= i}.
 //
-// Design (DESIGN.md "Kernels"):
+// Design (DESIGN.md §6):
 //  * Full decode: one WARP per 1024-key hint block ("chunk"), persistent over chunks.  The
 //    hint array gives the chunk's segment range [hint[h], hint[h+1]] with no search
 //    (PAPER.md:286's auxiliary localisation structure).  Lane 0 stages the chunk's starts,
 //    params and residual words into the warp's shared-memory page with cp.async.bulk (TMA 1D)
-//    on an mbarrier; dense chunks are paged.  The chunk is decoded as 32 windows of 32 keys,
-//    lane = key: a warp OR-reduction (REDUX) of the next 32 segment starts gives a bitmask of
-//    segment boundaries inside the window, so each lane gets its segment with POPC/CLZ —
-//    branch-free, no per-key search and no serial walk ("reduce the data
-//    dependencies ... to maximize parallelism").  The prediction is exact 32-bit integer
-//    math: floor(slope*d/2^32) = umulhi(slope_lo, d) + slope_hi*d (it is < 2^31 by the
-//    slope guard).  Residual fields are funnel-shifted out of the staged words.  Each warp
-//    store writes 32 consecutive keys (coalesced, streaming hint).
-//  * Random access: one thread per query (hint bracket + binary search over starts).
-//  * Range decode: one warp per range; cooperative bracket search, then the same window
-//    scheme reading through L1.
+//    on an mbarrier (dense chunks are paged) and prefetches the next chunk into L2.  The chunk
+//    is decoded as 16 pair-windows of 64 keys (2 keys per lane): warp OR-reductions (REDUX) of
+//    the next 32 segment starts give the boundary bitmasks, so each key gets its segment and
+//    offset with POPC/CLZ -- no per-key search and no serial walk ("reduce the
+//    data dependencies ... to maximize parallelism").  The prediction is exact 32-bit integer
+//    math (see pred_plus).  Each warp store writes 32 consecutive keys (coalesced, streaming).
+//  * Random access / quantiles: hint bracket + binary search, two interleaved queries per
+//    thread, L2 evict_last for the search structures and evict_first for the gathers.
+//  * Range decode: one warp per 32 ranges (lane-parallel search); len == 64 gathers each
+//    range's slices through a per-warp cp.async ring and decodes from shared memory.
+//  * Successor search / intersection: binary search over the anchored segment bases
+//    (segments as skip pointers), then inside one segment.
 #include <cuda_runtime.h>
 
 #include <array>
@@ -43,6 +44,7 @@ struct Sections {
     const ulonglong2* params;  // {base, slope_fx}
     const uint32_t* hint;
     const uint32_t* words;
+    uint32_t L, W;  // segments, residual words (bounds of params / words)
 };
 
 Sections sections_of(const lc_view* v) {
@@ -52,8 +54,31 @@ Sections sections_of(const lc_view* v) {
     s.params = (const ulonglong2*)(B + v->h.off_params);
     s.hint = (const uint32_t*)(B + v->h.off_hint);
     s.words = (const uint32_t*)(B + v->h.off_words);
+    s.L = (uint32_t)v->h.n_seg;
+    s.W = (uint32_t)v->h.n_words;
     return s;
 }
+
+// Bounds-checked build (-DLC_DEBUG_BOUNDS, tests/test_gpu_bounds.py): every shared-memory page
+// / ring-slot index and every section index is checked; a violation is counted in
+// g_lc_violations (read by lc_debug_violations) and the access is clamped instead of faulting.
+#ifdef LC_DEBUG_BOUNDS
+__device__ uint32_t g_lc_violations;
+__device__ uint32_t g_lc_where[3];  // source line, index, limit of the last violation
+__device__ __forceinline__ uint32_t lc_bound(bool live, uint32_t i, uint32_t n, uint32_t line) {
+    if (live && i >= n) {
+        atomicAdd(&g_lc_violations, 1u);
+        g_lc_where[0] = line;
+        g_lc_where[1] = i;
+        g_lc_where[2] = n;
+        return 0;
+    }
+    return i;
+}
+#define LC_BOUND(live, i, n) lc_bound((live), (i), (n), __LINE__)
+#else
+#define LC_BOUND(live, i, n) (i)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers (sm_90+/100a)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -87,22 +112,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // marked evict_first, so the binary-search probes keep hitting L2.
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint32_t ldh(const uint32_t* p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ ulonglong2 ldh(const ulonglong2* p, uint64_t pol) {
     ulonglong2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+    asm("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
                  : "=l"(v.x), "=l"(v.y)
                  : "l"(p), "l"(pol));
     return v;
@@ -136,16 +161,6 @@ __device__ __forceinline__ uint32_t pred_plus(uint64_t slope, uint32_t d, uint32
     return t;
 }
 
-template <bool K64>
-__device__ __forceinline__ void store_key(void* out, uint64_t pos, uint64_t base, uint32_t delta,
-                                          uint32_t u, uint32_t eps) {
-    if (K64) {
-        __stcs((unsigned long long*)out + pos, (unsigned long long)(base + delta + u - eps));
-    } else {
-        __stcs((unsigned int*)out + pos, (unsigned int)((uint32_t)base + delta + u - eps));
-    }
-}
-
 // --------------------------------------------------------------------------- full decode
 struct DecodeArgs {
     Sections sec;
@@ -173,6 +188,9 @@ struct Page {
     uint32_t* sW;         // the chunk's residual words
     uint32_t pj, cp;
     uint32_t phase;
+#ifdef LC_DEBUG_BOUNDS
+    uint32_t cs, nw;  // staged starts / words entries
+#endif
 };
 
 // Stage starts[pj, pj + cs) and params[pj, pj + cp) (plus, when wbytes != 0, the chunk's words)
@@ -185,6 +203,10 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
     pg.cp = min(kSegCap, jlast + 1 - pg.pj);
 #ifdef LC_EXP_NO_STAGE  // experiment build only
     return;
+#endif
+#ifdef LC_DEBUG_BOUNDS
+    pg.cs = (min(kSegCap + 4, jlast + 2 - pg.pj) + 3) & ~3u;
+    if (wbytes) pg.nw = wbytes / 4;
 #endif
     if (lane == 0) {
         const uint32_t cs = min(kSegCap + 4, jlast + 2 - pg.pj);
@@ -232,17 +254,20 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
-    const uint32_t x = pg.sS[cand - pg.pj] - wb;  // > 0: position of the next start
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;  // next start
     const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x));
     const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
     const uint32_t m = P & lmask;  // boundaries at or before this lane's key
     const uint32_t seg = jb + __popc(m);
     const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
-    const ulonglong2 pr = pg.sP[seg - pg.pj];
+    const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
+    LC_BOUND(B && (FULL || lane < valid), w * B + lw + 1, pg.nw);
     const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - eps);
     if (FULL || lane < valid) put<K64>(outw, pr.x, t);
-    jb += adv;
-    sb = pg.sS[jb - pg.pj];
+    // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
+    // the advance there so jb stays a valid staged index
+    jb = min(jb + adv, jlast + 1);
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
 
 // Two windows at once: keys [wb, wb + 64), lane handles wb + lane and wb + 32 + lane.  One
@@ -266,7 +291,7 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
-    const uint32_t x = pg.sS[cand - pg.pj] - wb;
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
     const uint32_t inside = __ballot_sync(kFull, x < 64);
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
         decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
@@ -283,16 +308,17 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t jB = jb + __popc(PA);                                // uniform
     const uint32_t mA = PA & lmask;
     const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
-    const ulonglong2 pA = pg.sP[jb + __popc(mA) - pg.pj];
+    const ulonglong2 pA = pg.sP[LC_BOUND(true, jb + __popc(mA) - pg.pj, pg.cp)];
     const uint32_t mB = PB & lmask;
     const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
-    const ulonglong2 pB = pg.sP[jB + __popc(mB) - pg.pj];
+    const ulonglong2 pB = pg.sP[LC_BOUND(true, jB + __popc(mB) - pg.pj, pg.cp)];
+    LC_BOUND(B, (2 * w2 + 1) * B + lw + 1, pg.nw);
     const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - eps);
     const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps);
     put<K64>(outw, pA.x, tA);
     put<K64>((uint8_t*)outw + 32 * kw, pB.x, tB);
-    jb += adv;
-    sb = pg.sS[jb - pg.pj];
+    jb = min(jb + adv, jlast + 1);  // see decode_window
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
 
 template <bool K64, uint32_t B>
@@ -339,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) lc_decode_kernel(const DecodeArgs a)
             bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
                              min(32 * B * 4 + 16, (a.nwords - (h + nwarps) * 32 * B) * 4));
         uint32_t jb = j0;                // segment holding the window's first key
-        uint32_t sb = pg.sS[j0 - pg.pj];  // its start
+        uint32_t sb = pg.sS[LC_BOUND(true, j0 - pg.pj, pg.cs)];  // its start
         uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
         if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
 #pragma unroll 1
@@ -398,7 +424,9 @@ __device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i, 
 __device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b,
                                              uint64_t pol) {
     const uint64_t bit = (uint64_t)i * b;
-    const uint32_t* wp = sec.words + (bit >> 5);
+    uint32_t wi = (uint32_t)(bit >> 5);
+    if (LC_BOUND(true, wi + 1, sec.W) == 0) wi = 0;  // (only a checked build can take this)
+    const uint32_t* wp = sec.words + wi;
     return make_uint2(ldh(wp, pol), ldh(wp + 1, pol));
 }
 __device__ __forceinline__ uint32_t field_of(uint2 w, uint32_t i, uint32_t b, uint32_t mask) {
@@ -475,8 +503,9 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
             const uint32_t mA = PA & lmask, mB = PB & lmask;
             const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
             const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
-            const ulonglong2 pA = ldh(sec.params + jb + __popc(mA), once);
-            const ulonglong2 pB = ldh(sec.params + jb + __popc(PA) + __popc(mB), once);
+            const ulonglong2 pA = ldh(sec.params + LC_BOUND(true, jb + __popc(mA), L), once);
+            const ulonglong2 pB =
+                ldh(sec.params + LC_BOUND(true, jb + __popc(PA) + __popc(mB), L), once);
             const uint32_t uA = b ? field_of(wA, rk + lane, b, mask) : 0;
             const uint32_t uB = b ? field_of(wB, rk + 32 + lane, b, mask) : 0;
             put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
@@ -494,7 +523,7 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
             const uint32_t m = P & lmask;
             const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sb + lane;
             if (lane < rem) {
-                const ulonglong2 pr = ldh(sec.params + jb + __popc(m), once);
+                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
                 const uint32_t u =
                     b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
                 put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
@@ -638,14 +667,15 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             const uint32_t mA = PA & lmask, mB = PB & lmask;
             const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
             const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
-            const ulonglong2 pA = P[__popc(mA)];
-            const ulonglong2 pB = P[__popc(PA) + __popc(mB)];
+            const ulonglong2 pA = P[LC_BOUND(true, __popc(mA), kR64Segs)];
+            const ulonglong2 pB = P[LC_BOUND(true, __popc(PA) + __popc(mB), kR64Segs)];
             uint32_t uA = 0, uB = 0;
             if (b) {
                 const uint32_t* Wd = (const uint32_t*)(rsm + 16 * (kR64Segs + kR64StartGroups));
                 const uint64_t wbase = ((((uint64_t)rk * b) >> 5) & ~3ull) << 5;
                 const uint32_t bA = (uint32_t)((uint64_t)(rk + lane) * b - wbase);
                 const uint32_t bB = bA + 32 * b;
+                LC_BOUND(true, (bB >> 5) + 1, r64_words(b));
                 uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
                 uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
             }
@@ -660,7 +690,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
                 const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
                 const uint32_t m = Pm & lmask;
                 const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
-                const ulonglong2 pr = ldh(sec.params + jb + __popc(m), once);
+                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
                 const uint32_t u =
                     b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
                 put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
@@ -749,7 +779,7 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {
         if (!live[k]) continue;
         const uint32_t s = ldh(sec.starts + lo[k], keep);
-        const ulonglong2 pr = ldh(sec.params + lo[k], once);
+        const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
         const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
         const uint64_t t = t0 + 256 * k;
         put<K64>((uint8_t*)a.out + t * (K64 ? 8 : 4), pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
@@ -1313,5 +1343,18 @@ int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, vo
     cudaStreamWaitEvent(s, g_pipe.done, 0);
     return cuda_status();
 }
+
+#ifdef LC_DEBUG_BOUNDS
+// bounds-checked builds only: violations counted since the previous call (and reset)
+uint32_t lc_debug_violations(void) {
+    uint32_t v = 0, z = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&v, g_lc_violations, sizeof v);
+    cudaMemcpyToSymbol(g_lc_violations, &z, sizeof z);
+    return v;
+}
+// source line / index / limit of the last violation
+void lc_debug_where(uint32_t* out3) { cudaMemcpyFromSymbol(out3, g_lc_where, 3 * sizeof(uint32_t)); }
+#endif
 
 }  // extern "C"
