@@ -201,9 +201,6 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
     __syncwarp();  // every lane is done reading the previous contents
     pg.pj = from & ~3u;
     pg.cp = min(kSegCap, jlast + 1 - pg.pj);
-#ifdef LC_EXP_NO_STAGE  // experiment build only
-    return;
-#endif
 #ifdef LC_DEBUG_BOUNDS
     pg.cs = (min(kSegCap + 4, jlast + 2 - pg.pj) + 3) & ~3u;
     if (wbytes) pg.nw = wbytes / 4;
@@ -279,15 +276,6 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
                                             uint32_t w2, uint32_t lane, uint32_t lmask,
                                             uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
     constexpr uint32_t kw = K64 ? 8 : 4;
-#ifdef LC_EXP_STORE_ONLY  // experiment build only: memory pattern without the decode math
-    put<K64>(outw, jb, lane);
-    put<K64>((uint8_t*)outw + 32 * kw, jb, lane);
-    return;
-#endif
-#ifdef LC_EXP_STAGE_ONLY  // experiment build only: staging reads, no decode, no stores
-    if (jb == 0xffffffffu) put<K64>(outw, jb, lane);
-    return;
-#endif
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
@@ -1173,7 +1161,6 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
-#ifndef LC_EXP_NO_RANGE64
     if (len == 64) {  // the config-5 shape: cp.async ring kernel
         const uint32_t smem = 8 * kR64Slots * r64_bytes(a.b);
         const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;
@@ -1183,7 +1170,6 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
         lc_detail::count_launch(1);
         return cuda_status();
     }
-#endif
     if (k64) lc_range_kernel<true><<<(unsigned)grid, 256, 0, st>>>(a);
     else lc_range_kernel<false><<<(unsigned)grid, 256, 0, st>>>(a);
     lc_detail::count_launch(1);

@@ -367,3 +367,26 @@ def test_intersect_key_width_mismatch(lc):
     vb = lc.View(lc.encode(np.arange(10, dtype=np.uint64), 1), device=DEV)
     with pytest.raises(lc.LcError):
         lc.intersect(va, vb)
+
+
+def test_full_config5_quantile_next_geq(lc):
+    """NEXT-1/NEXT-2 at the config-5 size (1e8 keys): 1e6 quantiles and 1e6 successor probes,
+    every answer checked (exact quantiles / next_geq vs the key array, approximate quantiles vs
+    the oracle's prediction)."""
+    keys = make_keys(5)
+    blob = lc.encode(keys, 127)
+    view = lc.View(blob, device=DEV)
+    rng = np.random.default_rng(5)
+    q = (1 << 32) - 1
+    ranks = rng.integers(0, q, 1_000_000, endpoint=True).astype(np.uint64)
+    idx = np.minimum((ranks.astype(object) * keys.size) // q, keys.size - 1).astype(np.int64)
+    ex = _host(lc.quantile(view, _dev(ranks), q), np.uint64)
+    assert np.array_equal(ex, keys[idx])
+    ap = _host(lc.quantile(view, _dev(ranks), q, exact=False), np.uint64)
+    want_ap, _ = orc.predict(blob, idx[:20_000].astype(np.uint64))
+    assert np.array_equal(ap[:20_000], want_ap)
+    assert np.abs(ap.astype(np.int64) - keys[idx].astype(np.int64)).max() <= 127
+    x = _probes(keys, rng, 1_000_000)
+    gi, gk = lc.next_geq(view, _dev(x))
+    wi, wk = setops.next_geq(keys, x)
+    assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, np.uint64), wk)
