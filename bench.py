@@ -325,6 +325,10 @@ def run_gpu(args):
         i_scr = torch.empty(lc.intersect_scratch_bytes(va), dtype=torch.uint8, device=dev)
         i_out = va.out_tensor(va.n)
         i_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        u_scr = torch.empty(lc.union_scratch_bytes(va, v5),
+                            dtype=torch.uint8, device=dev)
+        u_out = va.out_tensor(va.n + v5.n)
+        u_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         reps = max(3, min(args.steps, 20))
         with torch.cuda.stream(stream):
             _, pqe = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, True, q_out,
@@ -335,9 +339,13 @@ def run_gpu(args):
                                     stream, reps, 2)
             _, pis = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt,
                                                          stream=stream), stream, reps, 2)
+            _, pun = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt,
+                                                     stream=stream), stream, reps, 2)
         want_cnt = int(np.intersect1d(a_keys, k5, assume_unique=True).size)
         if int(i_cnt.item()) != want_cnt:
             raise SystemExit("intersection count mismatch")
+        if int(u_cnt.item()) != a_keys.size + k5.size - want_cnt:
+            raise SystemExit("union count mismatch")
         access = {
             "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
                         "lookups; 1e7 ranges x 64 keys",
@@ -347,6 +355,8 @@ def run_gpu(args):
             "intersect": {"a_keys": int(a_keys.size), "b_keys": int(k5.size),
                           "matches": want_cnt, "ms": statistics.mean(pis) * 1e3,
                           "a_keys_per_s": a_keys.size / statistics.mean(pis)},
+            "union": {"keys_out": int(u_cnt.item()), "ms": statistics.mean(pun) * 1e3,
+                      "out_keys_per_s": int(u_cnt.item()) / statistics.mean(pun)},
             "lookups_per_s": ws * idx.size / statistics.mean(pa),
             "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
             "ranges_per_s": ws * rs.size / statistics.mean(pr),
@@ -358,6 +368,7 @@ def run_gpu(args):
         if not (ok_a and ok_r):
             raise SystemExit("access/range mismatch")
         del v5, d_idx, a_out, d_rs, r_out, va, i_scr, i_out, d_ranks, q_out, d_probe, p_idx, p_key
+        del u_scr, u_out
 
     if ws > 1:
         dist.barrier()

@@ -145,6 +145,17 @@ uint64_t lc_intersect_scratch_bytes(const lc_view* a);
 int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                      void* d_out, uint64_t* d_count, lc_stream stream);
 
+/* Device scratch bytes lc_union needs for lists a and b. */
+uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b);
+
+/* Union of two compressed lists, the OR query of inverted-index processing:
+ * d_out receives the sorted keys present in either list (each once) and *d_count (device
+ * uint64) their number.  Both lists are decoded into d_scratch (>= lc_union_scratch_bytes(a, b)
+ * bytes, 256-byte aligned); keys of b absent from a are compacted, then merged with a by a
+ * merge-path pass.  d_out capacity: a->h.n + b->h.n keys.  Same key_bits required. */
+int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
+                 void* d_out, uint64_t* d_count, lc_stream stream);
+
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
  * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out

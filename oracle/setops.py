@@ -31,3 +31,8 @@ def next_geq(keys: np.ndarray, x: np.ndarray):
 def intersect(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Sorted keys present in both lists (both strictly increasing)."""
     return np.intersect1d(a, b, assume_unique=True)
+
+
+def union(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Sorted keys present in either list (each once)."""
+    return np.union1d(a, b)

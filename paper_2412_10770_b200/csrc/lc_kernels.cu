@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 #include "lc.h"
@@ -998,6 +999,74 @@ __global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) 
     }
 }
 
+// Union A ∪ B (OR query): both lists are decoded into scratch; the keys of B that
+// are absent from A are flagged (binary search in the decoded A) and compacted in order into
+// B \ A with the intersection's scan/scatter kernels; then one merge-path pass merges the two
+// disjoint sorted lists A and B \ A straight into the output.
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_union_flag_kernel(const IsectArgs a, const void* a_sorted,
+                                                            uint32_t n_sorted) {
+    __shared__ uint32_t warp_cnt[8];
+    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bool keep = false;
+    if (t < a.na) {  // a.a_keys = decoded B; keep keys of B not in A
+        const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
+        uint32_t lo = 0, hi = n_sorted;  // first A[i] >= x
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            const uint64_t v = K64 ? __ldg((const uint64_t*)a_sorted + mid)
+                                   : __ldg((const uint32_t*)a_sorted + mid);
+            if (v < x) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint64_t v = lo < n_sorted ? (K64 ? __ldg((const uint64_t*)a_sorted + lo)
+                                                : __ldg((const uint32_t*)a_sorted + lo))
+                                         : ~0ull;
+        keep = lo == n_sorted || v != x;
+    }
+    const uint32_t bal = __ballot_sync(kFull, keep);
+    if (lane == 0) {
+        if (t < a.na) a.flags[t >> 5] = bal;
+        warp_cnt[warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (int w = 0; w < 8; ++w) c += warp_cnt[w];
+        a.counts[blockIdx.x] = c;
+    }
+}
+
+constexpr uint32_t kMergeItems = 8;  // output keys per thread in the merge-path pass
+
+// merge the disjoint sorted lists A (na keys) and C (*nc keys) into out (merge path)
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_merge_kernel(const void* A, uint32_t na, const void* C,
+                                                       const uint32_t* nc_ptr, void* out,
+                                                       uint64_t* d_count) {
+    using K = typename std::conditional<K64, uint64_t, uint32_t>::type;
+    const K* a = (const K*)A;
+    const K* c = (const K*)C;
+    const uint32_t nc = *nc_ptr, total = na + nc;
+    const uint64_t diag64 = ((uint64_t)blockIdx.x * 256 + threadIdx.x) * kMergeItems;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = total;
+    if (diag64 >= total) return;
+    const uint32_t diag = (uint32_t)diag64;
+    uint32_t lo = diag > nc ? diag - nc : 0, hi = min(diag, na);
+    while (lo < hi) {  // i = number of A keys among the first diag merged keys
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < __ldg(c + (diag - 1 - mid))) lo = mid + 1;
+        else hi = mid;
+    }
+    uint32_t i = lo, j = diag - lo;
+    K* o = (K*)out + diag;
+    for (uint32_t k = 0; k < kMergeItems && diag + k < total; ++k) {
+        const bool take_a = j >= nc || (i < na && __ldg(a + i) < __ldg(c + j));
+        o[k] = take_a ? __ldg(a + i++) : __ldg(c + j++);
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
 uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
 
@@ -1281,6 +1350,53 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     if (kw == 8) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
     else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
     lc_detail::count_launch(3);
+    return cuda_status();
+}
+
+uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b) {
+    if (!a || !b) return 0;
+    const uint64_t na = a->h.n, nb = b->h.n, kw = a->h.key_bits / 8;
+    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
+    return r256(na * kw) + 2 * r256(nb * kw) + r256(4 * ((nb + 31) / 32)) +
+           r256(4 * ((nb + 255) / 256 + 1));
+}
+
+int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
+                 void* d_out, uint64_t* d_count, lc_stream stream) {
+    if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
+    if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
+    if (scratch_bytes < lc_union_scratch_bytes(a, b) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
+    const uint64_t na = a->h.n, nb = b->h.n, kw = a->h.key_bits / 8;
+    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
+    uint8_t* sc = (uint8_t*)d_scratch;
+    uint8_t* sA = sc;
+    uint8_t* sB = sA + r256(na * kw);
+    uint8_t* sC = sB + r256(nb * kw);  // B \ A
+    uint32_t* flags = (uint32_t*)(sC + r256(nb * kw));
+    uint32_t* counts = (uint32_t*)((uint8_t*)flags + r256(4 * ((nb + 31) / 32)));
+    IsectArgs g{};
+    g.a_keys = sB;
+    g.flags = flags;
+    g.counts = counts;
+    g.out = sC;
+    g.d_count = d_count;  // overwritten by the merge with the union size
+    g.na = (uint32_t)nb;
+    g.nblk = (uint32_t)((nb + 255) / 256);
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t rc = launch_decode(a, 0, na, sA, st);
+    if (!rc) rc = launch_decode(b, 0, nb, sB, st);
+    if (rc) return rc;
+    const bool k64 = kw == 8;
+    if (k64) lc_union_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g, sA, (uint32_t)na);
+    else lc_union_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g, sA, (uint32_t)na);
+    lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
+    if (k64) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
+    else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
+    const uint64_t threads = (na + nb + kMergeItems - 1) / kMergeItems;
+    const unsigned mgrid = (unsigned)((threads + 255) / 256);
+    if (k64) lc_merge_kernel<true><<<mgrid, 256, 0, st>>>(sA, (uint32_t)na, sC, counts + g.nblk, d_out, d_count);
+    else lc_merge_kernel<false><<<mgrid, 256, 0, st>>>(sA, (uint32_t)na, sC, counts + g.nblk, d_out, d_count);
+    lc_detail::count_launch(4);
     return cuda_status();
 }
 

@@ -56,6 +56,8 @@ _sig = {
     "lc_next_geq": ([C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_intersect_scratch_bytes": ([C.POINTER(lc_view)], _u64),
     "lc_intersect": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
+    "lc_union_scratch_bytes": ([C.POINTER(lc_view), C.POINTER(lc_view)], _u64),
+    "lc_union": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
@@ -233,6 +235,14 @@ def next_geq(view: View, x, out_idx=None, out_key=None, stream=None):
     return out_idx, out_key
 
 
+def ctypes_ref(view: View):
+    return C.byref(view.v)
+
+
+def union_scratch_bytes(a: View, b: View) -> int:
+    return int(_lib.lc_union_scratch_bytes(C.byref(a.v), C.byref(b.v)))
+
+
 def intersect_scratch_bytes(a: View) -> int:
     return int(_lib.lc_intersect_scratch_bytes(C.byref(a.v)))
 
@@ -252,6 +262,23 @@ def intersect(a: View, b: View, scratch=None, out=None, count=None, stream=None)
     _check(_lib.lc_intersect(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
                              scratch.numel() * scratch.element_size(), out.data_ptr(),
                              count.data_ptr(), _stream(stream)), "lc_intersect")
+    return out, count
+
+
+def union(a: View, b: View, scratch=None, out=None, count=None, stream=None):
+    """lc_union: sorted keys in either list.  Returns (out, count): out[:count] is the union."""
+    import torch
+    dev = a.d_blob.device
+    need = int(_lib.lc_union_scratch_bytes(C.byref(a.v), C.byref(b.v)))
+    if scratch is None:
+        scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+    if out is None:
+        out = a.out_tensor(a.n + b.n)
+    if count is None:
+        count = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.lc_union(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
+                         scratch.numel() * scratch.element_size(), out.data_ptr(),
+                         count.data_ptr(), _stream(stream)), "lc_union")
     return out, count
 
 

@@ -390,3 +390,38 @@ def test_full_config5_quantile_next_geq(lc):
     gi, gk = lc.next_geq(view, _dev(x))
     wi, wk = setops.next_geq(keys, x)
     assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, np.uint64), wk)
+
+
+def _union_case(lc, a, b, eps_a, eps_b):
+    va = lc.View(lc.encode(a, eps_a), device=DEV)
+    vb = lc.View(lc.encode(b, eps_b), device=DEV)
+    out, cnt = lc.union(va, vb)
+    torch.cuda.synchronize()
+    c = int(cnt.item())
+    want = setops.union(a, b)
+    assert c == want.size
+    assert np.array_equal(_host(out[:c], a.dtype), want)
+
+
+@pytest.mark.parametrize("na", [1, 1000, 33_333, 300_000])
+def test_union_subset_plus_noise(lc, na):
+    b = make_keys(2, 500_000)
+    rng = np.random.default_rng(na + 1)
+    pick = b[np.sort(rng.choice(b.size, na // 2 + 1, replace=False))]
+    noise = rng.integers(0, int(b[-1]) + 1000, na, dtype=np.uint64)
+    a = np.unique(np.concatenate([pick, noise]))[:na]
+    _union_case(lc, a, b, 63, 127)
+    _union_case(lc, b, a, 127, 63)
+
+
+def test_union_closed_form_and_edges(lc):
+    M = 2_000_000
+    a = np.arange(0, M, 6, dtype=np.uint64)
+    b = np.arange(0, M, 10, dtype=np.uint64)
+    _union_case(lc, a, b, 0, 31)
+    _union_case(lc, b, b, 127, 127)                  # identical lists
+    _union_case(lc, a + np.uint64(1), a, 7, 7)       # disjoint, interleaved
+    _union_case(lc, a, a + np.uint64(M), 7, 7)       # disjoint, b entirely after a
+    _union_case(lc, np.array([5], np.uint64), np.array([5], np.uint64), 1, 1)
+    a32 = np.arange(5, 2_000_000, 3, dtype=np.uint32)
+    _union_case(lc, a32, make_keys(1, 1_000_000), 15, 63)

@@ -424,6 +424,7 @@ def test_setops_bruteforce_tiny():
             assert int(i) == want
             assert int(k) == (int(a[want]) if want < len(a) else 0)
         assert setops.intersect(a, b).tolist() == sorted(set(a.tolist()) & set(b.tolist()))
+        assert setops.union(a, b).tolist() == sorted(set(a.tolist()) | set(b.tolist()))
 
 
 def test_intersect_lcm_closed_form():
@@ -434,6 +435,8 @@ def test_intersect_lcm_closed_form():
         b = np.arange(0, M, q, dtype=np.uint64)
         l = p * q // math.gcd(p, q)
         assert np.array_equal(setops.intersect(a, b), np.arange(0, M, l, dtype=np.uint64))
+        # inclusion-exclusion: |A u B| = |A| + |B| - |A n B|
+        assert setops.union(a, b).size == a.size + b.size - (M + l - 1) // l
 
 
 def test_next_geq_u32_probe_above_range():

@@ -84,6 +84,9 @@ def main():
     out, cnt = lc.intersect(va, vb)
     c = int(cnt.item())
     check("intersect", np.array_equal(h(out[:c], np.uint64), setops.intersect(a, k5)))
+    out, cnt = lc.union(va, vb)
+    c = int(cnt.item())
+    check("union", np.array_equal(h(out[:c], np.uint64), setops.union(a, k5)))
     print(f"bounds check ok: {checks} checks, 0 violations")
 
 
