@@ -999,10 +999,10 @@ __global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) 
     }
 }
 
-// Union A ∪ B (OR query): both lists are decoded into scratch; the keys of B that
-// are absent from A are flagged (binary search in the decoded A) and compacted in order into
-// B \ A with the intersection's scan/scatter kernels; then one merge-path pass merges the two
-// disjoint sorted lists A and B \ A straight into the output.
+// Union (OR query): both lists are decoded into scratch; the keys of the shorter
+// list that are absent from the longer one are flagged (binary search in the decoded longer
+// list) and compacted in order with the intersection's scan/scatter kernels; then one
+// merge-path pass merges the two disjoint sorted lists straight into the output.
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_union_flag_kernel(const IsectArgs a, const void* a_sorted,
                                                             uint32_t n_sorted) {
@@ -1356,9 +1356,10 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
 uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b) {
     if (!a || !b) return 0;
     const uint64_t na = a->h.n, nb = b->h.n, kw = a->h.key_bits / 8;
+    const uint64_t ns = na < nb ? na : nb;  // the shorter list is flagged and compacted
     auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
-    return r256(na * kw) + 2 * r256(nb * kw) + r256(4 * ((nb + 31) / 32)) +
-           r256(4 * ((nb + 255) / 256 + 1));
+    return r256(na * kw) + r256(nb * kw) + r256(ns * kw) + r256(4 * ((ns + 31) / 32)) +
+           r256(4 * ((ns + 255) / 256 + 1));
 }
 
 int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
@@ -1366,37 +1367,39 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_union_scratch_bytes(a, b) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
-    const uint64_t na = a->h.n, nb = b->h.n, kw = a->h.key_bits / 8;
+    // union = long ∪ (short \ long): only the shorter list is searched and compacted
+    const lc_view* lg = a->h.n >= b->h.n ? a : b;
+    const lc_view* sh = a->h.n >= b->h.n ? b : a;
+    const uint64_t nl = lg->h.n, ns = sh->h.n, kw = a->h.key_bits / 8;
     auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
-    uint8_t* sc = (uint8_t*)d_scratch;
-    uint8_t* sA = sc;
-    uint8_t* sB = sA + r256(na * kw);
-    uint8_t* sC = sB + r256(nb * kw);  // B \ A
-    uint32_t* flags = (uint32_t*)(sC + r256(nb * kw));
-    uint32_t* counts = (uint32_t*)((uint8_t*)flags + r256(4 * ((nb + 31) / 32)));
+    uint8_t* sL = (uint8_t*)d_scratch;
+    uint8_t* sS = sL + r256(nl * kw);
+    uint8_t* sC = sS + r256(ns * kw);  // short \ long
+    uint32_t* flags = (uint32_t*)(sC + r256(ns * kw));
+    uint32_t* counts = (uint32_t*)((uint8_t*)flags + r256(4 * ((ns + 31) / 32)));
     IsectArgs g{};
-    g.a_keys = sB;
+    g.a_keys = sS;
     g.flags = flags;
     g.counts = counts;
     g.out = sC;
     g.d_count = d_count;  // overwritten by the merge with the union size
-    g.na = (uint32_t)nb;
-    g.nblk = (uint32_t)((nb + 255) / 256);
+    g.na = (uint32_t)ns;
+    g.nblk = (uint32_t)((ns + 255) / 256);
     cudaStream_t st = (cudaStream_t)stream;
-    int32_t rc = launch_decode(a, 0, na, sA, st);
-    if (!rc) rc = launch_decode(b, 0, nb, sB, st);
+    int32_t rc = launch_decode(lg, 0, nl, sL, st);
+    if (!rc) rc = launch_decode(sh, 0, ns, sS, st);
     if (rc) return rc;
     const bool k64 = kw == 8;
-    if (k64) lc_union_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g, sA, (uint32_t)na);
-    else lc_union_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g, sA, (uint32_t)na);
+    if (k64) lc_union_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g, sL, (uint32_t)nl);
+    else lc_union_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g, sL, (uint32_t)nl);
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (k64) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
     else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
-    const uint64_t threads = (na + nb + kMergeItems - 1) / kMergeItems;
+    const uint64_t threads = (nl + ns + kMergeItems - 1) / kMergeItems;
     const unsigned mgrid = (unsigned)((threads + 255) / 256);
-    if (k64) lc_merge_kernel<true><<<mgrid, 256, 0, st>>>(sA, (uint32_t)na, sC, counts + g.nblk, d_out, d_count);
-    else lc_merge_kernel<false><<<mgrid, 256, 0, st>>>(sA, (uint32_t)na, sC, counts + g.nblk, d_out, d_count);
-    lc_detail::count_launch(4);
+    if (k64) lc_merge_kernel<true><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
+    else lc_merge_kernel<false><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
+    lc_detail::count_launch(6);
     return cuda_status();
 }
 
