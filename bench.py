@@ -285,6 +285,19 @@ def run_gpu(args):
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = ws * alg_bytes * e2e_steps / float(e2e_t.item()) / 1e9
+    # PCIe ceiling of the same transfers: plain pinned copies, each direction alone
+    cp_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            cp_ev[0].record(stream)
+            d_blob.copy_(h_blob, non_blocking=True)
+            cp_ev[1].record(stream)
+            h_out.copy_(out, non_blocking=True)
+            cp_ev[2].record(stream)
+    torch.cuda.synchronize()
+    h2d_gbps = len(blob) / (cp_ev[0].elapsed_time(cp_ev[1]) * 1e-3) / 1e9
+    d2h_gbps = n * w / (cp_ev[1].elapsed_time(cp_ev[2]) * 1e-3) / 1e9
+    e2e_floor_ms = max(len(blob) / h2d_gbps, n * w / d2h_gbps) / 1e6  # full-duplex overlap
     del h_blob, d_blob, h_out
 
     # ---- random access + range decodes (config 5), reported beside the headline
@@ -398,7 +411,10 @@ def run_gpu(args):
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": len(blob),
                 "d2h_bytes_per_step": n * w, "api": "lc_decode_host (pinned host blob -> "
-                "device -> decode -> pinned host keys)"},
+                "device -> decode -> pinned host keys)",
+                "ms_per_step": float(e2e_t.item()) / e2e_steps * 1e3,
+                "pcie_h2d_GBps": h2d_gbps, "pcie_d2h_GBps": d2h_gbps,
+                "pcie_floor_ms": e2e_floor_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "access": access,

@@ -1038,33 +1038,62 @@ __global__ void __launch_bounds__(256) lc_union_flag_kernel(const IsectArgs a, c
     }
 }
 
-constexpr uint32_t kMergeItems = 8;  // output keys per thread in the merge-path pass
+constexpr uint32_t kMergeItems = 8;                 // output keys per thread
+constexpr uint32_t kMergeTile = 256 * kMergeItems;  // output keys per CTA
 
-// merge the disjoint sorted lists A (na keys) and C (*nc keys) into out (merge path)
+// number of A keys among the first `diag` keys of merge(A, C) (disjoint sorted lists)
+template <typename K>
+__device__ __forceinline__ uint32_t merge_split(const K* a, uint32_t na, const K* c, uint32_t nc,
+                                                uint32_t diag) {
+    uint32_t lo = diag > nc ? diag - nc : 0, hi = min(diag, na);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < c[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Tiled merge path: CTA t produces outputs [t*2048, (t+1)*2048).  One thread finds the tile's
+// split on each input, the tile's slices of A and C are loaded coalesced into shared memory,
+// each thread merges 8 outputs from shared memory, and the tile is stored coalesced.
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_merge_kernel(const void* A, uint32_t na, const void* C,
                                                        const uint32_t* nc_ptr, void* out,
                                                        uint64_t* d_count) {
     using K = typename std::conditional<K64, uint64_t, uint32_t>::type;
+    __shared__ K sm[kMergeTile];   // A slice then C slice
+    __shared__ K so[kMergeTile];   // merged tile
+    __shared__ uint32_t bounds[4];
     const K* a = (const K*)A;
     const K* c = (const K*)C;
     const uint32_t nc = *nc_ptr, total = na + nc;
-    const uint64_t diag64 = ((uint64_t)blockIdx.x * 256 + threadIdx.x) * kMergeItems;
     if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = total;
-    if (diag64 >= total) return;
-    const uint32_t diag = (uint32_t)diag64;
-    uint32_t lo = diag > nc ? diag - nc : 0, hi = min(diag, na);
-    while (lo < hi) {  // i = number of A keys among the first diag merged keys
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < __ldg(c + (diag - 1 - mid))) lo = mid + 1;
-        else hi = mid;
+    const uint64_t t0 = (uint64_t)blockIdx.x * kMergeTile;
+    if (t0 >= total) return;
+    const uint32_t d0 = (uint32_t)t0, d1 = (uint32_t)min(t0 + kMergeTile, (uint64_t)total);
+    if (threadIdx.x < 2) {
+        const uint32_t d = threadIdx.x ? d1 : d0;
+        const uint32_t i = merge_split(a, na, c, nc, d);
+        bounds[2 * threadIdx.x] = i;
+        bounds[2 * threadIdx.x + 1] = d - i;
     }
-    uint32_t i = lo, j = diag - lo;
-    K* o = (K*)out + diag;
-    for (uint32_t k = 0; k < kMergeItems && diag + k < total; ++k) {
-        const bool take_a = j >= nc || (i < na && __ldg(a + i) < __ldg(c + j));
-        o[k] = take_a ? __ldg(a + i++) : __ldg(c + j++);
+    __syncthreads();
+    const uint32_t a0 = bounds[0], c0 = bounds[1], a1 = bounds[2], c1 = bounds[3];
+    const uint32_t la = a1 - a0, lcn = c1 - c0;  // la + lcn = d1 - d0
+    for (uint32_t k = threadIdx.x; k < la; k += 256) sm[k] = __ldg(a + a0 + k);
+    for (uint32_t k = threadIdx.x; k < lcn; k += 256) sm[la + k] = __ldg(c + c0 + k);
+    __syncthreads();
+    const uint32_t n = la + lcn;
+    const uint32_t dd = min(threadIdx.x * kMergeItems, n);
+    uint32_t i = merge_split(sm, la, sm + la, lcn, dd), j = dd - i;
+    for (uint32_t k = 0; k < kMergeItems && dd + k < n; ++k) {
+        const bool take_a = j >= lcn || (i < la && sm[i] < sm[la + j]);
+        so[dd + k] = take_a ? sm[i++] : sm[la + j++];
     }
+    __syncthreads();
+    K* o = (K*)out + d0;
+    for (uint32_t k = threadIdx.x; k < n; k += 256) __stcs(o + k, so[k]);
 }
 
 // ------------------------------------------------------------------------------ launchers
@@ -1395,8 +1424,7 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (k64) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
     else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
-    const uint64_t threads = (nl + ns + kMergeItems - 1) / kMergeItems;
-    const unsigned mgrid = (unsigned)((threads + 255) / 256);
+    const unsigned mgrid = (unsigned)((nl + ns + kMergeTile - 1) / kMergeTile);
     if (k64) lc_merge_kernel<true><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
     else lc_merge_kernel<false><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
     lc_detail::count_launch(6);
