@@ -30,7 +30,7 @@ def main(path: str, out: str, alg_bytes: float = 1086177040.0, steps: int = 5, w
         f"lc_decode_kernel full-list launches ({warmup} warm-up + {steps} timed): "
         + ", ".join(f"{t:.1f} us" for t in full),
         f"  mean of the timed launches: {mean:.1f} us -> {alg_bytes / (mean * 1e-6) / 1e9:.0f} GB/s algorithmic",
-        f"lc_decode_kernel span launches inside lc_decode_host (e2e): {len(spans)}, "
+        f"other lc_decode_kernel launches (e2e spans, intersect/union decodes): {len(spans)}, "
         f"mean {sum(spans) / max(len(spans), 1):.1f} us",
         "a bench step is exactly one lc_decode_kernel launch (100% of the timed region); torch",
         "kernels (compare/index) are the post-timing bit-exact checks, outside the timed region.",
