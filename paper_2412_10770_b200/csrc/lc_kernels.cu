@@ -312,6 +312,44 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
 
+// Four windows at once: keys [wb, wb + 128), lane handles wb + 32 q + lane (q = 0..3).  One
+// candidate load / advance vote serves four quarters when fewer than 32 segment starts fall
+// inside; otherwise two pair steps.  w4 = quad index (windows 4 w4 .. 4 w4 + 3).
+template <bool K64, uint32_t B, bool CHECK>
+__device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
+                                            uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                            uint32_t w4, uint32_t lane, uint32_t lmask,
+                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
+    if (__ballot_sync(kFull, x < 128) == kFull) {  // >= 32 boundaries in 128 keys
+        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls, eps,
+                                   outw);
+        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask, lw,
+                                   ls, eps, (uint8_t*)outw + 64 * kw);
+        return;
+    }
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 128));
+    uint32_t off = wb - sb, jq = jb;  // uniform: distance to the last start, segment base
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x - 32 * q));  // starts in quarter q
+        const uint32_t m = P & lmask;
+        const uint32_t d = m ? lane - (31 - __clz(m)) : off + lane;
+        const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
+        LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
+        put<K64>((uint8_t*)outw + 32 * kw * q, pr.x,
+                 pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - eps));
+        off = P ? __clz(P) + 1 : off + 32;
+        jq += __popc(P);
+    }
+    jb = min(jb + adv, jlast + 1);  // see decode_window
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+}
+
 // SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key, so the
 // kernel is issue-bound: cap registers at 40 for 6 resident CTAs and skip the L2 prefetch
 // (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch);
@@ -364,12 +402,12 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
         uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
         if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
 #pragma unroll 1
-            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
+            for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    decode_pair<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
-                                               lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
-                if (g == 4 && has_next && lane == 0) {  // next chunk's hint pair has landed:
+                for (uint32_t k = 0; k < 2; ++k)
+                    decode_quad<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k), g + k,
+                                               lane, lmask, lw, ls, a.eps, outl + 128 * kw * k);
+                if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
                     const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
                     const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
                     bulk_prefetch_l2(sec.starts + npj, ((ncs + 3) & ~3u) * 4);
