@@ -197,6 +197,34 @@ def _cpu_baseline(blob, keys, reps=3):
     return t, nt
 
 
+def _cpu_rows(blob, keys, idx, rs, a_keys, probes):
+    """The oracle timed beside every GPU row on bounded samples (host cores; OpenMP for the
+    C oracle, numpy for the set-operation definitions)."""
+    import os as _os
+
+    from oracle import native as orc
+    from oracle import setops
+
+    def rate(fn, units):
+        t0 = time.perf_counter()
+        fn()
+        return units / (time.perf_counter() - t0)
+
+    mi, mr = 2_000_000, 200_000
+    return {
+        "cores": _os.cpu_count(),
+        "sample": f"access {mi} idx, range {mr} x 64, next_geq {probes.size} probes, "
+                  f"intersect/union {a_keys.size} x {keys.size} keys",
+        "access_lookups_per_s": rate(lambda: orc.access(blob, idx[:mi]), mi),
+        "ranges_per_s": rate(lambda: orc.range_decode(blob, rs[:mr], 64), mr),
+        "quantile_exact_per_s": rate(lambda: orc.access(blob, idx[:mi]), mi),
+        "quantile_approx_per_s": rate(lambda: orc.predict(blob, idx[:mi // 4]), mi // 4),
+        "next_geq_per_s": rate(lambda: setops.next_geq(keys, probes), probes.size),
+        "intersect_ms": 1e3 / rate(lambda: setops.intersect(a_keys, keys), 1),
+        "union_ms": 1e3 / rate(lambda: setops.union(a_keys, keys), 1),
+    }
+
+
 def _time_launches(fn, stream, steps, warmup):
     """W untimed + K timed launches of fn on `stream`; per-launch CUDA events. Returns
     (total seconds of the timed region, per-launch seconds list)."""
@@ -359,9 +387,14 @@ def run_gpu(args):
             raise SystemExit("intersection count mismatch")
         if int(u_cnt.item()) != a_keys.size + k5.size - want_cnt:
             raise SystemExit("union count mismatch")
+        cpu_rows = None
+        if ws == 1 and not args.no_cpu:
+            cpu_rows = _cpu_rows(b5, k5, idx, rs, a_keys,
+                                 d_probe[:2_000_000].cpu().numpy().view(np.uint64))
         access = {
             "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
                         "lookups; 1e7 ranges x 64 keys",
+            "cpu_oracle": cpu_rows,
             "quantiles_exact_per_s": mq / statistics.mean(pqe),
             "quantiles_approx_per_s": mq / statistics.mean(pqa),
             "next_geq_per_s": mq / statistics.mean(png),
