@@ -7,7 +7,9 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRCS = [os.path.join(PKG, "csrc", f) for f in ("lc_host.cpp", "lc_kernels.cu")]
-DEPS = SRCS + [os.path.join(PKG, "csrc", "lc_internal.h"), os.path.join(ROOT, "include", "lc.h")]
+DEPS = SRCS + [os.path.join(PKG, "csrc", f) for f in (
+    "lc_internal.h", "lc_common.cuh", "lc_decode.cuh", "lc_gather.cuh", "lc_setops.cuh")] + [
+    os.path.join(ROOT, "include", "lc.h")]
 LIB = os.path.join(PKG, "liblc.so")
 
 NVCC_FLAGS = [

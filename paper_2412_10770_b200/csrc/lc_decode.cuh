@@ -1,0 +1,252 @@
+// lc_decode.cuh -- full decode: staging pages, window / pair / quad steps, kernel
+// Internal part of lc_kernels.cu: included inside its anonymous namespace (one translation
+// unit, so the launch tables and the bounds-check counter keep internal linkage).
+#pragma once
+
+// --------------------------------------------------------------------------- full decode
+struct DecodeArgs {
+    Sections sec;
+    void* out;         // receives keys [i0, i1)
+    uint32_t i0, i1;   // i0 % 1024 == 0
+    uint32_t chunk0;   // i0 / 1024
+    uint32_t nchunks;  // ceil((i1 - i0) / 1024)
+    uint32_t eps;
+    uint32_t warp_bytes;  // shared memory per warp
+    uint32_t nwords;      // W (words section length)
+};
+
+// Per-warp shared-memory page: [mbarrier | starts (kSegCap+4) | params kSegCap | words]
+__host__ __device__ constexpr uint32_t page_starts_off() { return 16; }
+__host__ __device__ constexpr uint32_t page_params_off() { return 16 + 4 * (kSegCap + 4); }
+__host__ __device__ constexpr uint32_t page_words_off() { return page_params_off() + 16 * kSegCap; }
+__host__ __device__ constexpr uint32_t warp_bytes_for(uint32_t b) {
+    return (page_words_off() + 4 * (b ? 32 * b + 4 : 0) + 127) & ~127u;
+}
+
+struct Page {
+    uint64_t* bar;
+    uint32_t* sS;         // starts[pj .. pj + cs)
+    ulonglong2* sP;       // params[pj .. pj + cp)
+    uint32_t* sW;         // the chunk's residual words
+    uint32_t pj, cp;
+    uint32_t phase;
+#ifdef LC_DEBUG_BOUNDS
+    uint32_t cs, nw;  // staged starts / words entries
+#endif
+};
+
+// Stage starts[pj, pj + cs) and params[pj, pj + cp) (plus, when wbytes != 0, the chunk's words)
+// with TMA bulk copies; cs covers one start past the params so every window candidate
+// (clamped at jlast + 1) is a real start.  Lane 0 issues, the warp waits on the mbarrier.
+__device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t from, uint32_t jlast,
+                                      const uint32_t* wsrc, uint32_t wbytes, uint32_t lane) {
+    __syncwarp();  // every lane is done reading the previous contents
+    pg.pj = from & ~3u;
+    pg.cp = min(kSegCap, jlast + 1 - pg.pj);
+#ifdef LC_DEBUG_BOUNDS
+    pg.cs = (min(kSegCap + 4, jlast + 2 - pg.pj) + 3) & ~3u;
+    if (wbytes) pg.nw = wbytes / 4;
+#endif
+    if (lane == 0) {
+        const uint32_t cs = min(kSegCap + 4, jlast + 2 - pg.pj);
+        const uint32_t sbytes = ((cs + 3) & ~3u) * 4, pbytes = pg.cp * 16;
+        mbar_expect_tx(pg.bar, sbytes + pbytes + wbytes);
+        bulk_g2s(pg.sS, sec.starts + pg.pj, sbytes, pg.bar);
+        bulk_g2s(pg.sP, sec.params + pg.pj, pbytes, pg.bar);
+        if (wbytes) bulk_g2s(pg.sW, wsrc, wbytes, pg.bar);
+    }
+    mbar_wait(pg.bar, pg.phase);
+    pg.phase ^= 1;
+}
+
+// Decode one 32-key window [wb, wb + 32) of a chunk, lane = key.  w is the window index in
+// the chunk (selects the residual words).  Segment j of each lane: boundaries inside the
+// window form a bitmask (REDUX.OR over the next 32 segment starts); popc/clz give the
+// segment and the offset d = i - s_j with no search.  key = base + t with
+// t = floor(slope d / 2^32) + u - eps = K[i] - K[s_j] in [0, 2^32) (FORMAT F2 anchor + guard).
+template <bool K64, uint32_t B, bool CHECK, bool FULL>
+__device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
+                                              uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                              uint32_t w, uint32_t lane, uint32_t lmask,
+                                              uint32_t lw, uint32_t ls, uint32_t eps,
+                                              void* outw, uint32_t valid) {
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;  // next start
+    const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x));
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 32));
+    const uint32_t m = P & lmask;  // boundaries at or before this lane's key
+    const uint32_t seg = jb + __popc(m);
+    const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
+    const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
+    LC_CHECK(B && (FULL || lane < valid), w * B + lw + 1, pg.nw);
+    const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - eps);
+    if (FULL || lane < valid) put<K64>(outw, pr.x, t);
+    // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
+    // the advance there so jb stays a valid staged index
+    jb = min(jb + adv, jlast + 1);
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+}
+
+// Two windows at once: keys [wb, wb + 64), lane handles wb + lane and wb + 32 + lane.  One
+// candidate load / vote serves both halves when fewer than 32 segment starts fall inside;
+// otherwise it falls back to two single windows.  w2 = pair index (windows 2 w2, 2 w2 + 1).
+template <bool K64, uint32_t B, bool CHECK>
+__device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint32_t& jb,
+                                            uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                            uint32_t w2, uint32_t lane, uint32_t lmask,
+                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
+    const uint32_t inside = __ballot_sync(kFull, x < 64);
+    if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
+        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
+                                           ls, eps, outw, 32);
+        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
+                                           lmask, lw, ls, eps, (uint8_t*)outw + 32 * kw, 32);
+        return;
+    }
+    const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));       // starts in (wb, wb+32)
+    const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));  // starts in [wb+32, wb+64)
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
+    const uint32_t off0 = wb - sb;                                      // uniform
+    const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;               // uniform
+    const uint32_t jB = jb + __popc(PA);                                // uniform
+    const uint32_t mA = PA & lmask;
+    const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+    const ulonglong2 pA = pg.sP[LC_BOUND(true, jb + __popc(mA) - pg.pj, pg.cp)];
+    const uint32_t mB = PB & lmask;
+    const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+    const ulonglong2 pB = pg.sP[LC_BOUND(true, jB + __popc(mB) - pg.pj, pg.cp)];
+    LC_CHECK(B, (2 * w2 + 1) * B + lw + 1, pg.nw);
+    const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - eps);
+    const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps);
+    put<K64>(outw, pA.x, tA);
+    put<K64>((uint8_t*)outw + 32 * kw, pB.x, tB);
+    jb = min(jb + adv, jlast + 1);  // see decode_window
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+}
+
+// Four windows at once: keys [wb, wb + 128), lane handles wb + 32 q + lane (q = 0..3).  One
+// candidate load / advance vote serves four quarters when fewer than 32 segment starts fall
+// inside; otherwise two pair steps.  w4 = quad index (windows 4 w4 .. 4 w4 + 3).
+template <bool K64, uint32_t B, bool CHECK>
+__device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
+                                            uint32_t& sb, uint32_t jlast, uint32_t wb,
+                                            uint32_t w4, uint32_t lane, uint32_t lmask,
+                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
+        stage(pg, sec, jb, jlast, nullptr, 0, lane);
+    const uint32_t cand = min(jb + 1 + lane, jlast + 1);
+    const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
+    if (__ballot_sync(kFull, x < 128) == kFull) {  // >= 32 boundaries in 128 keys
+        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls, eps,
+                                   outw);
+        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask, lw,
+                                   ls, eps, (uint8_t*)outw + 64 * kw);
+        return;
+    }
+    const uint32_t adv = __popc(__ballot_sync(kFull, x <= 128));
+    uint32_t off = wb - sb, jq = jb;  // uniform: distance to the last start, segment base
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(x - 32 * q));  // starts in quarter q
+        const uint32_t m = P & lmask;
+        const uint32_t d = m ? lane - (31 - __clz(m)) : off + lane;
+        const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
+        LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
+        put<K64>((uint8_t*)outw + 32 * kw * q, pr.x,
+                 pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - eps));
+        off = P ? __clz(P) + 1 : off + 32;
+        jq += __popc(P);
+    }
+    jb = min(jb + adv, jlast + 1);  // see decode_window
+    sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+}
+
+// SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key, so the
+// kernel is issue-bound: cap registers at 40 for 6 resident CTAs and skip the L2 prefetch
+// (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch);
+// dense lists keep 5 resident CTAs (<= 48 registers).
+template <bool K64, uint32_t B, bool SPARSE>
+__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(const DecodeArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* base = smem + warp * a.warp_bytes;
+    Page pg;
+    pg.bar = (uint64_t*)base;
+    pg.sS = (uint32_t*)(base + page_starts_off());
+    pg.sP = (ulonglong2*)(base + page_params_off());
+    pg.sW = (uint32_t*)(base + page_words_off());
+    pg.phase = 0;
+    if (lane == 0) mbar_init(pg.bar);
+    __syncwarp();
+
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lw = (lane * B) >> 5, ls = (lane * B) & 31;  // lane's field in a window
+    const uint32_t lmask = lanemask_le();
+    const uint32_t nwarps = gridDim.x * kWarpsPerCta;
+    const Sections sec = a.sec;
+
+    uint32_t c = blockIdx.x * kWarpsPerCta + warp;
+    // hint pair of the warp's next chunk, loaded one chunk ahead (hides a DRAM round trip)
+    uint32_t nj0 = 0, njl = 0;
+    if (c < a.nchunks) {
+        nj0 = __ldg(sec.hint + a.chunk0 + c);
+        njl = __ldg(sec.hint + a.chunk0 + c + 1);
+    }
+    for (; c < a.nchunks; c += nwarps) {
+        const uint32_t h = a.chunk0 + c;
+        const uint32_t key0 = h << 10;
+        const uint32_t nk = min(1024u, a.i1 - key0);
+        const uint32_t j0 = nj0;
+        const uint32_t jlast = njl;  // last segment the chunk can touch
+        if (c + nwarps < a.nchunks) {
+            nj0 = __ldg(sec.hint + h + nwarps);
+            njl = __ldg(sec.hint + h + nwarps + 1);
+        }
+        const uint32_t wbytes = B ? ((((nk * B + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
+        stage(pg, sec, j0, jlast, sec.words + (size_t)h * 32 * B, wbytes, lane);
+        const bool has_next = !SPARSE && c + nwarps < a.nchunks;
+        if (B && has_next && lane == 0)  // next chunk's residual words -> L2 now
+            bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
+                             min(32 * B * 4 + 16, (a.nwords - (h + nwarps) * 32 * B) * 4));
+        uint32_t jb = j0;                // segment holding the window's first key
+        uint32_t sb = pg.sS[LC_BOUND(true, j0 - pg.pj, pg.cs)];  // its start
+        uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
+        if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
+#pragma unroll 1
+            for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
+#pragma unroll
+                for (uint32_t k = 0; k < 2; ++k)
+                    decode_quad<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k), g + k,
+                                               lane, lmask, lw, ls, a.eps, outl + 128 * kw * k);
+                if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
+                    const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
+                    const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
+                    bulk_prefetch_l2(sec.starts + npj, ((ncs + 3) & ~3u) * 4);
+                    bulk_prefetch_l2(sec.params + npj, min(kSegCap, njl + 1 - npj) * 16);
+                }
+            }
+        } else if (nk == 1024) {  // dense chunk: paged
+#pragma unroll 1
+            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    decode_pair<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
+                                              lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
+            }
+        } else {  // ragged tail chunk
+            for (uint32_t w = 0; 32 * w < nk; ++w)
+                decode_window<K64, B, true, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane,
+                                                   lmask, lw, ls, a.eps, outl + 32 * kw * w,
+                                                   nk - 32 * w);
+        }
+    }
+}
+

@@ -1,0 +1,434 @@
+// lc_gather.cuh -- range decode (generic + cp.async ring for 64 keys), access, quantiles
+// Internal part of lc_kernels.cu: included inside its anonymous namespace (one translation
+// unit, so the launch tables and the bounds-check counter keep internal linkage).
+#pragma once
+
+// -------------------------------------------------------------------------- range decode
+struct RangeArgs {
+    Sections sec;
+    const uint64_t* start;
+    void* out;
+    uint32_t* err;
+    uint64_t q;
+    uint32_t len, n, L, b, eps, mask;
+    uint32_t nwords;  // W
+};
+
+// j = max{t in [hint[i>>10], hint[(i>>10)+1]] : starts[t] <= i} (Table I caption)
+__device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i, uint64_t keep) {
+    uint32_t lo = ldh(sec.hint + (i >> 10), keep), hi = ldh(sec.hint + (i >> 10) + 1, keep);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (ldh(sec.starts + mid, keep) <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// residual field of key i read from global words (two loads + funnel shift)
+__device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b,
+                                             uint64_t pol) {
+    const uint64_t bit = (uint64_t)i * b;
+    uint32_t wi = (uint32_t)(bit >> 5);
+    if (LC_BOUND(true, wi + 1, sec.W) == 0) wi = 0;  // (only a checked build can take this)
+    const uint32_t* wp = sec.words + wi;
+    return make_uint2(ldh(wp, pol), ldh(wp + 1, pol));
+}
+__device__ __forceinline__ uint32_t field_of(uint2 w, uint32_t i, uint32_t b, uint32_t mask) {
+    return __funnelshift_r(w.x, w.y, (i * b) & 31) & mask;
+}
+
+// One warp decodes 32 ranges.  Phase 1: lane r binary-searches the segment of range r's first
+// key (32 independent searches in flight).  Phase 2: the warp decodes the ranges one after
+// another with the window scheme of the full decode (64 keys per step, 2 keys per lane); the
+// next range's candidate starts and residual words are fetched while the current range is
+// decoded, so each range waits on a single dependent load (the params gather).
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    if (r0 >= a.q) return;  // warp-uniform
+    const Sections sec = a.sec;
+    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L, eps = a.eps;
+    const uint32_t lmask = lanemask_le();
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+
+    // ---- phase 1: lane-parallel search
+    uint32_t rs = 0, j = 0, sj = 0, ok = 0;
+    if (r0 + lane < a.q) {
+        const uint64_t s64 = __ldg(a.start + r0 + lane);
+        if (s64 <= a.n && len <= a.n - s64) {
+            ok = 1;
+            rs = (uint32_t)s64;
+            j = seg_search(sec, rs, keep);
+            sj = ldh(sec.starts + j, keep);
+        } else if (a.err) {
+            atomicOr(a.err, 1u);
+        }
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+
+    // candidate starts and first-step residual words of range k
+    uint32_t nx;
+    uint2 nwA = make_uint2(0, 0), nwB = make_uint2(0, 0);
+    auto fetch = [&](uint32_t k) {
+        const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
+        nx = ldh(sec.starts + min(jk + 1 + lane, L), keep) - rk;
+        if (b && len >= 64) {
+            nwA = field_words(sec, rk + lane, b, once);
+            nwB = field_words(sec, rk + 32 + lane, b, once);
+        }
+    };
+    fetch(0);
+    for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t rk = __shfl_sync(kFull, rs, k);
+        uint32_t jb = __shfl_sync(kFull, j, k);
+        uint32_t sb = __shfl_sync(kFull, sj, k);
+        const uint32_t okk = __shfl_sync(kFull, ok, k);
+        const uint32_t x = nx;
+        const uint2 wA = nwA, wB = nwB;
+        if (k + 1 < nr) fetch(k + 1);
+        uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * len * kw;
+        if (!okk) {
+            for (uint32_t e = lane; e < len; e += 32) {
+                if (K64) __stcs((unsigned long long*)outk + e, 0ull);
+                else __stcs((unsigned int*)outk + e, 0u);
+            }
+            continue;
+        }
+        uint32_t w0 = 0;
+        // first 64 keys as one pair step, from the prefetched candidates and words
+        if (len >= 64 && __ballot_sync(kFull, x < 64) != kFull) {
+            const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
+            const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
+            const uint32_t adv = __popc(__ballot_sync(kFull, x <= 64));
+            const uint32_t off0 = rk - sb;
+            const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
+            const uint32_t mA = PA & lmask, mB = PB & lmask;
+            const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+            const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+            const ulonglong2 pA = ldh(sec.params + LC_BOUND(true, jb + __popc(mA), L), once);
+            const ulonglong2 pB =
+                ldh(sec.params + LC_BOUND(true, jb + __popc(PA) + __popc(mB), L), once);
+            const uint32_t uA = b ? field_of(wA, rk + lane, b, mask) : 0;
+            const uint32_t uB = b ? field_of(wB, rk + 32 + lane, b, mask) : 0;
+            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
+            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+            if (len == 64) continue;
+            jb += adv;
+            sb = ldh(sec.starts + min(jb, L), keep);
+            w0 = 64;
+        }
+        while (w0 < len) {  // remaining keys: 32-key windows through L1/L2
+            const uint32_t wb = rk + w0, rem = len - w0;
+            const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
+            const uint32_t P = __reduce_or_sync(kFull, bit_or_zero(xw));
+            const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
+            const uint32_t m = P & lmask;
+            const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sb + lane;
+            if (lane < rem) {
+                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
+                const uint32_t u =
+                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
+            }
+            jb += adv;
+            sb = ldh(sec.starts + min(jb, L), keep);
+            w0 += 32;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- range decode, len == 64
+// cp.async (LDGSTS) 16-byte copy with zero fill when `valid` is false
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+#ifndef LC_R64_SEGS
+#define LC_R64_SEGS 8
+#endif
+// params staged per range: 1 + boundaries in 64 keys is <= 8 for 99.6% of config-5 ranges
+// (max 10); a range needing more is decoded through L2
+constexpr uint32_t kR64Segs = LC_R64_SEGS;
+constexpr uint32_t kR64StartGroups = (kR64Segs + 3 + 3) / 4;  // starts[j+1 .. j+kR64Segs] from a 16-B boundary
+#ifndef LC_R64_SLOTS
+#define LC_R64_SLOTS 4
+#endif
+constexpr uint32_t kR64Slots = LC_R64_SLOTS;  // ring depth per warp (ranges gathered ahead)
+__host__ __device__ constexpr uint32_t r64_words(uint32_t b) {  // staged residual words
+    return ((((64 * b + 31) >> 5) + 2 + 3) + 3) & ~3u;
+}
+__host__ __device__ constexpr uint32_t r64_bytes(uint32_t b) {  // per slot: params|starts|words
+    return 16 * kR64Segs + 16 * kR64StartGroups + 4 * r64_words(b);
+}
+
+// 64-key ranges (BASELINE config 5).  Phase 1: lane r binary-searches range r's first segment
+// (32 independent searches).  Phase 2: the warp walks its 32 ranges through a 4-slot shared-
+// memory ring: the lanes gather range k+3's params[j..j+8), starts[j+1..j+9) and residual
+// words with cp.async (one 16-byte copy per lane) while range k is decoded from smem with the
+// pair-window scheme, so the decode never waits on a dependent global load.  A range crossing
+// more than 7 segment starts is decoded through L2 instead.
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
+    if (r0 >= a.q) return;  // warp-uniform
+    const Sections sec = a.sec;
+    const uint32_t b = a.b, mask = a.mask, L = a.L, eps = a.eps;
+    const uint32_t RB = r64_bytes(b), nw16 = r64_words(b) / 4;
+    uint8_t* ring = smem + warp * kR64Slots * RB;
+    const uint32_t lmask = lanemask_le();
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+
+    // ---- phase 1: lane-parallel search
+    uint32_t rs = 0, j = 0, sj = 0, ok = 0;
+    if (r0 + lane < a.q) {
+        const uint64_t s64 = __ldg(a.start + r0 + lane);
+        if (s64 <= a.n && 64 <= a.n - s64) {
+            ok = 1;
+            rs = (uint32_t)s64;
+            j = seg_search(sec, rs, keep);
+            sj = ldh(sec.starts + j, keep);
+        } else if (a.err) {
+            atomicOr(a.err, 1u);
+        }
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+
+    // gather range k into ring slot k % kR64Slots: copy groups 0..11 = params, 12..16 = starts,
+    // then words; group g is done by lane g % 32.  Each lane's role (source section, offset in
+    // the slot) is fixed, so per range it only adds the range's uniform section offset.
+    const uint32_t ngroups = kR64Segs + kR64StartGroups + nw16;
+    struct Role {
+        const uint8_t* src;  // section base + 16 t
+        uint32_t dst, kind, t;
+    };
+    auto role_of = [&](uint32_t g) {
+        Role r;
+        const uint32_t gw = kR64Segs + kR64StartGroups;
+        if (g < kR64Segs) r = {(const uint8_t*)(sec.params + g), 16 * g, 0, g};
+        else if (g < gw)
+            r = {(const uint8_t*)(sec.starts + 4 * (g - kR64Segs)), 16 * g, 1, g - kR64Segs};
+        else
+            r = {(const uint8_t*)(sec.words + 4 * (g - gw)), 16 * g, 2, g - gw};
+        return r;
+    };
+    const Role ra = role_of(lane), rb = role_of(lane + 32);
+    const bool has_a = lane < ngroups, has_b = lane + 32 < ngroups;
+    auto copy = [&](const Role& r, uint8_t* slot, uint32_t jk, uint32_t s0, uint32_t w0) {
+        const uint64_t off = r.kind == 0 ? (uint64_t)jk * 16 : r.kind == 1 ? (uint64_t)s0 * 4
+                                                                            : (uint64_t)w0 * 4;
+        const bool valid = r.kind == 0 ? jk + r.t < L
+                                       : (r.kind == 1 || w0 + 4 * r.t + 4 <= a.nwords);
+        cp16(slot + r.dst, r.src + off, valid);
+    };
+    auto issue = [&](uint32_t k) {
+        if (k < nr) {
+            const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
+            const uint32_t okk = __shfl_sync(kFull, ok, k);
+            uint8_t* slot = ring + (k % kR64Slots) * RB;
+            if (okk) {
+                const uint32_t s0 = (jk + 1) & ~3u;
+                const uint32_t w0 = (uint32_t)(((uint64_t)rk * b) >> 5) & ~3u;
+                if (has_a) copy(ra, slot, jk, s0, w0);
+                if (has_b) copy(rb, slot, jk, s0, w0);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
+    };
+    for (uint32_t k = 0; k + 1 < kR64Slots; ++k) issue(k);
+
+    for (uint32_t k = 0; k < nr; ++k) {
+        issue(k + kR64Slots - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kR64Slots - 1) : "memory");
+        __syncwarp();
+        const uint32_t rk = __shfl_sync(kFull, rs, k);
+        const uint32_t jk = __shfl_sync(kFull, j, k);
+        const uint32_t sb = __shfl_sync(kFull, sj, k);
+        const uint32_t okk = __shfl_sync(kFull, ok, k);
+        uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * 64 * kw;
+        if (!okk) {
+            put<K64>(outk + lane * kw, 0, 0);
+            put<K64>(outk + (32 + lane) * kw, 0, 0);
+            __syncwarp();
+            continue;
+        }
+        const uint8_t* rsm = ring + (k % kR64Slots) * RB;
+        const ulonglong2* P = (const ulonglong2*)rsm;
+        const uint32_t* S = (const uint32_t*)(rsm + 16 * kR64Segs) + ((jk + 1) & 3);  // starts[jk+1+t]
+        const uint32_t x = (lane < kR64Segs && jk + 1 + lane <= L) ? S[lane] - rk : kFull;
+        const uint32_t inside = __ballot_sync(kFull, x < 64);
+        if (__popc(inside) < kR64Segs) {
+            const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));
+            const uint32_t PB = __reduce_or_sync(kFull, bit_or_zero(x - 32));
+            const uint32_t off0 = rk - sb;
+            const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;
+            const uint32_t mA = PA & lmask, mB = PB & lmask;
+            const uint32_t dA = mA ? lane - (31 - __clz(mA)) : off0 + lane;
+            const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
+            const ulonglong2 pA = P[LC_BOUND(true, __popc(mA), kR64Segs)];
+            const ulonglong2 pB = P[LC_BOUND(true, __popc(PA) + __popc(mB), kR64Segs)];
+            uint32_t uA = 0, uB = 0;
+            if (b) {
+                const uint32_t* Wd = (const uint32_t*)(rsm + 16 * (kR64Segs + kR64StartGroups));
+                const uint64_t wbase = ((((uint64_t)rk * b) >> 5) & ~3ull) << 5;
+                const uint32_t bA = (uint32_t)((uint64_t)(rk + lane) * b - wbase);
+                const uint32_t bB = bA + 32 * b;
+                LC_CHECK(true, (bB >> 5) + 1, r64_words(b));
+                uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
+                uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
+            }
+            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
+            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+        } else {  // dense range: two 32-key windows through L2
+            uint32_t jb = jk, sbw = sb;
+            for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
+                const uint32_t wb = rk + w0;
+                const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
+                const uint32_t Pm = __reduce_or_sync(kFull, bit_or_zero(xw));
+                const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
+                const uint32_t m = Pm & lmask;
+                const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
+                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
+                const uint32_t u =
+                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
+                jb += adv;
+                sbw = ldh(sec.starts + min(jb, L), keep);
+            }
+        }
+        __syncwarp();  // the slot is refilled by the next issue()
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------- random access
+struct AccessArgs {
+    Sections sec;
+    const uint64_t* idx;
+    void* out;
+    uint32_t* err;
+    uint64_t q;
+    uint32_t n, b, eps, mask;
+};
+
+constexpr uint32_t kAccessPerThread = 2;
+
+// Dec(K^c)[i] per query (Table I): hint bracket, binary search
+// over starts, one params gather, one residual field.  Each thread serves kAccessPerThread
+// queries whose dependent load chains are interleaved; the residual words do not depend on
+// the segment and are fetched before the search.
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
+    const uint64_t t0 = (uint64_t)blockIdx.x * (256 * kAccessPerThread) + threadIdx.x;
+    const Sections sec = a.sec;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    uint32_t i[kAccessPerThread], lo[kAccessPerThread], hi[kAccessPerThread];
+    bool live[kAccessPerThread];
+    uint2 w[kAccessPerThread];
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        const uint64_t t = t0 + 256 * k;
+        live[k] = false;
+        i[k] = 0;
+        lo[k] = hi[k] = 0;
+        w[k] = make_uint2(0, 0);
+        if (t < a.q) {
+            const uint64_t i64 = __ldcs(a.idx + t);
+            if (i64 < a.n) {
+                live[k] = true;
+                i[k] = (uint32_t)i64;
+            } else {
+                if (a.err) atomicOr(a.err, 1u);
+                if (K64) __stcs((unsigned long long*)a.out + t, 0ull);
+                else __stcs((unsigned int*)a.out + t, 0u);
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        if (live[k]) {
+            lo[k] = ldh(sec.hint + (i[k] >> 10), keep);
+            hi[k] = ldh(sec.hint + (i[k] >> 10) + 1, keep);
+            if (a.b) w[k] = field_words(sec, i[k], a.b, once);
+        }
+    }
+    for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
+        bool any = false;
+        uint32_t mid[kAccessPerThread], v[kAccessPerThread];
+#pragma unroll
+        for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+            mid[k] = (lo[k] + hi[k] + 1) >> 1;
+            v[k] = 0;
+            if (lo[k] < hi[k]) {
+                v[k] = ldh(sec.starts + mid[k], keep);
+                any = true;
+            }
+        }
+        if (!any) break;
+#pragma unroll
+        for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+            if (lo[k] < hi[k]) {
+                if (v[k] <= i[k]) lo[k] = mid[k];
+                else hi[k] = mid[k] - 1;
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        if (!live[k]) continue;
+        const uint32_t s = ldh(sec.starts + lo[k], keep);
+        const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
+        const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
+        const uint64_t t = t0 + 256 * k;
+        put<K64>((uint8_t*)a.out + t * (K64 ? 8 : 4), pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
+    }
+}
+
+// ----------------------------------------------------------------------------- quantiles
+struct QuantArgs {
+    Sections sec;
+    const uint64_t* k;
+    void* out;
+    uint32_t* err;
+    uint64_t m, q;
+    uint32_t n, b, eps, mask;
+};
+
+// The k-th q-quantile K[min(floor(N k / q), N - 1)] (§III-C; Table I): exact =
+// f(i) + Delta[i] through the hint bracket + binary search; approximate (EXACT = false) =
+// floor(f(i)) from the segment alone, no residual read, error <= eps.
+template <bool K64, bool EXACT>
+__global__ void __launch_bounds__(256) lc_quantile_kernel(const QuantArgs a) {
+    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (t >= a.m) return;
+    const Sections sec = a.sec;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    const uint64_t k = __ldg(a.k + t);
+    uint8_t* o = (uint8_t*)a.out + t * (K64 ? 8 : 4);
+    if (k > a.q) {
+        if (a.err) atomicOr(a.err, 1u);
+        put<K64>(o, 0, 0);
+        return;
+    }
+    const uint32_t i = (uint32_t)min((uint64_t)a.n * k / a.q, (uint64_t)a.n - 1);  // N k < 2^64
+    const uint32_t j = seg_search(sec, i, keep);
+    const uint32_t s = ldh(sec.starts + j, keep);
+    const ulonglong2 pr = ldh(sec.params + j, once);
+    if (EXACT) {
+        const uint32_t v = (a.b ? field_of(field_words(sec, i, a.b, once), i, a.b, a.mask) : 0) - a.eps;
+        put<K64>(o, pr.x, pred_plus(pr.y, i - s, v));
+    } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
+        const uint32_t t = pred_plus(pr.y, i - s, 0);
+        const uint64_t f = pr.x + t;
+        if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
+        else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
+    }
+}
+
