@@ -134,8 +134,10 @@ def test_decode_span_shards(lc):
         lc.decode_span(view, 0, 300_001)
 
 
-def test_decode_host_e2e(lc):
-    keys = make_keys(2, 1_000_003)
+@pytest.mark.parametrize("n", [1_000_003, 20_000_007, 40_000_000])
+def test_decode_host_e2e(lc, n):
+    """lc_decode_host: its 4 Mi-key spans (and the ragged last one) tile the list exactly."""
+    keys = make_keys(2, n)
     blob = lc.encode(keys, 127)
     h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
     d_blob = torch.empty(len(blob), dtype=torch.uint8, device=DEV)
