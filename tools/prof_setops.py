@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Time next_geq / intersect / union on config 5 (as in bench.py) for A/B runs (LC_LIB)."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    from paper_2412_10770_b200 import lc
+    from synth import make_keys
+
+    k5 = make_keys(5)
+    v5 = lc.View(lc.encode(k5, 127))
+    rng = np.random.default_rng(55)
+    probes = rng.integers(0, int(k5[-1]), 10_000_000, dtype=np.uint64)
+    d_probe = torch.from_numpy(probes.view(np.int64)).cuda()
+    na = 1_000_000
+    a = np.unique(np.concatenate([k5[np.sort(rng.choice(k5.size, na // 2, replace=False))],
+                                  rng.integers(0, int(k5[-1]), na // 2, dtype=np.uint64)]))
+    va = lc.View(lc.encode(a, 127))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def t(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(reps):
+            ev[0].record()
+            fn()
+            ev[1].record()
+            torch.cuda.synchronize()
+            best = min(best, ev[0].elapsed_time(ev[1]))
+        return best
+
+    gi, gk = lc.next_geq(v5, d_probe)
+    want = np.searchsorted(k5, probes, side="left")
+    assert np.array_equal(gi.cpu().numpy(), want.astype(np.int64)), "next_geq mismatch"
+    ms = t(lambda: lc.next_geq(v5, d_probe, gi, gk))
+    print(f"next_geq {ms:.3f} ms {probes.size / ms / 1e6:.3e} probes/s")
+    out, cnt = lc.intersect(va, v5)
+    ms = t(lambda: lc.intersect(va, v5, out=out, count=cnt))
+    print(f"intersect {ms:.4f} ms count {int(cnt.item())}")
+
+
+if __name__ == "__main__":
+    main()
