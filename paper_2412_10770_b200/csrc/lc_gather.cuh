@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         }
     }
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+    // first residual word of the range's staged words (16-byte aligned), per lane = range
+    const uint32_t wlo = (uint32_t)(((uint64_t)rs * b) >> 5) & ~3u;
 
     // gather range k into ring slot k % kR64Slots: copy groups 0..11 = params, 12..16 = starts,
     // then words; group g is done by lane g % 32.  Each lane's role (source section, offset in
@@ -230,12 +232,11 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     };
     auto issue = [&](uint32_t k) {
         if (k < nr) {
-            const uint32_t rk = __shfl_sync(kFull, rs, k), jk = __shfl_sync(kFull, j, k);
+            const uint32_t jk = __shfl_sync(kFull, j, k), w0 = __shfl_sync(kFull, wlo, k);
             const uint32_t okk = __shfl_sync(kFull, ok, k);
             uint8_t* slot = ring + (k % kR64Slots) * RB;
             if (okk) {
                 const uint32_t s0 = (jk + 1) & ~3u;
-                const uint32_t w0 = (uint32_t)(((uint64_t)rk * b) >> 5) & ~3u;
                 if (has_a) copy(ra, slot, jk, s0, w0);
                 if (has_b) copy(rb, slot, jk, s0, w0);
             }
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
     };
     for (uint32_t k = 0; k + 1 < kR64Slots; ++k) issue(k);
+    uint8_t* const out0 = (uint8_t*)a.out + ((size_t)r0 * 64 + lane) * kw;  // lane's slot, range 0
 
     for (uint32_t k = 0; k < nr; ++k) {
         issue(k + kR64Slots - 1);
@@ -252,10 +254,10 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         const uint32_t jk = __shfl_sync(kFull, j, k);
         const uint32_t sb = __shfl_sync(kFull, sj, k);
         const uint32_t okk = __shfl_sync(kFull, ok, k);
-        uint8_t* outk = (uint8_t*)a.out + (size_t)(r0 + k) * 64 * kw;
+        uint8_t* outk = out0 + (size_t)k * 64 * kw;
         if (!okk) {
-            put<K64>(outk + lane * kw, 0, 0);
-            put<K64>(outk + (32 + lane) * kw, 0, 0);
+            put<K64>(outk, 0, 0);
+            put<K64>(outk + 32 * kw, 0, 0);
             __syncwarp();
             continue;
         }
@@ -277,15 +279,15 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             uint32_t uA = 0, uB = 0;
             if (b) {
                 const uint32_t* Wd = (const uint32_t*)(rsm + 16 * (kR64Segs + kR64StartGroups));
-                const uint64_t wbase = ((((uint64_t)rk * b) >> 5) & ~3ull) << 5;
-                const uint32_t bA = (uint32_t)((uint64_t)(rk + lane) * b - wbase);
+                // bit offset inside the staged words; exact mod 2^32 (the true value is small)
+                const uint32_t bA = (rk + lane) * b - (__shfl_sync(kFull, wlo, k) << 5);
                 const uint32_t bB = bA + 32 * b;
                 LC_CHECK(true, (bB >> 5) + 1, r64_words(b));
                 uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
                 uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
             }
-            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
-            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+            put<K64>(outk, pA.x, pred_plus(pA.y, dA, uA - eps));
+            put<K64>(outk + 32 * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
         } else {  // dense range: two 32-key windows through L2
             uint32_t jb = jk, sbw = sb;
             for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
                 const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
                 const uint32_t u =
                     b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
-                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
+                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - eps));
                 jb += adv;
                 sbw = ldh(sec.starts + min(jb, L), keep);
             }

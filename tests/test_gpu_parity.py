@@ -427,3 +427,31 @@ def test_union_closed_form_and_edges(lc):
     _union_case(lc, np.array([5], np.uint64), np.array([5], np.uint64), 1, 1)
     a32 = np.arange(5, 2_000_000, 3, dtype=np.uint32)
     _union_case(lc, a32, make_keys(1, 1_000_000), 15, 63)
+
+
+def test_max_size_u32(lc):
+    """Maximum list size of the format (N = 2^32 - 1, FORMAT F1): u32 keys 0..N-1 at eps = 1,
+    so residual bit offsets reach 8.6e9 (> 2^32) and key indices the top of the 32-bit range.
+    Decode is checked element by element (in 2^28-key slices against arange on device);
+    access, range and quantile probe both ends and 2^31."""
+    N = (1 << 32) - 1
+    keys = np.arange(N, dtype=np.uint32)
+    blob = lc.encode(keys, 1)
+    del keys
+    view = lc.View(blob, device=DEV)
+    out = view.out_tensor(N)
+    lc.decode(view, out)
+    step = 1 << 28
+    for s in range(0, N, step):
+        e = min(s + step, N)
+        assert torch.equal(out[s:e], torch.arange(s, e, dtype=torch.int64, device=DEV).to(torch.int32)), s
+    del out
+    probe = [0, 1, (1 << 31) - 1, 1 << 31, N - 1025, N - 65, N - 2, N - 1]
+    idx = np.array(probe, np.uint64)
+    assert _host(lc.access(view, _dev(idx)), np.uint32).tolist() == probe
+    rs = np.array([0, (1 << 31) - 32, N - 64], np.uint64)
+    rg = _host(lc.range_decode(view, _dev(rs), 64), np.uint32)
+    assert all(rg[r].tolist() == list(range(int(s), int(s) + 64)) for r, s in enumerate(rs))
+    q = _host(lc.quantile(view, _dev(np.array([0, 1, 2], np.uint64)), 2), np.uint32)
+    assert q.tolist() == [0, N // 2, N - 1]
+    torch.cuda.empty_cache()
