@@ -81,6 +81,19 @@ int main() {
         cudaEventElapsedTime(&ms, a, b);
         printf("%s %.3f ms %.3e gathers/s\n", name, ms, q / (ms * 1e-3));
     };
+    {
+        size_t g = 0;
+        cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+        printf("default MaxL2FetchGranularity %zu\n", g);
+        for (size_t want : {32, 64, 128}) {
+            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, want);
+            cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+            char name[64];
+            snprintf(name, sizeof name, "ldg_l2fetch%zu(got %zu)", want, g);
+            run(name, [&] { gather<0><<<grid, 256>>>(src, idx, q, out); });
+        }
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 64);
+    }
     run("ldg", [&] { gather<0><<<grid, 256>>>(src, idx, q, out); });
     run("ld_plain", [&] { gather<1><<<grid, 256>>>(src, idx, q, out); });
     run("ld_nc_l1noalloc", [&] { gather<2><<<grid, 256>>>(src, idx, q, out); });
