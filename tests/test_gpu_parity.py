@@ -455,3 +455,53 @@ def test_max_size_u32(lc):
     q = _host(lc.quantile(view, _dev(np.array([0, 1, 2], np.uint64)), 2), np.uint32)
     assert q.tolist() == [0, N // 2, N - 1]
     torch.cuda.empty_cache()
+
+
+def test_concurrent_streams(lc):
+    """The library is stateless (lc.h): decodes / accesses of different blobs on different
+    streams, interleaved without synchronisation, each produce their own exact result."""
+    lists = [(make_keys(2, 3_000_001), 127), (make_keys(4, 2_000_003), 31),
+             (make_keys(1, 1_000_000), 63), (make_keys(3, 1_500_000), 255)]
+    views = [lc.View(lc.encode(k, e), device=DEV) for k, e in lists]
+    streams = [torch.cuda.Stream() for _ in lists]
+    outs = [v.out_tensor(v.n) for v in views]
+    idx = [torch.from_numpy(np.random.default_rng(i).integers(0, k.size, 100_000)).to(DEV)
+           for i, (k, _) in enumerate(lists)]
+    acc = [None] * len(lists)
+    torch.cuda.synchronize()  # inputs were staged on the default stream
+    for rep in range(3):
+        for i, (v, s) in enumerate(zip(views, streams)):
+            lc.decode(v, outs[i], stream=s)
+            acc[i] = lc.access(v, idx[i], stream=s)
+    torch.cuda.synchronize()
+    for i, (k, _) in enumerate(lists):
+        assert torch.equal(outs[i], _dev(k))
+        assert np.array_equal(_host(acc[i], k.dtype), k[idx[i].cpu().numpy()])
+
+
+def test_decode_host_two_threads(lc):
+    """lc_decode_host from two host threads at once (its internal copy streams are shared)."""
+    import threading
+    cases = [make_keys(2, 9_000_000), make_keys(5, 7_000_000)]
+    res = [None, None]
+
+    def run(t):
+        keys = cases[t]
+        blob = lc.encode(keys, 127)
+        s = torch.cuda.Stream()
+        h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
+        d_blob = torch.empty(len(blob), dtype=torch.uint8, device=DEV)
+        d_out = torch.empty(keys.size, dtype=torch.int64, device=DEV)
+        h_out = torch.empty(keys.size, dtype=torch.int64).pin_memory()
+        torch.cuda.synchronize()
+        for _ in range(3):
+            lc.decode_host(h_blob, d_blob, d_out, h_out, stream=s)
+        s.synchronize()
+        res[t] = np.array_equal(h_out.numpy().view(np.uint64), keys)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert res == [True, True]
