@@ -310,24 +310,34 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// ------------------------------------------------------------------------- random access
+// ------------------------------------------------------------- random access and quantiles
 struct AccessArgs {
     Sections sec;
-    const uint64_t* idx;
+    const uint64_t* idx;  // indices (kAccess) or quantile ranks k (kQuantile*)
     void* out;
     uint32_t* err;
-    uint64_t q;
+    uint64_t q;           // number of queries
+    uint64_t qdiv;        // quantile denominator q (kQuantile*)
     uint32_t n, b, eps, mask;
 };
 
-constexpr uint32_t kAccessPerThread = 2;
+enum AccessMode { kAccess = 0, kQuantileExact = 1, kQuantileApprox = 2 };
+// queries per thread: two interleaved chains when a residual gather follows the search (A/B:
+// +4% for exact quantiles), one for the params-only approximate quantile (-8% with two)
+__host__ __device__ constexpr uint32_t access_per_thread(int mode) {
+    return mode == kQuantileApprox ? 1 : 2;
+}
 
 // Dec(K^c)[i] per query (Table I): hint bracket, binary search
-// over starts, one params gather, one residual field.  Each thread serves kAccessPerThread
+// over starts, one params gather, one residual field.  Each thread serves access_per_thread()
 // queries whose dependent load chains are interleaved; the residual words do not depend on
-// the segment and are fetched before the search.
-template <bool K64>
+// the segment and are fetched before the search.  Quantiles use the same
+// path with i = min(floor(N k / q), N - 1): exact = f(i) + Delta[i]; approximate = floor(f(i))
+// from the segment alone, no residual read, error <= eps, saturated at the key width (L24).
+template <bool K64, int MODE>
 __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
+    constexpr bool kResidual = MODE != kQuantileApprox;
+    constexpr uint32_t kAccessPerThread = access_per_thread(MODE);
     const uint64_t t0 = (uint64_t)blockIdx.x * (256 * kAccessPerThread) + threadIdx.x;
     const Sections sec = a.sec;
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
@@ -342,10 +352,12 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         lo[k] = hi[k] = 0;
         w[k] = make_uint2(0, 0);
         if (t < a.q) {
-            const uint64_t i64 = __ldcs(a.idx + t);
-            if (i64 < a.n) {
+            const uint64_t v = __ldcs(a.idx + t);
+            const bool ok = MODE == kAccess ? v < a.n : v <= a.qdiv;
+            if (ok) {
                 live[k] = true;
-                i[k] = (uint32_t)i64;
+                i[k] = MODE == kAccess ? (uint32_t)v
+                                       : (uint32_t)min((uint64_t)a.n * v / a.qdiv, (uint64_t)a.n - 1);
             } else {
                 if (a.err) atomicOr(a.err, 1u);
                 if (K64) __stcs((unsigned long long*)a.out + t, 0ull);
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         if (live[k]) {
             lo[k] = ldh(sec.hint + (i[k] >> 10), keep);
             hi[k] = ldh(sec.hint + (i[k] >> 10) + 1, keep);
-            if (a.b) w[k] = field_words(sec, i[k], a.b, once);
+            if (kResidual && a.b) w[k] = field_words(sec, i[k], a.b, once);
         }
     }
     for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
@@ -387,50 +399,16 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         if (!live[k]) continue;
         const uint32_t s = ldh(sec.starts + lo[k], keep);
         const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
-        const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
-        const uint64_t t = t0 + 256 * k;
-        put<K64>((uint8_t*)a.out + t * (K64 ? 8 : 4), pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
+        uint8_t* o = (uint8_t*)a.out + (t0 + 256 * k) * (K64 ? 8 : 4);
+        if (kResidual) {
+            const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
+            put<K64>(o, pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
+        } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
+            const uint64_t f = pr.x + pred_plus(pr.y, i[k] - s, 0);
+            if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
+            else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
+        }
     }
 }
 
-// ----------------------------------------------------------------------------- quantiles
-struct QuantArgs {
-    Sections sec;
-    const uint64_t* k;
-    void* out;
-    uint32_t* err;
-    uint64_t m, q;
-    uint32_t n, b, eps, mask;
-};
-
-// The k-th q-quantile K[min(floor(N k / q), N - 1)] (§III-C; Table I): exact =
-// f(i) + Delta[i] through the hint bracket + binary search; approximate (EXACT = false) =
-// floor(f(i)) from the segment alone, no residual read, error <= eps.
-template <bool K64, bool EXACT>
-__global__ void __launch_bounds__(256) lc_quantile_kernel(const QuantArgs a) {
-    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-    if (t >= a.m) return;
-    const Sections sec = a.sec;
-    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    const uint64_t k = __ldg(a.k + t);
-    uint8_t* o = (uint8_t*)a.out + t * (K64 ? 8 : 4);
-    if (k > a.q) {
-        if (a.err) atomicOr(a.err, 1u);
-        put<K64>(o, 0, 0);
-        return;
-    }
-    const uint32_t i = (uint32_t)min((uint64_t)a.n * k / a.q, (uint64_t)a.n - 1);  // N k < 2^64
-    const uint32_t j = seg_search(sec, i, keep);
-    const uint32_t s = ldh(sec.starts + j, keep);
-    const ulonglong2 pr = ldh(sec.params + j, once);
-    if (EXACT) {
-        const uint32_t v = (a.b ? field_of(field_words(sec, i, a.b, once), i, a.b, a.mask) : 0) - a.eps;
-        put<K64>(o, pr.x, pred_plus(pr.y, i - s, v));
-    } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
-        const uint32_t t = pred_plus(pr.y, i - s, 0);
-        const uint64_t f = pr.x + t;
-        if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
-        else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
-    }
-}
 

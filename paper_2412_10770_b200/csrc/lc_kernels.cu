@@ -147,6 +147,41 @@ int32_t up_bytes(const void* h, void* d, uint64_t a, uint64_t b, cudaStream_t st
                : LC_ERR_CUDA;
 }
 
+int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64_t qdiv, int mode,
+                      void* d_out, uint32_t* d_err, cudaStream_t st) {
+    AccessArgs a;
+    a.sec = sections_of(v);
+    a.idx = d_in;
+    a.out = d_out;
+    a.err = d_err;
+    a.q = q;
+    a.qdiv = qdiv;
+    a.n = (uint32_t)v->h.n;
+    a.b = v->h.res_bits;
+    a.eps = v->h.eps;
+    a.mask = mask_of(a.b);
+    const uint64_t per = 256 * access_per_thread(mode);
+    const uint64_t grid = (q + per - 1) / per;
+    if (grid > 0x7fffffffULL) return LC_ERR_ARG;
+    const unsigned g = (unsigned)grid;
+    const bool k64 = v->h.key_bits == 64;
+    switch (mode) {
+        case kAccess:
+            if (k64) lc_access_kernel<true, kAccess><<<g, 256, 0, st>>>(a);
+            else lc_access_kernel<false, kAccess><<<g, 256, 0, st>>>(a);
+            break;
+        case kQuantileExact:
+            if (k64) lc_access_kernel<true, kQuantileExact><<<g, 256, 0, st>>>(a);
+            else lc_access_kernel<false, kQuantileExact><<<g, 256, 0, st>>>(a);
+            break;
+        default:
+            if (k64) lc_access_kernel<true, kQuantileApprox><<<g, 256, 0, st>>>(a);
+            else lc_access_kernel<false, kQuantileApprox><<<g, 256, 0, st>>>(a);
+    }
+    lc_detail::count_launch(1);
+    return cuda_status();
+}
+
 }  // namespace
 
 extern "C" {
@@ -170,24 +205,7 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
     if (!v || !v->d_blob) return LC_ERR_ARG;
     if (q == 0) return LC_OK;
     if (!d_idx || !d_out) return LC_ERR_ARG;
-    AccessArgs a;
-    a.sec = sections_of(v);
-    a.idx = d_idx;
-    a.out = d_out;
-    a.err = d_err;
-    a.q = q;
-    a.n = (uint32_t)v->h.n;
-    a.b = v->h.res_bits;
-    a.eps = v->h.eps;
-    a.mask = mask_of(a.b);
-    const uint64_t grid = (q + 256 * kAccessPerThread - 1) / (256 * kAccessPerThread);
-    if (grid > 0x7fffffffULL) return LC_ERR_ARG;
-    if (v->h.key_bits == 64)
-        lc_access_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
-    else
-        lc_access_kernel<false><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
-    lc_detail::count_launch(1);
-    return cuda_status();
+    return launch_access(v, d_idx, q, 1, kAccess, d_out, d_err, (cudaStream_t)stream);
 }
 
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
@@ -231,33 +249,11 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
 int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t q,
                     int32_t exact, void* d_out, uint32_t* d_err, lc_stream stream) {
     if (!v || !v->d_blob) return LC_ERR_ARG;
-    if (q == 0 || q > 0xffffffffULL) return LC_ERR_ARG;
+    if (q == 0 || q > 0xffffffffULL) return LC_ERR_ARG;  // N k < 2^64 for k <= q
     if (m == 0) return LC_OK;
     if (!d_k || !d_out) return LC_ERR_ARG;
-    QuantArgs a;
-    a.sec = sections_of(v);
-    a.k = d_k;
-    a.out = d_out;
-    a.err = d_err;
-    a.m = m;
-    a.q = q;
-    a.n = (uint32_t)v->h.n;
-    a.b = v->h.res_bits;
-    a.eps = v->h.eps;
-    a.mask = mask_of(a.b);
-    const uint64_t grid = (m + 255) / 256;
-    if (grid > 0x7fffffffULL) return LC_ERR_ARG;
-    cudaStream_t st = (cudaStream_t)stream;
-    const bool k64 = v->h.key_bits == 64;
-    if (exact) {
-        if (k64) lc_quantile_kernel<true, true><<<(unsigned)grid, 256, 0, st>>>(a);
-        else lc_quantile_kernel<false, true><<<(unsigned)grid, 256, 0, st>>>(a);
-    } else {
-        if (k64) lc_quantile_kernel<true, false><<<(unsigned)grid, 256, 0, st>>>(a);
-        else lc_quantile_kernel<false, false><<<(unsigned)grid, 256, 0, st>>>(a);
-    }
-    lc_detail::count_launch(1);
-    return cuda_status();
+    return launch_access(v, d_k, m, q, exact ? kQuantileExact : kQuantileApprox, d_out, d_err,
+                         (cudaStream_t)stream);
 }
 
 int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,

@@ -39,6 +39,12 @@ def main():
             best = min(best, ev[0].elapsed_time(ev[1]))
         return best
 
+    ranks = torch.from_numpy(rng.integers(0, (1 << 32) - 1, 10_000_000, endpoint=True)
+                             .astype(np.uint64).view(np.int64)).cuda()
+    qo = torch.empty(ranks.numel(), dtype=torch.int64, device="cuda")
+    for exact in (True, False):
+        ms = t(lambda: lc.quantile(v5, ranks, (1 << 32) - 1, exact, qo))
+        print(f"quantile exact={exact} {ms:.3f} ms {ranks.numel() / ms * 1e3:.3e} per s")
     gi, gk = lc.next_geq(v5, d_probe)
     want = np.searchsorted(k5, probes, side="left")
     assert np.array_equal(gi.cpu().numpy(), want.astype(np.int64)), "next_geq mismatch"
