@@ -115,6 +115,88 @@ int64_t oracle_segment(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t F, 
     return oracle_segment_ex(K, n, eps, F, gmax, 0, 0, starts, base, slope);
 }
 
+/* ---------------------------------------------------------------------------------------
+ * FORMAT F7: greedy maximal extension over integer lines with a free intercept (O'Rourke's
+ * rule, on the format's lattice).  Written as the definition: every admissible
+ * intercept beta = K[s] + delta, delta in [max(-eps, eps - K[s]), eps], keeps its own exact
+ * slope interval (the F4 cone computed from beta instead of K[s]); a segment grows while any
+ * intercept still has a non-empty interval.  O(segment length * (2 eps + 1)) -- slow on
+ * purpose.  The chosen intercept is the feasible delta with the least |delta| (the negative
+ * one on a tie), its slope the middle of its interval (F5); base = beta - eps (F7).
+ * F / gmax as in oracle_segment_ex (reduced precision for the brute-force pins).
+ */
+int64_t oracle_segment_free(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t F,
+                            uint64_t gmax, uint64_t* starts, uint64_t* base, uint64_t* slope) {
+    if (n == 0) return OR_ERR_EMPTY;
+    if (F > 32 || eps > 0x3fffffffULL) return OR_ERR_ARG;
+    for (uint64_t i = 1; i < n; i++)
+        if (K[i] <= K[i - 1]) return OR_ERR_UNSORTED;
+    typedef __int128 i128;
+    const uint64_t m = 2 * eps + 1; /* delta = t - eps, t in [0, m) */
+    i128* lo = malloc(m * sizeof(i128));
+    i128* hi = malloc(m * sizeof(i128));
+    i128* nlo = malloc(m * sizeof(i128));
+    i128* nhi = malloc(m * sizeof(i128));
+    uint8_t* alive = malloc(m);
+    if (!lo || !hi || !nlo || !nhi || !alive) {
+        free(lo); free(hi); free(nlo); free(nhi); free(alive);
+        return OR_ERR_ALLOC;
+    }
+    uint64_t L = 0, s = 0;
+    while (s < n) {
+        /* admissible intercepts: K[s] + delta - eps >= 0 */
+        const i128 dmin = K[s] >= 2 * eps ? -(i128)eps : (i128)eps - (i128)K[s];
+        for (uint64_t t = 0; t < m; t++) {
+            alive[t] = ((i128)t - (i128)eps) >= dmin;
+            lo[t] = 0;
+            hi[t] = gmax;
+        }
+        uint64_t e = s + 1;
+        while (e < n) {
+            const i128 d = (i128)(e - s);
+            int any = 0;
+            for (uint64_t t = 0; t < m; t++) {
+                if (!alive[t]) continue;
+                const i128 delta = (i128)t - (i128)eps;
+                const i128 Dp = (i128)(K[e] - K[s]) - delta; /* K[e] - beta */
+                /* S*d >= (Dp - eps) 2^F  and  S*d <= (Dp + eps + 1) 2^F - 1  and  S*d <= gmax */
+                i128 l = 0;
+                if (Dp > (i128)eps) {
+                    const i128 num = (Dp - (i128)eps) << F;
+                    l = num / d + (num % d != 0);
+                }
+                i128 h = ((((Dp + (i128)eps + 1) << F) - 1) / d); /* Dp + eps + 1 >= 2 */
+                if ((i128)gmax / d < h) h = (i128)gmax / d;
+                nlo[t] = lo[t] > l ? lo[t] : l;
+                nhi[t] = hi[t] < h ? hi[t] : h;
+                if (nlo[t] <= nhi[t]) any = 1;
+            }
+            if (!any) break; /* F6/F7: the first infeasible index ends the segment */
+            for (uint64_t t = 0; t < m; t++) {
+                if (!alive[t]) continue;
+                if (nlo[t] > nhi[t]) { alive[t] = 0; continue; }
+                lo[t] = nlo[t];
+                hi[t] = nhi[t];
+            }
+            e++;
+        }
+        /* least |delta|, negative first */
+        uint64_t pick = m;
+        for (uint64_t k = 0; k <= eps && pick == m; k++) {
+            if (alive[eps - k]) pick = eps - k;
+            else if (alive[eps + k]) pick = eps + k;
+        }
+        const i128 delta = (i128)pick - (i128)eps;
+        starts[L] = s;
+        base[L] = (uint64_t)((i128)K[s] + delta - (i128)eps);
+        slope[L] = e - s == 1 ? 0 : (uint64_t)(lo[pick] + (hi[pick] - lo[pick]) / 2);
+        L++;
+        s = e;
+    }
+    free(lo); free(hi); free(nlo); free(nhi); free(alive);
+    return (int64_t)L;
+}
+
 /* --------------------------------------------------------------------------- blob layout */
 
 static uint64_t rd64(const uint8_t* p) {
@@ -134,7 +216,7 @@ static void wr32(uint8_t* p, uint32_t v) {
 static uint64_t up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 typedef struct {
-    uint32_t key_bits, b, eps, hint_log2;
+    uint32_t key_bits, b, eps, hint_log2, flags;
     uint64_t n, L, n_hint, W, o_starts, o_params, o_hint, o_words, total;
 } or_hdr;
 
@@ -163,7 +245,11 @@ static uint64_t field_at(const uint8_t* words, uint64_t i, uint32_t b) {
     return u;
 }
 
-/* prediction floor(f(i)) = base + floor(slope * d / 2^32)  (Eq. 1 in fixed point, F3) */
+/* decode bias c of FORMAT F3: eps for anchored blobs, 0 for free-intercept blobs (F7) */
+static uint64_t bias_of(const or_hdr* h) { return (h->flags & 1u) ? 0 : h->eps; }
+
+/* base + floor(slope * d / 2^32) (Eq. 1 in fixed point, F3); floor(f(i)) for anchored blobs,
+ * floor(f(i)) - eps for free-intercept blobs (F7 stores base = beta - eps) */
 static uint64_t predict(uint64_t base, uint64_t slope, uint64_t d) {
     return base + (uint64_t)(((u128)slope * d) >> 32);
 }
@@ -173,14 +259,14 @@ static uint64_t predict(uint64_t base, uint64_t slope, uint64_t d) {
  * force_break / slope_mode as in oracle_segment_ex (NULL / 0 give the normative encoder).
  * *blob is malloc'ed; free with oracle_free.
  */
-int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
-                         const uint8_t* force_break, int slope_mode, uint8_t** blob,
-                         uint64_t* blob_bytes) {
+static int32_t or_encode(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
+                         uint32_t flags, const uint8_t* force_break, int slope_mode,
+                         uint8_t** blob, uint64_t* blob_bytes) {
     if (!blob || !blob_bytes) return OR_ERR_ARG;
     if (n == 0) return OR_ERR_EMPTY;
     if (!K) return OR_ERR_ARG;
     if (key_bits != 32 && key_bits != 64) return OR_ERR_ARG;
-    if (eps > 0x7fffffffULL) return OR_ERR_ARG;
+    if (eps > ((flags & 1u) ? 0x3fffffffULL : 0x7fffffffULL)) return OR_ERR_ARG;
     if (n >= (1ULL << 32)) return OR_ERR_TOO_LARGE;
     for (uint64_t i = 1; i < n; i++)
         if (K[i] <= K[i - 1]) return OR_ERR_UNSORTED;
@@ -188,8 +274,10 @@ int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
 
     uint64_t* st = malloc(n * 8), *ba = malloc(n * 8), *sl = malloc(n * 8);
     if (!st || !ba || !sl) { free(st); free(ba); free(sl); return OR_ERR_ALLOC; }
-    int64_t L = oracle_segment_ex(K, n, eps, 32, 0x7fffffffffffffffULL, force_break, slope_mode,
-                                  st, ba, sl);
+    int64_t L = (flags & 1u)
+                    ? oracle_segment_free(K, n, eps, 32, 0x7fffffffffffffffULL, st, ba, sl)
+                    : oracle_segment_ex(K, n, eps, 32, 0x7fffffffffffffffULL, force_break,
+                                        slope_mode, st, ba, sl);
     if (L < 0) { free(st); free(ba); free(sl); return (int32_t)L; }
 
     or_hdr h;
@@ -198,6 +286,7 @@ int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
     h.b = oracle_width(eps);
     h.eps = (uint32_t)eps;
     h.hint_log2 = OR_HINT_LOG2;
+    h.flags = flags;
     h.n = n;
     h.L = (uint64_t)L;
     or_layout(&h);
@@ -220,6 +309,7 @@ int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
     wr64(B + 64, h.o_hint);
     wr64(B + 72, h.o_words);
     wr64(B + 80, h.total);
+    wr32(B + 88, h.flags);
 
     /* F2 starts (with starts[L] = N) and params */
     for (uint64_t j = 0; j < h.L; j++) {
@@ -237,11 +327,12 @@ int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
     }
     wr32(B + h.o_hint + 4 * H, (uint32_t)(h.L - 1));
 
-    /* residuals u_i = K[i] - floor(f(i)) + eps in [0, 2 eps], packed LSB-first (F2, F3) */
+    /* residuals u_i = K[i] - floor(f(i)) + eps in [0, 2 eps], packed LSB-first (F2, F3):
+     * K[i] - (base + floor(slope d / 2^32)) + c with the decode bias c (F3, F7) */
     uint64_t j = 0;
     for (uint64_t i = 0; i < n; i++) {
         while (j + 1 < h.L && st[j + 1] <= i) j++;
-        uint64_t u = K[i] - predict(ba[j], sl[j], i - st[j]) + eps;
+        uint64_t u = K[i] - predict(ba[j], sl[j], i - st[j]) + bias_of(&h);
         for (uint32_t t = 0; t < h.b; t++) {
             if ((u >> t) & 1) {
                 uint64_t p = i * h.b + t;
@@ -255,9 +346,21 @@ int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
     return OR_OK;
 }
 
+int32_t oracle_encode_ex(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
+                         const uint8_t* force_break, int slope_mode, uint8_t** blob,
+                         uint64_t* blob_bytes) {
+    return or_encode(K, n, key_bits, eps, 0, force_break, slope_mode, blob, blob_bytes);
+}
+
 int32_t oracle_encode(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
                       uint8_t** blob, uint64_t* blob_bytes) {
-    return oracle_encode_ex(K, n, key_bits, eps, 0, 0, blob, blob_bytes);
+    return or_encode(K, n, key_bits, eps, 0, 0, 0, blob, blob_bytes);
+}
+
+/* FORMAT F7 blob (flags = 1): free-intercept segments from oracle_segment_free */
+int32_t oracle_encode_free(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
+                           uint8_t** blob, uint64_t* blob_bytes) {
+    return or_encode(K, n, key_bits, eps, 1, 0, 0, blob, blob_bytes);
 }
 
 void oracle_free(void* p) { free(p); }
@@ -281,7 +384,10 @@ static int or_read_hdr(const uint8_t* B, uint64_t bytes, or_hdr* h) {
     if (h->eps > 0x7fffffffu || h->b != oracle_width(h->eps)) return OR_ERR_FORMAT;
     if (h->hint_log2 != OR_HINT_LOG2) return OR_ERR_FORMAT;
     if (h->n == 0 || h->n >= (1ULL << 32) || h->L == 0 || h->L > h->n) return OR_ERR_FORMAT;
-    for (int k = 88; k < 128; k++)
+    h->flags = rd32(B + 88);
+    if (h->flags > 1u) return OR_ERR_FORMAT;
+    if ((h->flags & 1u) && h->eps > 0x3fffffffu) return OR_ERR_FORMAT; /* F7 */
+    for (int k = 92; k < 128; k++)
         if (B[k] != 0) return OR_ERR_FORMAT;
     or_layout(h);
     if (n_hint != h->n_hint || W != h->W || o1 != h->o_starts || o2 != h->o_params ||
@@ -302,14 +408,14 @@ static uint64_t seg_of(const uint8_t* B, const or_hdr* h, uint64_t i) {
     return lo;
 }
 
-/* FORMAT F3 for one index: key = (base_j + floor(slope_j d / 2^32) + u - eps) mod 2^64,
- * truncated to key_bits. */
+/* FORMAT F3 for one index: key = (base_j + floor(slope_j d / 2^32) + u - c) mod 2^64,
+ * truncated to key_bits (c = eps, or 0 for F7 blobs). */
 static uint64_t key_at(const uint8_t* B, const or_hdr* h, uint64_t i, uint64_t j) {
     uint64_t s = rd32(B + h->o_starts + 4 * j);
     uint64_t base = rd64(B + h->o_params + 16 * j);
     uint64_t slope = rd64(B + h->o_params + 16 * j + 8);
     uint64_t u = field_at(B + h->o_words, i, h->b);
-    uint64_t k = predict(base, slope, i - s) + u - h->eps;
+    uint64_t k = predict(base, slope, i - s) + u - bias_of(h);
     if (h->key_bits == 32) k &= 0xffffffffULL;
     return k;
 }
@@ -411,7 +517,9 @@ int32_t oracle_predict(const uint8_t* B, uint64_t bytes, const uint64_t* idx, ui
         uint64_t j = seg_of(B, &h, i);
         uint64_t s = rd32(B + h.o_starts + 4 * j);
         uint64_t slope = rd64(B + h.o_params + 16 * j + 8);
-        u128 f = (u128)rd64(B + h.o_params + 16 * j) + (((u128)slope * (i - s)) >> 32);
+        /* floor(f(i)) = base + floor(slope d / 2^32) + (eps - c): F7 bases sit eps below beta */
+        u128 f = (u128)rd64(B + h.o_params + 16 * j) + (((u128)slope * (i - s)) >> 32) +
+                 (h.eps - bias_of(&h));
         u128 top = h.key_bits == 32 ? (u128)0xffffffffULL : (u128)0xffffffffffffffffULL;
         put_key(out, h.key_bits, t, (uint64_t)(f > top ? top : f)); /* saturate (DESIGN L24) */
     }
@@ -481,9 +589,11 @@ int32_t oracle_validate(const uint8_t* B, uint64_t bytes) {
     /* residual fields in [0, 2 eps]; stream bits past n*b are zero */
     for (uint64_t i = 0; i < h.n; i++)
         if (field_at(B + h.o_words, i, h.b) > 2ULL * h.eps) return OR_ERR_FORMAT;
-    /* anchor: the field at every segment start is eps (base_j = K[s_j]) */
-    for (uint64_t j = 0; j < h.L; j++)
-        if (field_at(B + h.o_words, rd32(B + h.o_starts + 4 * j), h.b) != h.eps) return OR_ERR_FORMAT;
+    /* anchor (F2, anchored blobs only): the field at every segment start is eps */
+    if (!(h.flags & 1u))
+        for (uint64_t j = 0; j < h.L; j++)
+            if (field_at(B + h.o_words, rd32(B + h.o_starts + 4 * j), h.b) != h.eps)
+                return OR_ERR_FORMAT;
     for (uint64_t p = h.n * h.b; p < 32 * h.W; p++)
         if (bit_at(B + h.o_words, p)) return OR_ERR_FORMAT;
     /* decoded keys strictly increasing and within key_bits (corruption detector) */
@@ -495,8 +605,8 @@ int32_t oracle_validate(const uint8_t* B, uint64_t bytes) {
         uint64_t slope = rd64(B + h.o_params + 16 * j + 8);
         u128 full = (u128)base + (((u128)slope * (i - s)) >> 32) +
                     field_at(B + h.o_words, i, h.b);
-        if (full < h.eps) return OR_ERR_FORMAT;
-        full -= h.eps;
+        if (full < bias_of(&h)) return OR_ERR_FORMAT;
+        full -= bias_of(&h);
         if (full > (h.key_bits == 32 ? (u128)0xffffffffULL : (u128)0xffffffffffffffffULL))
             return OR_ERR_FORMAT;
         if (i > 0 && (uint64_t)full <= prev) return OR_ERR_FORMAT;
@@ -505,14 +615,14 @@ int32_t oracle_validate(const uint8_t* B, uint64_t bytes) {
     return OR_OK;
 }
 
-/* header fields for the Python side: out[0..13] =
- * key_bits, b, eps, hint_log2, n, L, n_hint, W, o_starts, o_params, o_hint, o_words, total */
+/* header fields for the Python side: out[0..14] = key_bits, b, eps, hint_log2, n, L,
+ * n_hint, W, o_starts, o_params, o_hint, o_words, total, flags */
 int32_t oracle_header(const uint8_t* B, uint64_t bytes, uint64_t* out) {
     or_hdr h;
     int32_t st = or_read_hdr(B, bytes, &h);
     if (st) return st;
-    uint64_t v[13] = {h.key_bits, h.b, h.eps, h.hint_log2, h.n, h.L, h.n_hint, h.W,
-                      h.o_starts, h.o_params, h.o_hint, h.o_words, h.total};
+    uint64_t v[14] = {h.key_bits, h.b, h.eps, h.hint_log2, h.n, h.L, h.n_hint, h.W,
+                      h.o_starts, h.o_params, h.o_hint, h.o_words, h.total, h.flags};
     memcpy(out, v, sizeof v);
     return OR_OK;
 }

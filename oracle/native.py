@@ -42,6 +42,10 @@ def lib():
         L.oracle_encode_ex.argtypes = [p, u64, u32, u64, p, C.c_int, C.POINTER(p),
                                        C.POINTER(u64)]
         L.oracle_encode_ex.restype = i32
+        L.oracle_segment_free.argtypes = [p, u64, u64, u32, u64, p, p, p]
+        L.oracle_segment_free.restype = i64
+        L.oracle_encode_free.argtypes = [p, u64, u32, u64, C.POINTER(p), C.POINTER(u64)]
+        L.oracle_encode_free.restype = i32
         L.oracle_free.argtypes = [p]
         L.oracle_free.restype = None
         L.oracle_decode.argtypes = [p, u64, p]
@@ -93,9 +97,23 @@ def segment(keys, eps: int, F: int = 32, gmax: int = GMAX, force_break=None, slo
     return st[:L].copy(), ba[:L].copy(), sl[:L].copy()
 
 
+def segment_free(keys, eps: int, F: int = 32, gmax: int = GMAX):
+    """Free-intercept greedy segmentation (FORMAT F7). Returns (starts, base, slope) u64
+    arrays, base = beta - eps."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    n = k.size
+    st = np.empty(max(n, 1), np.uint64)
+    ba = np.empty(max(n, 1), np.uint64)
+    sl = np.empty(max(n, 1), np.uint64)
+    L = lib().oracle_segment_free(_ptr(k), n, eps, F, gmax, _ptr(st), _ptr(ba), _ptr(sl))
+    if L < 0:
+        raise OracleError(L, "segment_free")
+    return st[:L].copy(), ba[:L].copy(), sl[:L].copy()
+
+
 def encode(keys, eps: int, key_bits: int | None = None, force_break=None,
-           slope_mode: int = 0) -> bytes:
-    """LCG1 blob of `keys` (FORMAT F1-F6)."""
+           slope_mode: int = 0, free: bool = False) -> bytes:
+    """LCG1 blob of `keys`: anchored (FORMAT F1-F6) or, with free=True, free-intercept (F7)."""
     arr = np.asarray(keys)
     if key_bits is None:
         key_bits = 32 if arr.dtype == np.uint32 else 64
@@ -103,9 +121,15 @@ def encode(keys, eps: int, key_bits: int | None = None, force_break=None,
     fb = None if force_break is None else np.ascontiguousarray(force_break, dtype=np.uint8)
     out = C.c_void_p()
     nb = C.c_uint64()
-    st = lib().oracle_encode_ex(_ptr(k) if k.size else None, k.size, key_bits, eps,
-                                None if fb is None else _ptr(fb), slope_mode,
-                                C.byref(out), C.byref(nb))
+    if free:
+        if fb is not None or slope_mode:
+            raise ValueError("force_break / slope_mode apply to the anchored encoder only")
+        st = lib().oracle_encode_free(_ptr(k) if k.size else None, k.size, key_bits, eps,
+                                      C.byref(out), C.byref(nb))
+    else:
+        st = lib().oracle_encode_ex(_ptr(k) if k.size else None, k.size, key_bits, eps,
+                                    None if fb is None else _ptr(fb), slope_mode,
+                                    C.byref(out), C.byref(nb))
     if st != 0:
         raise OracleError(st, "encode")
     try:
@@ -129,10 +153,11 @@ class Header:
     o_hint: int
     o_words: int
     total: int
+    flags: int
 
 
 def header(blob: bytes) -> Header:
-    v = np.zeros(13, np.uint64)
+    v = np.zeros(14, np.uint64)
     st = lib().oracle_header(blob, len(blob), _ptr(v))
     if st != 0:
         raise OracleError(st, "header")

@@ -10,7 +10,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-HEADER_FMT = "<4sHBBII9Q40s"  # FORMAT F1, 128 bytes
+HEADER_FMT = "<4sHBBII9QI36s"  # FORMAT F1, 128 bytes (flags at offset 88)
 assert struct.calcsize(HEADER_FMT) == 128
 
 
@@ -36,17 +36,28 @@ class Blob:
     slope: np.ndarray
     hint: np.ndarray
     words: np.ndarray
+    flags: int = 0
+
+    @property
+    def bias(self) -> int:
+        """Decode bias c of FORMAT F3: eps (anchored) or 0 (free intercept, F7)."""
+        return 0 if self.flags & 1 else self.eps
+
+    @property
+    def beta(self) -> list[int]:
+        """Segment intercepts beta_j = floor(f(s_j)) as Python ints (F7 stores beta - eps)."""
+        return [int(x) + self.eps - self.bias for x in self.base]
 
 
 def parse(blob: bytes) -> Blob:
     (magic, version, key_bits, b, eps, hint_log2, n, L, n_hint, W, o_s, o_p, o_h, o_w, total,
-     _res) = struct.unpack_from(HEADER_FMT, blob, 0)
+     flags, _res) = struct.unpack_from(HEADER_FMT, blob, 0)
     starts = np.frombuffer(blob, np.uint32, L + 1, o_s)
     params = np.frombuffer(blob, np.uint64, 2 * L, o_p).reshape(L, 2)
     hint = np.frombuffer(blob, np.uint32, n_hint, o_h)
     words = np.frombuffer(blob, np.uint32, W, o_w)
     return Blob(magic, version, key_bits, b, eps, hint_log2, n, L, n_hint, W, o_s, o_p, o_h,
-                o_w, total, starts, params[:, 0], params[:, 1], hint, words)
+                o_w, total, starts, params[:, 0], params[:, 1], hint, words, flags)
 
 
 def fields(bl: Blob) -> list[int]:
