@@ -50,8 +50,13 @@ typedef struct lc_header {
     uint64_t n_hint;      /* H + 1, H = ceil(N / 1024) */
     uint64_t n_words;     /* W residual words */
     uint64_t off_starts, off_params, off_hint, off_words, total_bytes;
-    uint8_t reserved[40];
+    uint32_t flags;       /* 0, or LC_FLAG_FREE_INTERCEPT (FORMAT F7) */
+    uint8_t reserved[36];
 } lc_header;
+
+/* Header flag (FORMAT F7): segments use a free integer intercept (O'Rourke's rule)
+ * instead of the F2 anchor; params hold base = beta - eps and the decode bias is 0. */
+#define LC_FLAG_FREE_INTERCEPT 1u
 
 /* A blob resident in device memory: a host copy of its header plus the device pointer.
  * d_blob must be 256-byte aligned (torch / cudaMalloc allocations are). */
@@ -75,7 +80,15 @@ typedef struct CUstream_st* lc_stream;
 int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps, void** blob,
                   uint64_t* blob_bytes);
 
-/* Release a blob returned by lc_encode (NULL is a no-op). */
+/* lc_encode with format flags: flags = LC_FLAG_FREE_INTERCEPT selects the FORMAT F7 encoder
+ * (greedy maximal extension over all integer lines, the O'Rourke rule of PAPER.md:188 on the
+ * format's lattice: fewer segments, same decode kernels), which needs eps <= 2^30 - 1.
+ * flags = 0 is lc_encode.  Output ownership and errors as lc_encode; unknown flag bits or
+ * eps out of range give LC_ERR_ARG. */
+int32_t lc_encode_ex(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
+                     uint32_t flags, void** blob, uint64_t* blob_bytes);
+
+/* Release a blob returned by lc_encode / lc_encode_ex (NULL is a no-op). */
 void lc_free(void* blob);
 
 /* Full validation of a HOST copy of a blob (header, offsets, monotone starts, slope guard,

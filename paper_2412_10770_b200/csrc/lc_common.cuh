@@ -29,6 +29,10 @@ Sections sections_of(const lc_view* v) {
     return s;
 }
 
+// FORMAT F3 decode bias c: eps for anchored blobs, 0 for free-intercept blobs (F7)
+bool is_free(const lc_view* v) { return v->h.flags & LC_FLAG_FREE_INTERCEPT; }
+uint32_t bias_of(const lc_view* v) { return is_free(v) ? 0u : v->h.eps; }
+
 // Bounds-checked build (-DLC_DEBUG_BOUNDS, tests/test_gpu_bounds.py): every shared-memory page
 // / ring-slot index and every section index is checked; a violation is counted in
 // g_lc_violations (read by lc_debug_violations) and the access is clamped instead of faulting.
@@ -122,7 +126,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
-// t = floor(slope * d / 2^32) + v  (v = u - eps), with floor(slope * d / 2^32) =
+// t = floor(slope * d / 2^32) + v  (v = u - c, c the decode bias), with floor(slope * d / 2^32) =
 // umulhi(slope_lo, d) + slope_hi * d exact in 32 bits because slope * d < 2^63 (FORMAT F2
 // guard): mul.hi + mad.lo + add, kept as 3 ops
 __device__ __forceinline__ uint32_t pred_plus(uint64_t slope, uint32_t d, uint32_t v) {

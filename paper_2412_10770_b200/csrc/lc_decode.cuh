@@ -10,7 +10,7 @@ struct DecodeArgs {
     uint32_t i0, i1;   // i0 % 1024 == 0
     uint32_t chunk0;   // i0 / 1024
     uint32_t nchunks;  // ceil((i1 - i0) / 1024)
-    uint32_t eps;
+    uint32_t bias;
     uint32_t warp_bytes;  // shared memory per warp
     uint32_t nwords;      // W (words section length)
 };
@@ -63,12 +63,13 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
 // the chunk (selects the residual words).  Segment j of each lane: boundaries inside the
 // window form a bitmask (REDUX.OR over the next 32 segment starts); popc/clz give the
 // segment and the offset d = i - s_j with no search.  key = base + t with
-// t = floor(slope d / 2^32) + u - eps = K[i] - K[s_j] in [0, 2^32) (FORMAT F2 anchor + guard).
+// t = floor(slope d / 2^32) + u - bias = K[i] - base_j in [0, 2^32) (FORMAT F2 anchor, or the
+// F7 band floor with bias 0, plus the guard).
 template <bool K64, uint32_t B, bool CHECK, bool FULL>
 __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
                                               uint32_t& sb, uint32_t jlast, uint32_t wb,
                                               uint32_t w, uint32_t lane, uint32_t lmask,
-                                              uint32_t lw, uint32_t ls, uint32_t eps,
+                                              uint32_t lw, uint32_t ls, uint32_t bias,
                                               void* outw, uint32_t valid) {
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
@@ -81,7 +82,7 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
     const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
     const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
     LC_CHECK(B && (FULL || lane < valid), w * B + lw + 1, pg.nw);
-    const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - eps);
+    const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - bias);
     if (FULL || lane < valid) put<K64>(outw, pr.x, t);
     // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
     // the advance there so jb stays a valid staged index
@@ -96,7 +97,7 @@ template <bool K64, uint32_t B, bool CHECK>
 __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w2, uint32_t lane, uint32_t lmask,
-                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw) {
     constexpr uint32_t kw = K64 ? 8 : 4;
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
@@ -105,9 +106,9 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t inside = __ballot_sync(kFull, x < 64);
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
         decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
-                                           ls, eps, outw, 32);
+                                           ls, bias, outw, 32);
         decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
-                                           lmask, lw, ls, eps, (uint8_t*)outw + 32 * kw, 32);
+                                           lmask, lw, ls, bias, (uint8_t*)outw + 32 * kw, 32);
         return;
     }
     const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));       // starts in (wb, wb+32)
@@ -123,8 +124,8 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
     const ulonglong2 pB = pg.sP[LC_BOUND(true, jB + __popc(mB) - pg.pj, pg.cp)];
     LC_CHECK(B, (2 * w2 + 1) * B + lw + 1, pg.nw);
-    const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - eps);
-    const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - eps);
+    const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - bias);
+    const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - bias);
     put<K64>(outw, pA.x, tA);
     put<K64>((uint8_t*)outw + 32 * kw, pB.x, tB);
     jb = min(jb + adv, jlast + 1);  // see decode_window
@@ -138,17 +139,17 @@ template <bool K64, uint32_t B, bool CHECK>
 __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w4, uint32_t lane, uint32_t lmask,
-                                            uint32_t lw, uint32_t ls, uint32_t eps, void* outw) {
+                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw) {
     constexpr uint32_t kw = K64 ? 8 : 4;
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
     if (__ballot_sync(kFull, x < 128) == kFull) {  // >= 32 boundaries in 128 keys
-        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls, eps,
+        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls, bias,
                                    outw);
         decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask, lw,
-                                   ls, eps, (uint8_t*)outw + 64 * kw);
+                                   ls, bias, (uint8_t*)outw + 64 * kw);
         return;
     }
     const uint32_t adv = __popc(__ballot_sync(kFull, x <= 128));
@@ -161,7 +162,7 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
         LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
         put<K64>((uint8_t*)outw + 32 * kw * q, pr.x,
-                 pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - eps));
+                 pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - bias));
         off = P ? __clz(P) + 1 : off + 32;
         jq += __popc(P);
     }
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
 #pragma unroll
                 for (uint32_t k = 0; k < 2; ++k)
                     decode_quad<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k), g + k,
-                                               lane, lmask, lw, ls, a.eps, outl + 128 * kw * k);
+                                               lane, lmask, lw, ls, a.bias, outl + 128 * kw * k);
                 if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
                     const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
                     const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
@@ -239,12 +240,12 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
                     decode_pair<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
-                                              lane, lmask, lw, ls, a.eps, outl + 64 * kw * k);
+                                              lane, lmask, lw, ls, a.bias, outl + 64 * kw * k);
             }
         } else {  // ragged tail chunk
             for (uint32_t w = 0; 32 * w < nk; ++w)
                 decode_window<K64, B, true, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane,
-                                                   lmask, lw, ls, a.eps, outl + 32 * kw * w,
+                                                   lmask, lw, ls, a.bias, outl + 32 * kw * w,
                                                    nk - 32 * w);
         }
     }

@@ -10,7 +10,7 @@ struct RangeArgs {
     void* out;
     uint32_t* err;
     uint64_t q;
-    uint32_t len, n, L, b, eps, mask;
+    uint32_t len, n, L, b, bias, mask;
     uint32_t nwords;  // W
 };
 
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
     const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
-    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L, eps = a.eps;
+    const uint32_t len = a.len, b = a.b, mask = a.mask, L = a.L, bias = a.bias;
     const uint32_t lmask = lanemask_le();
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
 
@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
                 ldh(sec.params + LC_BOUND(true, jb + __popc(PA) + __popc(mB), L), once);
             const uint32_t uA = b ? field_of(wA, rk + lane, b, mask) : 0;
             const uint32_t uB = b ? field_of(wB, rk + 32 + lane, b, mask) : 0;
-            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - eps));
-            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+            put<K64>(outk + lane * kw, pA.x, pred_plus(pA.y, dA, uA - bias));
+            put<K64>(outk + (32 + lane) * kw, pB.x, pred_plus(pB.y, dB, uB - bias));
             if (len == 64) continue;
             jb += adv;
             sb = ldh(sec.starts + min(jb, L), keep);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
                 const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
                 const uint32_t u =
                     b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
-                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - eps));
+                put<K64>(outk + (w0 + lane) * kw, pr.x, pred_plus(pr.y, d, u - bias));
             }
             jb += adv;
             sb = ldh(sec.starts + min(jb, L), keep);
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
-    const uint32_t b = a.b, mask = a.mask, L = a.L, eps = a.eps;
+    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
     const uint32_t RB = r64_bytes(b), nw16 = r64_words(b) / 4;
     uint8_t* ring = smem + warp * kR64Slots * RB;
     const uint32_t lmask = lanemask_le();
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
                 uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
                 uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
             }
-            put<K64>(outk, pA.x, pred_plus(pA.y, dA, uA - eps));
-            put<K64>(outk + 32 * kw, pB.x, pred_plus(pB.y, dB, uB - eps));
+            put<K64>(outk, pA.x, pred_plus(pA.y, dA, uA - bias));
+            put<K64>(outk + 32 * kw, pB.x, pred_plus(pB.y, dB, uB - bias));
         } else {  // dense range: two 32-key windows through L2
             uint32_t jb = jk, sbw = sb;
             for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
                 const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
                 const uint32_t u =
                     b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
-                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - eps));
+                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
                 jb += adv;
                 sbw = ldh(sec.starts + min(jb, L), keep);
             }
@@ -318,7 +318,8 @@ struct AccessArgs {
     uint32_t* err;
     uint64_t q;           // number of queries
     uint64_t qdiv;        // quantile denominator q (kQuantile*)
-    uint32_t n, b, eps, mask;
+    uint32_t n, b, bias, mask;
+    uint32_t center;  // eps - bias: 0 for anchored blobs, eps for F7 (approximate mode)
 };
 
 enum AccessMode { kAccess = 0, kQuantileExact = 1, kQuantileApprox = 2 };
@@ -402,9 +403,10 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         uint8_t* o = (uint8_t*)a.out + (t0 + 256 * k) * (K64 ? 8 : 4);
         if (kResidual) {
             const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
-            put<K64>(o, pr.x, pred_plus(pr.y, i[k] - s, u - a.eps));
+            put<K64>(o, pr.x, pred_plus(pr.y, i[k] - s, u - a.bias));
         } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
-            const uint64_t f = pr.x + pred_plus(pr.y, i[k] - s, 0);
+            // floor(f(i)) = base + floor(slope d / 2^32) + (eps - bias): F7 bases sit eps below
+            const uint64_t f = pr.x + pred_plus(pr.y, i[k] - s, a.center);
             if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
             else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
         }

@@ -1,11 +1,13 @@
-// lc_host.cpp -- host side of the C ABI (include/lc.h): encoder, validator, view setup.
+// lc_host.cpp -- host side of the C ABI (include/lc.h): encoders, validator, view setup.
 //
-// The encoder is the greedy anchored integer cone of FORMAT F4-F6 (the eps-PLA of Def. 2,
-// PAPER.md:171-181, fitted greedily per the north star instead of O'Rourke's optimal fit,
-// PAPER.md:188), with residual packing per PAPER.md:184-186.  It is written independently of
+// Two encoders: the greedy anchored integer cone of FORMAT F4-F6 (the eps-PLA of Def. 2,
+// PAPER.md:171-181, fitted greedily per the north star) and the free-intercept O'Rourke rule of
+// FORMAT F7 on the format's integer lattice; residual packing per
+// PAPER.md:184-186.  It is written independently of
 // oracle/ (which tests compare byte for byte) and optimised for throughput: the
 // cone is tested with 64x64->128 multiplications and divides only when a bound tightens.
 #include <atomic>
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -14,10 +16,14 @@
 #include "lc.h"
 #include "lc_internal.h"
 
+static_assert(sizeof(lc_header) == 128, "FORMAT F1: 128-byte header");
+static_assert(offsetof(lc_header, flags) == 88, "FORMAT F1: flags at offset 88");
+
 namespace {
 
 using u128 = unsigned __int128;
 constexpr uint64_t kSlopeMax = 0x7fffffffffffffffULL;  // guard G = 2^63 - 1 (FORMAT F2)
+constexpr uint32_t kEpsMaxFree = 0x3fffffffu;           // FORMAT F7: eps <= 2^30 - 1
 
 // floor(x / d) for a quotient known to be < 2^64
 inline uint64_t div_q64(u128 x, uint64_t d) {
@@ -88,9 +94,337 @@ inline uint64_t fit_segment(const K* k, uint64_t n, uint64_t s, uint64_t eps, ui
     return e;
 }
 
+// ------------------------------------------------------------------ FORMAT F7 (free intercept)
+// Segment [s, e) with intercept beta = K[s] + delta and slope S (x 2^-32) must satisfy, per key
+// i (d = i - s, D = K[i] - K[s]):  S d >= (D - eps - delta) 2^32  and  S d <= (D + eps + 1 -
+// delta) 2^32 - 1, plus 0 <= S <= G / d_max.  For fixed delta this is the F4 cone; as functions
+// of delta the bounds are lines  lo_i(delta) = (Lo_i - delta) 2^32 / d_i  (Lo_i = D - eps) and
+// up_i(delta) = ((Up_i - delta) 2^32 - 1) / d_i  (Up_i = D + eps + 1).  Keys arrive with d
+// increasing, so every new line is flatter than all earlier ones: the max of the lower lines and
+// the min of the upper lines are convex-hull-trick envelopes with pushes at one end, and the new
+// key's constraints cut the real-feasible delta set by a ray (new lower line vs old upper
+// envelope: a left ray; old lower envelope vs new upper line, and the guard: right rays).
+// A witness (delta, S) is tested in O(1) per key; only when it fails are the exact integer ends
+// of the feasible delta interval re-derived by binary search and a new witness placed in its
+// middle.  All comparisons are exact in 128-bit integers (|values| < 2^99).
+using i128 = __int128;
+
+// floor(a / d) for d > 0, clamped to kSlopeMax + 1 (every caller clamps to <= kSlopeMax);
+// one divq when the quotient fits 64 bits instead of a 128-bit library division
+inline i128 fdiv(i128 a, int64_t d) {
+    if (a < 0) return -(i128)(((unsigned __int128)(-a) + (uint64_t)d - 1) / (uint64_t)d);
+    const unsigned __int128 ua = (unsigned __int128)a;
+    if ((uint64_t)(ua >> 64) >= (uint64_t)d) return (i128)kSlopeMax + 1;
+    return (i128)div_q64(ua, (uint64_t)d);
+}
+inline i128 cdiv0(i128 a, int64_t d) {  // max(0, ceil(a / d)), d > 0, same clamp
+    return a <= 0 ? 0 : fdiv(a + d - 1, d);
+}
+
+struct Line {
+    int64_t c;   // Lo_i (lower band) or Up_i (upper band)
+    int64_t d;   // i - s >= 1
+};
+
+class FreeFit {
+public:
+    explicit FreeFit(uint64_t eps) : eps_((int64_t)eps) {
+        lo_.reserve(64);
+        up_.reserve(64);
+    }
+
+    // fits the segment starting at s; returns e, writes base (= beta - eps) and slope
+    template <typename K>
+    uint64_t fit(const K* k, uint64_t n, uint64_t s, uint64_t* base, uint64_t* slope) {
+        const uint64_t ks = (uint64_t)k[s];
+        dlo_ = ks >= 2 * (uint64_t)eps_ ? -eps_ : eps_ - (int64_t)ks;  // beta - eps >= 0
+        p_ = dlo_;
+        q_ = eps_;
+        lo_.clear();
+        up_.clear();
+        wd_ = clamp0();
+        cl_ = 0;
+        ch_ = kSlopeMax;
+        gd_ = kSlopeMax;
+        const uint64_t dmax_key = (uint64_t)0x7fffffff + 2 * (uint64_t)eps_;
+        uint64_t e = s + 1;
+        for (; e < n; ++e) {
+            const int64_t d = (int64_t)(e - s);
+            const uint64_t D = (uint64_t)k[e] - ks;
+            if (D > dmax_key) break;  // floor(S d / 2^32) <= 2^31 - 1 under the guard
+            const Line lo{(int64_t)D - eps_, d}, up{(int64_t)D + eps_ + 1, d};
+            const uint64_t gd = kSlopeMax / (uint64_t)d;
+            if (!cone_step(lo, up, gd) && !refit(lo, up, gd)) break;
+            push_lo(lo);
+            push_up(up);
+            gd_ = gd;
+        }
+        int64_t dc;
+        uint64_t sc = 0;
+        if (e - s == 1) {
+            dc = clamp0();
+        } else {
+            choose(&dc, &sc);
+        }
+        *base = (uint64_t)((int64_t)(ks - (uint64_t)eps_) + dc);  // K[s] + delta - eps >= 0
+        *slope = sc;
+        return e;
+    }
+
+private:
+    int64_t eps_, dlo_ = 0, p_ = 0, q_ = 0, wd_ = 0;
+    uint64_t cl_ = 0, ch_ = 0, gd_ = 0;  // slope interval [cl_, ch_] of the witness intercept
+    std::vector<Line> lo_, up_;
+
+    int64_t clamp0() const { return dlo_ > 0 ? dlo_ : 0; }
+
+    // (c - delta) 2^32 for the lower band, (c - delta) 2^32 - 1 for the upper band
+    static i128 lnum(const Line& l, int64_t x) { return ((i128)(l.c - x)) << 32; }
+    static i128 unum(const Line& l, int64_t x) { return (((i128)(l.c - x)) << 32) - 1; }
+
+    // envelope positions: lo_ back = flattest = rightmost region; up_ back = flattest = leftmost
+    static bool lo_ge(const Line& a, const Line& b, int64_t x) {  // lo_a(x) >= lo_b(x)
+        return (i128)(a.c - x) * b.d >= (i128)(b.c - x) * a.d;
+    }
+    static bool up_le(const Line& a, const Line& b, int64_t x) {  // up_a(x) <= up_b(x)
+        return unum(a, x) * b.d <= unum(b, x) * a.d;
+    }
+    // crossing abscissa of lines a (steeper, d_a < d_b) and b: (c_a d_b - c_b d_a)/(d_b - d_a)
+    // (the upper band's crossings share a -2^-32 shift, which cancels in comparisons)
+    static bool cross_le(const Line& a, const Line& b, const Line& c, const Line& e) {
+        // x(a, b) <= x(c, e)
+        const i128 n1 = (i128)a.c * b.d - (i128)b.c * a.d, d1 = b.d - a.d;
+        const i128 n2 = (i128)c.c * e.d - (i128)e.c * c.d, d2 = e.d - c.d;
+        return n1 * d2 <= n2 * d1;
+    }
+    void push_lo(const Line& l) {
+        while (lo_.size() >= 2) {
+            const Line& t = lo_.back();
+            const Line& t1 = lo_[lo_.size() - 2];
+            if (cross_le(t, l, t1, t)) lo_.pop_back();  // x(t, new) <= x(t1, t): t never maximal
+            else break;
+        }
+        lo_.push_back(l);
+    }
+    void push_up(const Line& l) {
+        while (up_.size() >= 2) {
+            const Line& t = up_.back();
+            const Line& t1 = up_[up_.size() - 2];
+            if (cross_le(t1, t, t, l)) up_.pop_back();  // x(t, new) >= x(t1, t): t never minimal
+            else break;
+        }
+        up_.push_back(l);
+    }
+    const Line& lo_at(int64_t x) const {  // active line of max_i lo_i at x (lo_ non-empty)
+        size_t a = 0, b = lo_.size() - 1;
+        while (a < b) {
+            const size_t m = (a + b) >> 1;
+            if (lo_ge(lo_[m], lo_[m + 1], x)) b = m;
+            else a = m + 1;
+        }
+        return lo_[a];
+    }
+    const Line& up_at(int64_t x) const {  // active line of min_i up_i at x (up_ non-empty)
+        size_t a = 0, b = up_.size() - 1;
+        while (a < b) {
+            const size_t m = (a + b) >> 1;
+            if (up_le(up_[m], up_[m + 1], x)) b = m;
+            else a = m + 1;
+        }
+        return up_[a];
+    }
+    // lo_a(x) <= up_b(x) and lo_a(x) <= gd (real comparisons)
+    static bool lo_le_up(const Line& a, const Line& b, int64_t x) {
+        return lnum(a, x) * b.d <= unum(b, x) * a.d;
+    }
+    static bool lo_le_g(const Line& a, uint64_t gd_num, int64_t gd_den, int64_t x) {
+        // lo_a(x) <= G / gd_den  <=>  lnum * gd_den <= G * d_a
+        return lnum(a, x) * gd_den <= (i128)gd_num * a.d;
+    }
+
+    // the F4 cone at the witness intercept wd_, advanced by one key (divides only when a bound
+    // tightens); false when it empties -- then refit() moves the intercept
+    bool cone_step(const Line& lo, const Line& up, uint64_t gd) {
+        const int64_t d = lo.d;
+        const i128 lod = (i128)cl_ * d, hid = (i128)ch_ * d;
+        const i128 X = unum(up, wd_), Y = lnum(lo, wd_);  // S d <= X, S d >= Y
+        if (lod > X || Y > hid || cl_ > gd) return false;
+        uint64_t nlo = cl_, nhi = ch_;
+        if (Y > lod) nlo = (uint64_t)cdiv0(Y, d);
+        if (X < hid) nhi = (uint64_t)fdiv(X, d);
+        if (gd < nhi) nhi = gd;
+        if (nlo > nhi) return false;
+        cl_ = nlo;
+        ch_ = nhi;
+        return true;
+    }
+
+    // membership tests for the state extended by (lo, up) with guard G / d
+    bool old_ok(int64_t x) const {
+        return lo_.empty() || up_.empty() || lo_le_up(lo_at(x), up_at(x), x);
+    }
+    bool ray_a(const Line& lo, int64_t x) const { return up_.empty() || lo_le_up(lo, up_at(x), x); }
+    bool ray_bc(const Line& lo, const Line& up, int64_t x) const {
+        if (!lo_le_g(lo, kSlopeMax, lo.d, x)) return false;
+        if (lo_.empty()) return true;
+        const Line& a = lo_at(x);
+        return lo_le_up(a, up, x) && lo_le_g(a, kSlopeMax, lo.d, x);
+    }
+    // real-feasibility of x for the state extended by (lo, up): one lookup per envelope
+    struct Eval {
+        bool a, bc, old;
+        const Line *la, *ua;  // active envelope lines at x (nullptr if the envelope is empty)
+    };
+    Eval eval(const Line& lo, const Line& up, int64_t x) const {
+        Eval r{true, lo_le_g(lo, kSlopeMax, lo.d, x), true, nullptr, nullptr};
+        if (!lo_.empty()) r.la = &lo_at(x);
+        if (!up_.empty()) {
+            r.ua = &up_at(x);
+            r.a = lo_le_up(lo, *r.ua, x);
+            if (r.la) r.old = lo_le_up(*r.la, *r.ua, x);
+        }
+        if (r.la && r.bc) r.bc = lo_le_up(*r.la, up, x) && lo_le_g(*r.la, kSlopeMax, lo.d, x);
+        return r;
+    }
+    bool real_ok(const Line& lo, const Line& up, int64_t x) const {
+        const Eval r = eval(lo, up, x);
+        return r.a && r.bc && r.old;
+    }
+    // integer slope interval at x for the extended state; false if empty.  la / ua: the active
+    // envelope lines at x when the caller has them (nullptr: look them up)
+    bool int_range(const Line* lo, const Line* up, uint64_t gd, int64_t x, uint64_t* slo,
+                   uint64_t* shi, const Line* la = nullptr, const Line* ua = nullptr) const {
+        i128 l = 0, h = (i128)gd;
+        if (!lo_.empty()) {
+            const Line& a = la ? *la : lo_at(x);
+            const i128 c = cdiv0(lnum(a, x), a.d);  // clamped values only feed the l > h test
+            if (c > l) l = c;
+        }
+        if (lo) {
+            const i128 c = cdiv0(lnum(*lo, x), lo->d);
+            if (c > l) l = c;
+        }
+        if (l > h) return false;
+        if (up) {
+            const i128 f = fdiv(unum(*up, x), up->d);
+            if (f < h) h = f;
+        }
+        if (!up_.empty() && l <= h) {
+            const Line& b = ua ? *ua : up_at(x);
+            const i128 f = fdiv(unum(b, x), b.d);
+            if (f < h) h = f;
+        }
+        if (l > h) return false;
+        *slo = (uint64_t)l;
+        *shi = (uint64_t)h;
+        return true;
+    }
+    template <typename P>
+    static int64_t first_true(int64_t a, int64_t b, P pred) {  // F..F T..T on [a, b]; b+1 if none
+        int64_t lo = a, hi = b + 1;
+        while (lo < hi) {
+            const int64_t m = lo + ((hi - lo) >> 1);
+            if (pred(m)) hi = m;
+            else lo = m + 1;
+        }
+        return lo;
+    }
+    template <typename P>
+    static int64_t last_true(int64_t a, int64_t b, P pred) {  // T..T F..F on [a, b]; a-1 if none
+        int64_t lo = a - 1, hi = b;
+        while (lo < hi) {
+            const int64_t m = hi - ((hi - lo) >> 1);
+            if (pred(m)) lo = m;
+            else hi = m - 1;
+        }
+        return lo;
+    }
+
+    // the witness fails on the new key: re-derive the exact feasible interval and a new witness
+    bool refit(const Line& lo, const Line& up, uint64_t gd) {
+        const int64_t w = wd_;
+        const Eval ew = eval(lo, up, w);
+        const bool a = ew.a, bc = ew.bc;
+        auto ok = [&](int64_t x) { return real_ok(lo, up, x); };
+        int64_t p, q;
+        if (!a && !bc) return false;
+        if (a && bc) {  // w stays real-feasible
+            uint64_t sl, sh;
+            if (int_range(&lo, &up, gd, w, &sl, &sh, ew.la, ew.ua)) {  // defensive: the cone
+                cl_ = sl;                                              // step already said no
+                ch_ = sh;
+                return true;
+            }
+            p = ok(p_) ? p_ : first_true(p_ + 1, w, ok);  // both ends by bisection around w
+            q = ok(q_) ? q_ : last_true(w, q_ - 1, ok);
+        } else if (!a) {  // the new lower line cut the right side off: a left ray below w
+            q = last_true(p_, w - 1, [&](int64_t x) { return ray_a(lo, x); });
+            if (q < p_ || !ok(q)) return false;
+            p = first_true(p_, q, ok);
+        } else {  // the new upper line or the guard cut the left side off
+            p = first_true(w + 1, q_, [&](int64_t x) { return ray_bc(lo, up, x); });
+            if (p > q_ || !ok(p)) return false;
+            q = last_true(p, q_, ok);
+        }
+        // an integer slope at some integer delta in [p, q], searched from the middle outward
+        const int64_t mid = p + ((q - p) >> 1);
+        for (int64_t k = 0; mid - k >= p || mid + k <= q; ++k) {
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                const int64_t x = sgn ? mid + k : mid - k;
+                if (x < p || x > q || (sgn && k == 0)) continue;
+                uint64_t sl, sh;
+                if (int_range(&lo, &up, gd, x, &sl, &sh)) {
+                    p_ = p;
+                    q_ = q;
+                    wd_ = x;
+                    cl_ = sl;
+                    ch_ = sh;
+                    return true;
+                }
+            }
+        }
+        return false;
+    }
+
+    // F7 choice for the committed state: least |delta| (negative first), middle slope.  The
+    // witness w is feasible; the real-feasible set I is an interval containing it.  If I holds
+    // 0 the scan runs |delta| = 0, 1, ... (both signs, exact integer test) and stops by |w|;
+    // otherwise the end of I nearest 0 is bisected and the scan walks away from 0 from there.
+    void choose(int64_t* dc, uint64_t* sc) {
+        const int64_t w = wd_;
+        const int64_t dlast = lo_.back().d;
+        auto ok = [&](int64_t x) {
+            if (!old_ok(x)) return false;
+            return lo_le_g(lo_at(x), kSlopeMax, dlast, x);
+        };
+        auto hit = [&](int64_t x) {
+            uint64_t sl, sh;
+            if (!int_range(nullptr, nullptr, gd_, x, &sl, &sh)) return false;
+            *dc = x;
+            *sc = sl + (sh - sl) / 2;
+            return true;
+        };
+        const int64_t z = w >= 0 ? (p_ > 0 ? p_ : 0) : (q_ < 0 ? q_ : 0);
+        if (z == 0 && ok(0)) {
+            for (int64_t k = 0; k <= (w >= 0 ? w : -w); ++k) {
+                if (-k >= p_ && hit(-k)) return;
+                if (k > 0 && k <= q_ && hit(k)) return;
+            }
+        } else if (w >= 0) {  // I lies right of 0: scan up from its left end
+            for (int64_t x = ok(z) ? z : first_true(z + 1, w, ok); x <= w; ++x)
+                if (hit(x)) return;
+        } else {  // I lies left of 0: scan down from its right end
+            for (int64_t x = ok(z) ? z : last_true(w, z - 1, ok); x >= w; --x)
+                if (hit(x)) return;
+        }
+        *dc = w;  // not reached: the witness is feasible
+        *sc = cl_ + (ch_ - cl_) / 2;
+    }
+};
+
 template <typename K>
-int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, void** out_blob,
-                 uint64_t* out_bytes) {
+int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, uint32_t flags,
+                 void** out_blob, uint64_t* out_bytes) {
     int32_t st = check_sorted(keys, n);
     if (st) return st;
     if (key_bits == 32 && (uint64_t)keys[n - 1] > 0xffffffffULL) return LC_ERR_TOO_LARGE;
@@ -98,14 +432,18 @@ int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, voi
     std::vector<uint64_t> params;  // interleaved base, slope
     starts.reserve(n / 8 + 16);
     params.reserve(n / 4 + 32);
+    const bool free_base = flags & LC_FLAG_FREE_INTERCEPT;
+    FreeFit ff(eps);
     for (uint64_t s = 0; s < n;) {
-        uint64_t slope;
-        uint64_t e = fit_segment(keys, n, s, eps, &slope);
+        uint64_t slope, base = (uint64_t)keys[s];
+        const uint64_t e = free_base ? ff.fit(keys, n, s, &base, &slope)
+                                     : fit_segment(keys, n, s, eps, &slope);
         starts.push_back((uint32_t)s);
-        params.push_back((uint64_t)keys[s]);
+        params.push_back(base);
         params.push_back(slope);
         s = e;
     }
+    const uint64_t bias = free_base ? 0 : eps;  // FORMAT F3 decode bias c
     const uint64_t L = starts.size();
     const uint32_t b = lc_detail::res_bits(eps);
     const Layout y = layout_of(n, L, b);
@@ -120,6 +458,7 @@ int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, voi
     h.res_bits = (uint8_t)b;
     h.eps = eps;
     h.hint_log2 = 10;
+    h.flags = flags;
     h.n = n;
     h.n_seg = L;
     h.n_hint = y.n_hint;
@@ -145,7 +484,8 @@ int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, voi
     }
     Hn[y.H] = (uint32_t)(L - 1);
 
-    // residual fields u = K[i] - floor(f(i)) + eps, LSB-first into 32-bit words
+    // residual fields u = K[i] - floor(f(i)) + eps = K[i] - base - floor(slope d / 2^32) + c,
+    // LSB-first into 32-bit words
     if (b) {
         uint32_t* Wd = (uint32_t*)(blob + y.o_words);
         uint64_t acc = 0;
@@ -156,7 +496,7 @@ int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, voi
             const uint64_t base = params[2 * j], slope = params[2 * j + 1];
             uint64_t run = 0;  // slope * d, < 2^63 by the guard
             for (uint64_t i = s; i < e; ++i, run += slope) {
-                const uint64_t u = (uint64_t)keys[i] - base - (run >> 32) + eps;
+                const uint64_t u = (uint64_t)keys[i] - base - (run >> 32) + bias;
                 acc |= u << nbits;
                 nbits += b;
                 if (nbits >= 32) {
@@ -192,7 +532,9 @@ int32_t check_header(const lc_header* h, uint64_t blob_bytes) {
     if (h->hint_log2 != 10) return LC_ERR_FORMAT;
     if (h->n == 0 || h->n >= (1ULL << 32) || h->n_seg == 0 || h->n_seg > h->n)
         return LC_ERR_FORMAT;
-    for (int i = 0; i < 40; ++i)
+    if (h->flags & ~(uint32_t)LC_FLAG_FREE_INTERCEPT) return LC_ERR_FORMAT;
+    if ((h->flags & LC_FLAG_FREE_INTERCEPT) && h->eps > kEpsMaxFree) return LC_ERR_FORMAT;
+    for (int i = 0; i < 36; ++i)
         if (h->reserved[i]) return LC_ERR_FORMAT;
     const Layout y = layout_of(h->n, h->n_seg, h->res_bits);
     if (h->n_hint != y.n_hint || h->n_words != y.W || h->off_starts != y.o_starts ||
@@ -209,17 +551,23 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxe
 
 extern "C" {
 
-int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps, void** blob,
-                  uint64_t* blob_bytes) {
+int32_t lc_encode_ex(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
+                     uint32_t flags, void** blob, uint64_t* blob_bytes) {
     if (!blob || !blob_bytes) return LC_ERR_ARG;
     if (key_bits != 32 && key_bits != 64) return LC_ERR_ARG;
-    if (eps > 0x7fffffffu) return LC_ERR_ARG;
+    if (flags & ~(uint32_t)LC_FLAG_FREE_INTERCEPT) return LC_ERR_ARG;
+    if (eps > ((flags & LC_FLAG_FREE_INTERCEPT) ? kEpsMaxFree : 0x7fffffffu)) return LC_ERR_ARG;
     if (n == 0) return LC_ERR_EMPTY;
     if (!keys) return LC_ERR_ARG;
     if (n >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
     if (key_bits == 32)
-        return encode_t((const uint32_t*)keys, n, key_bits, eps, blob, blob_bytes);
-    return encode_t((const uint64_t*)keys, n, key_bits, eps, blob, blob_bytes);
+        return encode_t((const uint32_t*)keys, n, key_bits, eps, flags, blob, blob_bytes);
+    return encode_t((const uint64_t*)keys, n, key_bits, eps, flags, blob, blob_bytes);
+}
+
+int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps, void** blob,
+                  uint64_t* blob_bytes) {
+    return lc_encode_ex(keys, n, key_bits, eps, 0, blob, blob_bytes);
 }
 
 void lc_free(void* blob) { std::free(blob); }
@@ -232,6 +580,8 @@ int32_t lc_validate(const void* blob, uint64_t blob_bytes) {
     if (st) return st;
     const uint8_t* B = (const uint8_t*)blob;
     const uint64_t n = h.n, L = h.n_seg, b = h.res_bits, eps = h.eps;
+    const bool free_base = h.flags & LC_FLAG_FREE_INTERCEPT;
+    const uint64_t bias = free_base ? 0 : eps;  // FORMAT F3 decode bias c
     // zero filler between header/sections
     const uint64_t sec_beg[4] = {h.off_starts, h.off_params, h.off_hint, h.off_words};
     const uint64_t sec_end[4] = {h.off_starts + 4 * (L + 1), h.off_params + 16 * L,
@@ -272,10 +622,10 @@ int32_t lc_validate(const void* blob, uint64_t blob_bytes) {
                 u = (two >> (p & 31)) & ((1ULL << b) - 1);
             }
             if (u > 2 * eps) return LC_ERR_FORMAT;
-            if (i == S[j] && u != eps) return LC_ERR_FORMAT;  // anchor: base_j = K[s_j]
+            if (!free_base && i == S[j] && u != eps) return LC_ERR_FORMAT;  // F2 anchor
             const u128 full = (u128)base + (run >> 32) + u;
-            if (full < eps || full - eps > kmax) return LC_ERR_FORMAT;
-            const uint64_t key = (uint64_t)(full - eps);
+            if (full < bias || full - bias > kmax) return LC_ERR_FORMAT;
+            const uint64_t key = (uint64_t)(full - bias);
             if (i > 0 && key <= prev) return LC_ERR_FORMAT;
             prev = key;
         }

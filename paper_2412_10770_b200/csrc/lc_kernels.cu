@@ -19,8 +19,9 @@
 //    thread, L2 evict_last for the search structures and evict_first for the gathers.
 //  * Range decode: one warp per 32 ranges (lane-parallel search); len == 64 gathers each
 //    range's slices through a per-warp cp.async ring and decodes from shared memory.
-//  * Successor search / intersection: binary search over the anchored segment bases
-//    (segments as skip pointers), then inside one segment.
+//  * Successor search / intersection: binary search over the segments' first keys (the
+//    anchored bases, or decoded first keys for F7 blobs: segments as skip pointers), then
+//    inside one segment.
 #include <cuda_runtime.h>
 
 #include <array>
@@ -96,7 +97,7 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     a.i1 = (uint32_t)i1;
     a.chunk0 = (uint32_t)(i0 >> 10);
     a.nchunks = (uint32_t)((i1 - i0 + 1023) >> 10);
-    a.eps = v->h.eps;
+    a.bias = bias_of(v);
     a.nwords = (uint32_t)v->h.n_words;
     const uint32_t b = v->h.res_bits;
     a.warp_bytes = warp_bytes_for(b);
@@ -158,7 +159,8 @@ int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64
     a.qdiv = qdiv;
     a.n = (uint32_t)v->h.n;
     a.b = v->h.res_bits;
-    a.eps = v->h.eps;
+    a.bias = bias_of(v);
+    a.center = v->h.eps - a.bias;
     a.mask = mask_of(a.b);
     const uint64_t per = 256 * access_per_thread(mode);
     const uint64_t grid = (q + per - 1) / per;
@@ -224,7 +226,7 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     a.n = (uint32_t)v->h.n;
     a.L = (uint32_t)v->h.n_seg;
     a.b = v->h.res_bits;
-    a.eps = v->h.eps;
+    a.bias = bias_of(v);
     a.mask = mask_of(a.b);
     a.nwords = (uint32_t)v->h.n_words;
     const uint64_t grid = (q + 255) / 256;  // 8 warps x 32 ranges per CTA
@@ -270,12 +272,19 @@ int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t*
     a.n = (uint32_t)v->h.n;
     a.L = (uint32_t)v->h.n_seg;
     a.b = v->h.res_bits;
-    a.eps = v->h.eps;
+    a.bias = bias_of(v);
     a.mask = mask_of(a.b);
     const uint64_t grid = (m + 255) / 256;
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
-    if (v->h.key_bits == 64) lc_next_geq_kernel<true><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
-    else lc_next_geq_kernel<false><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (unsigned)grid;
+    if (is_free(v)) {
+        if (v->h.key_bits == 64) lc_next_geq_kernel<true, true><<<g, 256, 0, st>>>(a);
+        else lc_next_geq_kernel<false, true><<<g, 256, 0, st>>>(a);
+    } else {
+        if (v->h.key_bits == 64) lc_next_geq_kernel<true, false><<<g, 256, 0, st>>>(a);
+        else lc_next_geq_kernel<false, false><<<g, 256, 0, st>>>(a);
+    }
     lc_detail::count_launch(1);
     return cuda_status();
 }
@@ -307,14 +316,19 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     g.nb = (uint32_t)b->h.n;
     g.Lb = (uint32_t)b->h.n_seg;
     g.b = b->h.res_bits;
-    g.eps = b->h.eps;
+    g.bias = bias_of(b);
     g.mask = mask_of(g.b);
     g.nblk = (uint32_t)((na + 255) / 256);
     cudaStream_t st = (cudaStream_t)stream;
     int32_t rc = launch_decode(a, 0, na, sc, st);
     if (rc) return rc;
-    if (kw == 8) lc_isect_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g);
-    else lc_isect_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g);
+    if (is_free(b)) {
+        if (kw == 8) lc_isect_flag_kernel<true, true><<<g.nblk, 256, 0, st>>>(g);
+        else lc_isect_flag_kernel<false, true><<<g.nblk, 256, 0, st>>>(g);
+    } else {
+        if (kw == 8) lc_isect_flag_kernel<true, false><<<g.nblk, 256, 0, st>>>(g);
+        else lc_isect_flag_kernel<false, false><<<g.nblk, 256, 0, st>>>(g);
+    }
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (kw == 8) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
     else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);

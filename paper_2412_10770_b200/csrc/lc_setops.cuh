@@ -4,15 +4,16 @@
 #pragma once
 
 // ------------------------------------------------------ successor search and intersection
-// Key-space search uses the segments as skip pointers (Fig. 4b): with the
-// FORMAT F2 anchor, base_j = K[s_j] and the bases are strictly increasing, so segment j covers
-// exactly the keys [base_j, base_{j+1}).  next_geq(x) = binary search over the bases, then a
-// binary search inside the one segment, decoding only the probed keys (never a whole segment).
+// Key-space search uses the segments as skip pointers (Fig. 4b): segment j
+// covers exactly the keys [K[s_j], K[s_{j+1}]).  With the FORMAT F2 anchor K[s_j] = base_j (one
+// load per search step); F7 blobs decode K[s_j] = base_j + u(s_j).  next_geq(x) = binary search
+// over the first keys, then a binary search inside the one segment, decoding only the probed
+// keys (never a whole segment).
 __device__ __forceinline__ uint64_t key_at(const Sections& sec, uint32_t i, uint32_t s,
-                                           ulonglong2 pr, uint32_t b, uint32_t mask, uint32_t eps,
+                                           ulonglong2 pr, uint32_t b, uint32_t mask, uint32_t bias,
                                            uint64_t once) {
     const uint32_t u = b ? field_of(field_words(sec, i, b, once), i, b, mask) : 0;
-    return pr.x + pred_plus(pr.y, i - s, u - eps);
+    return pr.x + pred_plus(pr.y, i - s, u - bias);
 }
 
 struct SuccResult {
@@ -20,28 +21,41 @@ struct SuccResult {
     uint64_t key;  // K[idx], 0 if none
 };
 
+// K[s_j]: base_j for anchored blobs (F2); base_j + u(s_j) for F7 blobs (bias 0, the base is
+// the band floor, not a key), one more dependent load (the starts and params loads overlap)
+template <bool FREE>
+__device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, uint32_t b,
+                                              uint32_t mask, uint64_t keep, uint64_t once) {
+    const uint64_t base = __ldg((const uint64_t*)sec.params + 2 * (size_t)j);
+    if (!FREE) return base;
+    const uint32_t s = ldh(sec.starts + j, keep);
+    return base + (b ? field_of(field_words(sec, s, b, once), s, b, mask) : 0);
+}
+
+// Key-space search over the segments' first keys (strictly increasing in both formats), then
+// a binary search inside the one segment.
+template <bool FREE>
 __device__ SuccResult next_geq_one(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
-                                   uint32_t mask, uint32_t eps, uint64_t x, uint64_t keep,
+                                   uint32_t mask, uint32_t bias, uint64_t x, uint64_t keep,
                                    uint64_t once) {
-    const uint64_t* bases = (const uint64_t*)sec.params;  // base_j at bases[2 j]
-    const uint64_t b0 = __ldg(bases);
-    if (x <= b0) return {0u, b0};
-    uint32_t lo = 0, hi = L - 1;  // max{j : base_j <= x}
+    const uint64_t k0 = seg_first<FREE>(sec, 0, b, mask, keep, once);
+    if (x <= k0) return {0u, k0};
+    uint32_t lo = 0, hi = L - 1;  // max{j : K[s_j] <= x}
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(bases + 2 * (size_t)mid) <= x) lo = mid;
+        if (seg_first<FREE>(sec, mid, b, mask, keep, once) <= x) lo = mid;
         else hi = mid - 1;
     }
     const uint32_t j = lo;
     const uint32_t s = ldh(sec.starts + j, keep), e = ldh(sec.starts + j + 1, keep);
     const ulonglong2 pr = ldh(sec.params + j, once);
-    uint32_t l = s + 1, r = e;  // K[s] = base_j <= x; answer in (s, e]
-    if (pr.x == x) return {s, x};
+    uint32_t l = s + 1, r = e;  // K[s] <= x; answer in (s, e]
+    if ((FREE ? key_at(sec, s, s, pr, b, mask, bias, once) : pr.x) == x) return {s, x};
     uint64_t kr = 0;
     bool have = false;
     while (l < r) {
         const uint32_t mid = (l + r) >> 1;
-        const uint64_t km = key_at(sec, mid, s, pr, b, mask, eps, once);
+        const uint64_t km = key_at(sec, mid, s, pr, b, mask, bias, once);
         if (km >= x) {
             r = mid;
             kr = km;
@@ -51,11 +65,11 @@ __device__ SuccResult next_geq_one(const Sections& sec, uint32_t n, uint32_t L, 
         }
     }
     if (l < e) {
-        if (!have || r != l) kr = key_at(sec, l, s, pr, b, mask, eps, once);
+        if (!have || r != l) kr = key_at(sec, l, s, pr, b, mask, bias, once);
         return {l, kr};
     }
     if (e >= n) return {n, 0};
-    return {e, __ldg(bases + 2 * (size_t)(j + 1))};  // K[e] = base_{j+1} > x
+    return {e, seg_first<FREE>(sec, j + 1, b, mask, keep, once)};  // K[e] = K[s_{j+1}] > x
 }
 
 struct SuccArgs {
@@ -64,10 +78,10 @@ struct SuccArgs {
     uint64_t* out_idx;
     void* out_key;
     uint64_t m;
-    uint32_t n, L, b, eps, mask;
+    uint32_t n, L, b, bias, mask;
 };
 
-template <bool K64>
+template <bool K64, bool FREE>
 __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
     if (t >= a.m) return;
@@ -75,7 +89,7 @@ __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
     const uint64_t x = __ldg(a.x + t);
     SuccResult r;
     if (!K64 && x > 0xffffffffull) r = {a.n, 0};
-    else r = next_geq_one(a.sec, a.n, a.L, a.b, a.mask, a.eps, x, keep, once);
+    else r = next_geq_one<FREE>(a.sec, a.n, a.L, a.b, a.mask, a.bias, x, keep, once);
     if (a.out_idx) a.out_idx[t] = r.idx;
     if (a.out_key) put<K64>((uint8_t*)a.out_key + t * (K64 ? 8 : 4), r.key, 0);
 }
@@ -90,10 +104,10 @@ struct IsectArgs {
     uint32_t* counts;       // per-CTA match counts, then exclusive offsets; [nblk] = total
     void* out;
     uint64_t* d_count;
-    uint32_t na, nb, Lb, b, eps, mask, nblk;
+    uint32_t na, nb, Lb, b, bias, mask, nblk;
 };
 
-template <bool K64>
+template <bool K64, bool FREE>
 __global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
     __shared__ uint32_t warp_cnt[8];
     const uint32_t t = blockIdx.x * 256 + threadIdx.x;
@@ -102,7 +116,7 @@ __global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
     bool hit = false;
     if (t < a.na) {
         const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
-        const SuccResult r = next_geq_one(a.sb, a.nb, a.Lb, a.b, a.mask, a.eps, x, keep, once);
+        const SuccResult r = next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, x, keep, once);
         hit = r.idx < a.nb && r.key == x;
     }
     const uint32_t bal = __ballot_sync(kFull, hit);

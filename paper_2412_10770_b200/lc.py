@@ -23,6 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 
 LC_OK, LC_ERR_ARG, LC_ERR_EMPTY, LC_ERR_UNSORTED = 0, -1, -2, -3
 LC_ERR_TOO_LARGE, LC_ERR_FORMAT, LC_ERR_ALLOC, LC_ERR_CUDA = -4, -5, -6, -7
+LC_FLAG_FREE_INTERCEPT = 1  # FORMAT F7
 
 
 class lc_header(C.Structure):
@@ -31,7 +32,8 @@ class lc_header(C.Structure):
         ("res_bits", C.c_uint8), ("eps", C.c_uint32), ("hint_log2", C.c_uint32),
         ("n", C.c_uint64), ("n_seg", C.c_uint64), ("n_hint", C.c_uint64), ("n_words", C.c_uint64),
         ("off_starts", C.c_uint64), ("off_params", C.c_uint64), ("off_hint", C.c_uint64),
-        ("off_words", C.c_uint64), ("total_bytes", C.c_uint64), ("reserved", C.c_uint8 * 40),
+        ("off_words", C.c_uint64), ("total_bytes", C.c_uint64), ("flags", C.c_uint32),
+        ("reserved", C.c_uint8 * 36),
     ]
 
 
@@ -45,6 +47,7 @@ class lc_view(C.Structure):
 _p, _u64, _u32, _i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32
 _sig = {
     "lc_encode": ([_p, _u64, _u32, _u32, C.POINTER(_p), C.POINTER(_u64)], _i32),
+    "lc_encode_ex": ([_p, _u64, _u32, _u32, _u32, C.POINTER(_p), C.POINTER(_u64)], _i32),
     "lc_free": ([_p], None),
     "lc_validate": ([_p, _u64], _i32),
     "lc_view_init": ([C.POINTER(lc_view), _p, _p, _u64], _i32),
@@ -94,8 +97,9 @@ def launch_count() -> int:
 
 
 # ---------------------------------------------------------------------------- host side
-def encode(keys: np.ndarray, eps: int, key_bits: int | None = None) -> bytes:
-    """lc_encode: host blob (FORMAT F1-F6) of sorted keys (uint32 or uint64 numpy array)."""
+def encode(keys: np.ndarray, eps: int, key_bits: int | None = None, free: bool = False) -> bytes:
+    """lc_encode / lc_encode_ex: host blob of sorted keys (uint32 or uint64 numpy array);
+    anchored greedy (FORMAT F1-F6) or, with free=True, the free-intercept encoder (F7)."""
     k = np.asarray(keys)
     if key_bits is None:
         key_bits = 32 if k.dtype == np.uint32 else 64
@@ -104,8 +108,9 @@ def encode(keys: np.ndarray, eps: int, key_bits: int | None = None) -> bytes:
             raise LcError(LC_ERR_TOO_LARGE, "lc_encode")
     k = np.ascontiguousarray(k, dtype=np.uint32 if key_bits == 32 else np.uint64)
     out, nb = C.c_void_p(), C.c_uint64()
-    _check(_lib.lc_encode(k.ctypes.data if k.size else None, k.size, key_bits, eps,
-                          C.byref(out), C.byref(nb)), "lc_encode")
+    _check(_lib.lc_encode_ex(k.ctypes.data if k.size else None, k.size, key_bits, eps,
+                             LC_FLAG_FREE_INTERCEPT if free else 0, C.byref(out), C.byref(nb)),
+           "lc_encode_ex")
     try:
         return C.string_at(out.value, nb.value)
     finally:

@@ -135,6 +135,82 @@ def test_header_struct_matches_format(lc):
         bl.o_starts, bl.o_params, bl.o_hint, bl.o_words, len(blob))
 
 
+# ------------------------------------------------------------ FORMAT F7 (NEXT-3, free intercept)
+@pytest.mark.parametrize("seed", range(5000, 5120))
+def test_free_blob_equals_oracle_fuzz(lc, seed):
+    """The product's free-intercept encoder (line envelopes + witness cone) emits the same
+    bytes as the oracle's per-intercept brute force (FORMAT F7 is normative)."""
+    keys, eps, kb, law = fuzz_case(seed, n_max=8_000)
+    eps = min(eps, 4095)  # the oracle is O(N eps)
+    a = lc.encode(keys, eps, kb, free=True)
+    assert a == orc.encode(keys, eps, kb, free=True), (seed, law, eps)
+    assert lc.validate(a) == 0 and lc.header(a).flags == lc.LC_FLAG_FREE_INTERCEPT
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_free_blob_equals_oracle_configs_small(lc, cid):
+    keys = make_keys(cid, 300_000 if cid != 1 else None)
+    eps = {1: 63, 2: 127, 3: 255, 4: 31, 5: 127}[cid]
+    a = lc.encode(keys, eps, free=True)
+    assert a == orc.encode(keys, eps, free=True)
+    bl = blobparse.parse(a)
+    assert bl.flags == 1
+    assert len(a) == blobparse.expected_size(keys.size, bl.L, bl.b)
+
+
+def test_free_extremes(lc):
+    """Large eps (up to 2^30 - 1, where the oracle's O(N eps) scan is out of reach) is checked
+    by round trip through the oracle's decoder and both validators; small-eps extremes by bytes."""
+    rng = np.random.default_rng(77)
+    for trial in range(60):
+        n = int(rng.integers(1, 2000))
+        eps = int(rng.choice([0, 1, 3, (1 << 20) - 1, 1 << 29, (1 << 30) - 1]))
+        gmax = int(rng.choice([2, 1000, 1 << 20, 1 << 31, 1 << 40]))
+        g = rng.integers(1, gmax, n, endpoint=True).astype(np.uint64)
+        k = np.cumsum(g, dtype=np.uint64)
+        top = (1 << 64) - 1 - int(g.sum()) - 1
+        k = k + np.uint64(top if trial % 3 == 0 else int(rng.integers(0, 1 << 40)))
+        k = np.unique(k)
+        b = lc.encode(k, eps, free=True)
+        assert lc.validate(b) == 0 and orc.validate(b) == 0, trial
+        assert np.array_equal(orc.decode(b), k), trial
+        if eps <= 3:
+            assert b == orc.encode(k, eps, free=True), trial
+    for keys, eps in [(np.array([5], np.uint64), 3), (np.array([0xFFFFFFFF], np.uint32), 0),
+                      (np.array([0, 1, 2, 3], np.uint32), 2),
+                      (np.arange(5000, dtype=np.uint64) * np.uint64(1 << 20), 0)]:
+        assert lc.encode(keys, eps, free=True) == orc.encode(keys, eps, free=True)
+
+
+def test_free_encode_errors_and_validator(lc):
+    with pytest.raises(lc.LcError) as e:
+        lc.encode(np.array([1, 2], np.uint64), 1 << 30, free=True)
+    assert e.value.code == lc.LC_ERR_ARG
+    keys = make_keys(5, 7000)
+    blob = lc.encode(keys, 127, free=True)
+    bl = blobparse.parse(blob)
+
+    def put(off, val):
+        b = bytearray(blob)
+        b[off:off + len(val)] = val
+        return bytes(b)
+
+    variants = [
+        blob,
+        put(88, b"\x02"),                                   # unknown flag bit
+        put(88, b"\x00"),                                   # read as anchored: anchor/bias break
+        put(8, np.uint32(1 << 30).tobytes()),               # eps above the F7 limit
+        put(bl.o_params, np.uint64(int(bl.base[0]) + 1).tobytes()),
+        put(bl.o_params + 16, np.uint64(int(bl.base[1]) + 10**6).tobytes()),
+        put(bl.o_words, np.uint32(int(bl.words[0]) ^ 1).tobytes()),
+    ]
+    for i, v in enumerate(variants):
+        want = orc.validate(v)
+        got = lc.validate(v)
+        assert (got == 0) == (want == 0), (i, got, want)
+    assert lc.validate(variants[0]) == 0 and lc.validate(variants[1]) != 0
+
+
 def test_product_never_touches_oracle():
     """The product path must not import, load or call anything under oracle/ (task ②/③)."""
     pkg = os.path.join(ROOT, "paper_2412_10770_b200")

@@ -56,6 +56,15 @@ def main():
     for cid in (1, 2, 3, 4):
         keys = make_keys(cid, 70_001)
         cases.append((keys, CONFIGS[cid].eps, CONFIGS[cid].key_bits, f"cfg{cid}"))
+    # FORMAT F7 (free intercept): bias 0 and the first-key search of next_geq
+    for s in range(7100, 7130):
+        keys, eps, kb, law = fuzz_case(s, n_max=60_000)
+        eps = min(eps, (1 << 30) - 1)
+        cases.append((keys, eps, kb, "free-" + law, lc.encode(keys, eps, kb, free=True)))
+    for cid in (1, 2, 4, 5):
+        keys = make_keys(cid, 70_001)
+        cases.append((keys, CONFIGS[cid].eps, CONFIGS[cid].key_bits, f"free-cfg{cid}",
+                      lc.encode(keys, CONFIGS[cid].eps, free=True)))
     for case in cases:
         keys, eps, kb, law = case[:4]
         blob = case[4] if len(case) > 4 else lc.encode(keys, eps, kb)
@@ -87,6 +96,10 @@ def main():
     out, cnt = lc.union(va, vb)
     c = int(cnt.item())
     check("union", np.array_equal(h(out[:c], np.uint64), setops.union(a, k5)))
+    vf = lc.View(lc.encode(k5, 127, free=True), device=dev)
+    out, cnt = lc.intersect(va, vf)
+    c = int(cnt.item())
+    check("intersect-free", np.array_equal(h(out[:c], np.uint64), setops.intersect(a, k5)))
     print(f"bounds check ok: {checks} checks, 0 violations")
 
 
