@@ -264,7 +264,9 @@ def run_gpu(args):
     keys = make_keys(cid)
     n = keys.size
     w = spec.key_bits // 8
+    t_enc = time.perf_counter()
     blob = lc.encode(keys, spec.eps)
+    t_enc = time.perf_counter() - t_enc
     h = lc.header(blob)
     view = lc.View(blob, device=dev)
     out = view.out_tensor(n)
@@ -329,6 +331,56 @@ def run_gpu(args):
     d2h_gbps = n * w / (cp_ev[1].elapsed_time(cp_ev[2]) * 1e-3) / 1e9
     e2e_floor_ms = max(len(blob) / h2d_gbps, n * w / d2h_gbps) / 1e6  # full-duplex overlap
     del h_blob, d_blob, h_out
+
+    # ---- NEXT-3: the same keys under FORMAT F7 (free-intercept segments), same kernels
+    free = None
+    if not args.no_free:
+        t_encf = time.perf_counter()
+        blob_f = lc.encode(keys, spec.eps, free=True)
+        t_encf = time.perf_counter() - t_encf
+        hf = lc.header(blob_f)
+        view_f = lc.View(blob_f, device=dev)
+        alg_f = len(blob_f) + n * w
+        reps = max(5, min(args.steps, 50))
+        with torch.cuda.stream(stream):
+            tf, pf = _time_launches(lambda: lc.decode(view_f, out, stream=stream), stream, reps, 3)
+        ref = torch.from_numpy(keys.view(np.int64) if w == 8 else keys.view(np.int32)).to(dev)
+        ok_f = torch.equal(out, ref)
+        frng = np.random.default_rng(77)
+        d_fi = torch.from_numpy(frng.integers(0, n, 10_000_000).astype(np.int64)).to(dev)
+        fa_out = torch.empty(d_fi.numel(), dtype=out.dtype, device=dev)
+        d_fx = torch.from_numpy(frng.integers(0, int(keys[-1]), 10_000_000, dtype=np.uint64)
+                                .view(np.int64)).to(dev)
+        f_idx = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
+        f_key = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
+        with torch.cuda.stream(stream):
+            _, pfa = _time_launches(lambda: lc.access(view_f, d_fi, fa_out, stream=stream),
+                                    stream, reps, 2)
+            _, pfn = _time_launches(lambda: lc.next_geq(view_f, d_fx, f_idx, f_key,
+                                                        stream=stream), stream, reps, 2)
+            _, pan = _time_launches(lambda: lc.next_geq(view, d_fx, f_idx, f_key,
+                                                        stream=stream), stream, reps, 2)
+        ok_f = ok_f and torch.equal(fa_out, ref[d_fi])
+        del ref
+        if not ok_f:
+            raise SystemExit("F7 decode/access mismatch")
+        kf = statistics.mean(pf)
+        free = {
+            "format": "FORMAT F7: free integer intercept (O'Rourke rule on the lattice), "
+                      "header flag 1, decode bias 0",
+            "segments": int(hf.n_seg), "segments_anchored": int(h.n_seg),
+            "segment_reduction": 1 - hf.n_seg / h.n_seg,
+            "blob_bytes": len(blob_f), "bits_per_int": 8 * len(blob_f) / n,
+            "ratio_r": len(blob_f) / (n * w),
+            "decode_GBps": alg_f / kf / 1e9, "decode_keys_per_s": n / kf,
+            "decode_keys_per_s_anchored": n / kern, "hbm_frac": alg_f / kf / 1e9 / peak,
+            "lookups_per_s": d_fi.numel() / statistics.mean(pfa),
+            "next_geq_per_s": d_fx.numel() / statistics.mean(pfn),
+            "next_geq_per_s_anchored": d_fx.numel() / statistics.mean(pan),
+            "encode_keys_per_s_host": n / t_encf, "encode_keys_per_s_host_anchored": n / t_enc,
+            "bit_exact": True,
+        }
+        del view_f, d_fi, fa_out, d_fx, f_idx, f_key
 
     # ---- random access + range decodes (config 5), reported beside the headline
     access = None
@@ -453,6 +505,7 @@ def run_gpu(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "access": access,
+        "free_intercept": free,
     }
     if t_cpu is not None:
         line["cpu_baseline"] = {
@@ -473,6 +526,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-access", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-free", action="store_true", help="skip the FORMAT F7 block")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

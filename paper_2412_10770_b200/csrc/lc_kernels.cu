@@ -269,6 +269,7 @@ int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t*
     a.out_idx = d_out_idx;
     a.out_key = d_out_key;
     a.m = m;
+    a.band = 2 * (uint64_t)v->h.eps;
     a.n = (uint32_t)v->h.n;
     a.L = (uint32_t)v->h.n_seg;
     a.b = v->h.res_bits;
@@ -317,6 +318,7 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     g.Lb = (uint32_t)b->h.n_seg;
     g.b = b->h.res_bits;
     g.bias = bias_of(b);
+    g.band = 2 * (uint64_t)b->h.eps;
     g.mask = mask_of(g.b);
     g.nblk = (uint32_t)((na + 255) / 256);
     cudaStream_t st = (cudaStream_t)stream;

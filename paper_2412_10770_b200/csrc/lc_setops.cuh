@@ -34,16 +34,27 @@ __device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, u
 
 // Key-space search over the segments' first keys (strictly increasing in both formats), then
 // a binary search inside the one segment.
+// For F7 blobs K[s_j] lies in [base_j, base_j + 2 eps] (the residual u <= 2 eps, bias 0), so
+// a search step decodes the first key only when x falls inside that band (band = 2 eps).
 template <bool FREE>
 __device__ SuccResult next_geq_one(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
-                                   uint32_t mask, uint32_t bias, uint64_t x, uint64_t keep,
-                                   uint64_t once) {
+                                   uint32_t mask, uint32_t bias, uint64_t band, uint64_t x,
+                                   uint64_t keep, uint64_t once) {
     const uint64_t k0 = seg_first<FREE>(sec, 0, b, mask, keep, once);
     if (x <= k0) return {0u, k0};
     uint32_t lo = 0, hi = L - 1;  // max{j : K[s_j] <= x}
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (seg_first<FREE>(sec, mid, b, mask, keep, once) <= x) lo = mid;
+        bool le;
+        if (FREE) {
+            const uint64_t base = __ldg((const uint64_t*)sec.params + 2 * (size_t)mid);
+            if (base > x) le = false;
+            else if (x - base >= band) le = true;
+            else le = seg_first<FREE>(sec, mid, b, mask, keep, once) <= x;
+        } else {
+            le = seg_first<FREE>(sec, mid, b, mask, keep, once) <= x;
+        }
+        if (le) lo = mid;
         else hi = mid - 1;
     }
     const uint32_t j = lo;
@@ -78,6 +89,7 @@ struct SuccArgs {
     uint64_t* out_idx;
     void* out_key;
     uint64_t m;
+    uint64_t band;  // 2 eps (F7 first-key band)
     uint32_t n, L, b, bias, mask;
 };
 
@@ -89,7 +101,7 @@ __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
     const uint64_t x = __ldg(a.x + t);
     SuccResult r;
     if (!K64 && x > 0xffffffffull) r = {a.n, 0};
-    else r = next_geq_one<FREE>(a.sec, a.n, a.L, a.b, a.mask, a.bias, x, keep, once);
+    else r = next_geq_one<FREE>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, keep, once);
     if (a.out_idx) a.out_idx[t] = r.idx;
     if (a.out_key) put<K64>((uint8_t*)a.out_key + t * (K64 ? 8 : 4), r.key, 0);
 }
@@ -104,6 +116,7 @@ struct IsectArgs {
     uint32_t* counts;       // per-CTA match counts, then exclusive offsets; [nblk] = total
     void* out;
     uint64_t* d_count;
+    uint64_t band;          // 2 eps of list B (F7 first-key band)
     uint32_t na, nb, Lb, b, bias, mask, nblk;
 };
 
@@ -116,7 +129,8 @@ __global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
     bool hit = false;
     if (t < a.na) {
         const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
-        const SuccResult r = next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, x, keep, once);
+        const SuccResult r =
+            next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, keep, once);
         hit = r.idx < a.nb && r.key == x;
     }
     const uint32_t bal = __ballot_sync(kFull, hit);
