@@ -163,9 +163,13 @@ uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b);
 
 /* Union of two compressed lists, the OR query of inverted-index processing:
  * d_out receives the sorted keys present in either list (each once) and *d_count (device
- * uint64) their number.  Both lists are decoded into d_scratch (>= lc_union_scratch_bytes(a, b)
- * bytes, 256-byte aligned); keys of b absent from a are compacted, then merged with a by a
- * merge-path pass.  d_out capacity: a->h.n + b->h.n keys.  Same key_bits required. */
+ * uint64) their number.  Only the shorter list s is decoded (into d_scratch, >=
+ * lc_union_scratch_bytes(a, b) bytes, 256-byte aligned); each of its keys is searched in the
+ * longer list l with next_geq (segments as skip pointers), the keys absent from l are written
+ * to their final slots, and l is decoded once straight into d_out with every key shifted by
+ * the number of inserted keys below it (no decoded copy of l, no merge pass).  d_out capacity:
+ * a->h.n + b->h.n keys, aligned to the key width.  Same key_bits required.  Either argument
+ * order gives the same result. */
 int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                  void* d_out, uint64_t* d_count, lc_stream stream);
 

@@ -13,7 +13,74 @@ struct DecodeArgs {
     uint32_t bias;
     uint32_t warp_bytes;  // shared memory per warp
     uint32_t nwords;      // W (words section length)
+    const uint32_t* rho;   // lc_union fused path only (UNI kernels): see Ins
+    const uint32_t* coff;  // [h] = #{m : rho_m < 1024 h}
 };
+
+// Insertion shifts for lc_union's fused path: the long list's key i goes to output slot
+// i + #{m : rho_m <= i}, where rho (sorted) holds, for each short-list key absent from the long
+// list, the number of long-list keys below it (its own slot is m + rho_m).  Per chunk the
+// entries with rho in the chunk, [coff[h], coff[h+1]), are read in batches of 32 (one per lane,
+// v = rho - key0); cur = #{rho < window start} and nxt = the next entry's chunk offset are
+// warp-uniform, so a window holding no entry costs one compare.
+struct Ins {
+    const uint32_t* rho;
+    uint32_t key0, cur, end, bat, v, nxt;
+};
+
+// chunk start: [lo, hi) = [coff[h], coff[h+1]) (loaded one chunk ahead); the first batch's
+// load is issued here, before the chunk's staging, and consumed by ins_ready after it
+__device__ __forceinline__ void ins_begin(Ins& s, uint32_t lo, uint32_t hi, uint32_t key0,
+                                          uint32_t lane) {
+    s.key0 = key0;
+    s.cur = s.bat = lo;
+    s.end = hi;
+    s.v = lo + lane < hi ? __ldg(s.rho + lo + lane) - key0 : kFull;
+}
+__device__ __forceinline__ void ins_ready(Ins& s) {
+    s.nxt = __reduce_min_sync(kFull, s.v);  // the first entry; kFull when the chunk has none
+}
+
+// shift (in keys) of this lane's key wb + lane; the windows of a chunk are asked in order.
+// Entries at distinct positions are one bit each in a REDUX.OR mask (add = popc of the bits
+// at or below the lane); equal ranks (several absent keys between two long-list keys) count
+// one by one.
+template <bool UNI>
+__device__ __forceinline__ uint32_t ins_shift(Ins& s, uint32_t wb, uint32_t lane) {
+    if (!UNI) return 0;
+    const uint32_t o = wb - s.key0;
+    if (s.nxt - o >= 32) return s.cur;  // warp-uniform: no entry in this window (nxt >= o)
+    const uint32_t c0 = s.cur;
+    uint32_t add = 0;
+    for (;;) {
+        const uint32_t x = s.v - o;  // < 32: this batch's entries in the window
+        uint32_t in = __ballot_sync(kFull, x < 32);
+        const uint32_t n = __popc(in);
+        const uint32_t M = __reduce_or_sync(kFull, bit_or_zero(x));
+        s.cur += n;
+        if (__popc(M) == n) {
+            add += __popc(M & ((2u << lane) - 1));  // bits at or below the lane
+        } else {
+            while (in) {
+                const uint32_t k = __ffs(in) - 1;
+                in &= in - 1;
+                add += __shfl_sync(kFull, x, k) <= lane;
+            }
+        }
+        if (s.cur - s.bat < 32 || s.cur == s.end) break;
+        s.bat = s.cur;  // batch used up inside the window: next 32 entries
+        s.v = s.bat + lane < s.end ? __ldg(s.rho + s.bat + lane) - s.key0 : kFull;
+    }
+    // first unconsumed entry: every entry below the window's end has been counted
+    s.nxt = __reduce_min_sync(kFull, s.v < o + 32 ? kFull : s.v);
+    return c0 + add;
+}
+
+template <bool K64, bool UNI>
+__device__ __forceinline__ void* shifted(void* outw, Ins& ins, uint32_t wb, uint32_t lane) {
+    if (!UNI) return outw;
+    return (uint8_t*)outw + (size_t)ins_shift<UNI>(ins, wb, lane) * (K64 ? 8 : 4);
+}
 
 // Per-warp shared-memory page: [mbarrier | starts (kSegCap+4) | params kSegCap | words]
 __host__ __device__ constexpr uint32_t page_starts_off() { return 16; }
@@ -65,12 +132,12 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
 // segment and the offset d = i - s_j with no search.  key = base + t with
 // t = floor(slope d / 2^32) + u - bias = K[i] - base_j in [0, 2^32) (FORMAT F2 anchor, or the
 // F7 band floor with bias 0, plus the guard).
-template <bool K64, uint32_t B, bool CHECK, bool FULL>
+template <bool K64, uint32_t B, bool CHECK, bool FULL, bool UNI>
 __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
                                               uint32_t& sb, uint32_t jlast, uint32_t wb,
                                               uint32_t w, uint32_t lane, uint32_t lmask,
                                               uint32_t lw, uint32_t ls, uint32_t bias,
-                                              void* outw, uint32_t valid) {
+                                              void* outw, uint32_t valid, Ins& ins) {
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)  // warp-uniform: re-page a dense chunk
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
@@ -83,6 +150,7 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
     const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
     LC_CHECK(B && (FULL || lane < valid), w * B + lw + 1, pg.nw);
     const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - bias);
+    outw = shifted<K64, UNI>(outw, ins, wb, lane);
     if (FULL || lane < valid) put<K64>(outw, pr.x, t);
     // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
     // the advance there so jb stays a valid staged index
@@ -93,11 +161,12 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
 // Two windows at once: keys [wb, wb + 64), lane handles wb + lane and wb + 32 + lane.  One
 // candidate load / vote serves both halves when fewer than 32 segment starts fall inside;
 // otherwise it falls back to two single windows.  w2 = pair index (windows 2 w2, 2 w2 + 1).
-template <bool K64, uint32_t B, bool CHECK>
+template <bool K64, uint32_t B, bool CHECK, bool UNI>
 __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w2, uint32_t lane, uint32_t lmask,
-                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw) {
+                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw,
+                                            Ins& ins) {
     constexpr uint32_t kw = K64 ? 8 : 4;
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
@@ -105,10 +174,11 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
     const uint32_t inside = __ballot_sync(kFull, x < 64);
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
-        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask, lw,
-                                           ls, bias, outw, 32);
-        decode_window<K64, B, CHECK, true>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
-                                           lmask, lw, ls, bias, (uint8_t*)outw + 32 * kw, 32);
+        decode_window<K64, B, CHECK, true, UNI>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask,
+                                                lw, ls, bias, outw, 32, ins);
+        decode_window<K64, B, CHECK, true, UNI>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
+                                                lmask, lw, ls, bias, (uint8_t*)outw + 32 * kw, 32,
+                                                ins);
         return;
     }
     const uint32_t PA = __reduce_or_sync(kFull, bit_or_zero(x));       // starts in (wb, wb+32)
@@ -126,8 +196,8 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     LC_CHECK(B, (2 * w2 + 1) * B + lw + 1, pg.nw);
     const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - bias);
     const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - bias);
-    put<K64>(outw, pA.x, tA);
-    put<K64>((uint8_t*)outw + 32 * kw, pB.x, tB);
+    put<K64>(shifted<K64, UNI>(outw, ins, wb, lane), pA.x, tA);
+    put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw, ins, wb + 32, lane), pB.x, tB);
     jb = min(jb + adv, jlast + 1);  // see decode_window
     sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
@@ -135,21 +205,22 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
 // Four windows at once: keys [wb, wb + 128), lane handles wb + 32 q + lane (q = 0..3).  One
 // candidate load / advance vote serves four quarters when fewer than 32 segment starts fall
 // inside; otherwise two pair steps.  w4 = quad index (windows 4 w4 .. 4 w4 + 3).
-template <bool K64, uint32_t B, bool CHECK>
+template <bool K64, uint32_t B, bool CHECK, bool UNI>
 __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w4, uint32_t lane, uint32_t lmask,
-                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw) {
+                                            uint32_t lw, uint32_t ls, uint32_t bias, void* outw,
+                                            Ins& ins) {
     constexpr uint32_t kw = K64 ? 8 : 4;
     if (CHECK && min(jb + 31, jlast) >= pg.pj + pg.cp)
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
     if (__ballot_sync(kFull, x < 128) == kFull) {  // >= 32 boundaries in 128 keys
-        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls, bias,
-                                   outw);
-        decode_pair<K64, B, CHECK>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask, lw,
-                                   ls, bias, (uint8_t*)outw + 64 * kw);
+        decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls,
+                                        bias, outw, ins);
+        decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask,
+                                        lw, ls, bias, (uint8_t*)outw + 64 * kw, ins);
         return;
     }
     const uint32_t adv = __popc(__ballot_sync(kFull, x <= 128));
@@ -161,7 +232,7 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         const uint32_t d = m ? lane - (31 - __clz(m)) : off + lane;
         const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
         LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
-        put<K64>((uint8_t*)outw + 32 * kw * q, pr.x,
+        put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
                  pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - bias));
         off = P ? __clz(P) + 1 : off + 32;
         jq += __popc(P);
@@ -174,7 +245,8 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
 // kernel is issue-bound: cap registers at 40 for 6 resident CTAs and skip the L2 prefetch
 // (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch);
 // dense lists keep 5 resident CTAs (<= 48 registers).
-template <bool K64, uint32_t B, bool SPARSE>
+// UNI: lc_union's fused path (stores shifted by Ins; dense settings)
+template <bool K64, uint32_t B, bool SPARSE, bool UNI = false>
 __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(const DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -193,13 +265,19 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
     const uint32_t lmask = lanemask_le();
     const uint32_t nwarps = gridDim.x * kWarpsPerCta;
     const Sections sec = a.sec;
+    Ins ins;
+    ins.rho = a.rho;
 
     uint32_t c = blockIdx.x * kWarpsPerCta + warp;
     // hint pair of the warp's next chunk, loaded one chunk ahead (hides a DRAM round trip)
-    uint32_t nj0 = 0, njl = 0;
+    uint32_t nj0 = 0, njl = 0, nlo = 0, nhi = 0;
     if (c < a.nchunks) {
         nj0 = __ldg(sec.hint + a.chunk0 + c);
         njl = __ldg(sec.hint + a.chunk0 + c + 1);
+        if (UNI) {  // the chunk's insertion range, also one chunk ahead
+            nlo = __ldg(a.coff + a.chunk0 + c);
+            nhi = __ldg(a.coff + a.chunk0 + c + 1);
+        }
     }
     for (; c < a.nchunks; c += nwarps) {
         const uint32_t h = a.chunk0 + c;
@@ -211,8 +289,16 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
             nj0 = __ldg(sec.hint + h + nwarps);
             njl = __ldg(sec.hint + h + nwarps + 1);
         }
+        if (UNI) {
+            ins_begin(ins, nlo, nhi, key0, lane);
+            if (c + nwarps < a.nchunks) {
+                nlo = __ldg(a.coff + h + nwarps);
+                nhi = __ldg(a.coff + h + nwarps + 1);
+            }
+        }
         const uint32_t wbytes = B ? ((((nk * B + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
         stage(pg, sec, j0, jlast, sec.words + (size_t)h * 32 * B, wbytes, lane);
+        if (UNI) ins_ready(ins);
         const bool has_next = !SPARSE && c + nwarps < a.nchunks;
         if (B && has_next && lane == 0)  // next chunk's residual words -> L2 now
             bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
@@ -225,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
             for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
 #pragma unroll
                 for (uint32_t k = 0; k < 2; ++k)
-                    decode_quad<K64, B, false>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k), g + k,
-                                               lane, lmask, lw, ls, a.bias, outl + 128 * kw * k);
+                    decode_quad<K64, B, false, UNI>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k),
+                                                    g + k, lane, lmask, lw, ls, a.bias,
+                                                    outl + 128 * kw * k, ins);
                 if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
                     const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
                     const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
@@ -239,14 +326,15 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(con
             for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
-                    decode_pair<K64, B, true>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
-                                              lane, lmask, lw, ls, a.bias, outl + 64 * kw * k);
+                    decode_pair<K64, B, true, UNI>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
+                                                   lane, lmask, lw, ls, a.bias, outl + 64 * kw * k,
+                                                   ins);
             }
         } else {  // ragged tail chunk
             for (uint32_t w = 0; 32 * w < nk; ++w)
-                decode_window<K64, B, true, false>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane,
-                                                   lmask, lw, ls, a.bias, outl + 32 * kw * w,
-                                                   nk - 32 * w);
+                decode_window<K64, B, true, false, UNI>(pg, sec, jb, sb, jlast, key0 + 32 * w, w,
+                                                        lane, lmask, lw, ls, a.bias,
+                                                        outl + 32 * kw * w, nk - 32 * w, ins);
         }
     }
 }

@@ -48,9 +48,9 @@ int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? LC_OK : LC_ER
 
 using DecodeFn = void (*)(DecodeArgs);
 
-template <bool K64, bool SPARSE, uint32_t... Bs>
+template <bool K64, bool SPARSE, bool UNI = false, uint32_t... Bs>
 constexpr std::array<DecodeFn, sizeof...(Bs)> decode_table(std::integer_sequence<uint32_t, Bs...>) {
-    return {{&lc_decode_kernel<K64, Bs, SPARSE>...}};
+    return {{&lc_decode_kernel<K64, Bs, SPARSE, UNI>...}};
 }
 // one instantiation per residual width b = 0..32 (compile-time field offsets and masks),
 // key width and segment density: kDecode[sparse][k64][b]
@@ -59,17 +59,21 @@ const std::array<DecodeFn, 33> kDecode[2][2] = {
      decode_table<true, false>(std::make_integer_sequence<uint32_t, 33>{})},
     {decode_table<false, true>(std::make_integer_sequence<uint32_t, 33>{}),
      decode_table<true, true>(std::make_integer_sequence<uint32_t, 33>{})}};
+// lc_union's fused path: stores shifted by the short list's insertions, kDecodeUni[k64][b]
+const std::array<DecodeFn, 33> kDecodeUni[2] = {
+    decode_table<false, false, true>(std::make_integer_sequence<uint32_t, 33>{}),
+    decode_table<true, false, true>(std::make_integer_sequence<uint32_t, 33>{})};
 
 struct GridCache {
     std::mutex mu;
     int dev = -1;
     int sms = 0;
-    int occ[2][2][33] = {};  // [sparse][K64][res_bits] -> resident CTAs per SM
+    int occ[3][2][33] = {};  // [sparse | 2 = union][K64][res_bits] -> resident CTAs per SM
 };
 GridCache g_grid;
 
 // persistent grid size for the decode kernel: SMs x resident CTAs at this smem footprint
-int persistent_grid(bool sparse, bool k64, uint32_t b) {
+int persistent_grid(int kind, bool k64, uint32_t b) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_grid.mu);
@@ -78,9 +82,9 @@ int persistent_grid(bool sparse, bool k64, uint32_t b) {
         cudaDeviceGetAttribute(&g_grid.sms, cudaDevAttrMultiProcessorCount, dev);
         std::memset(g_grid.occ, 0, sizeof g_grid.occ);
     }
-    int& occ = g_grid.occ[sparse][k64][b];
+    int& occ = g_grid.occ[kind][k64][b];
     if (occ == 0) {
-        const void* fn = (const void*)kDecode[sparse][k64][b];
+        const void* fn = (const void*)(kind == 2 ? kDecodeUni[k64][b] : kDecode[kind][k64][b]);
         const int smem = (int)(warp_bytes_for(b) * kWarpsPerCta);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
@@ -89,8 +93,12 @@ int persistent_grid(bool sparse, bool k64, uint32_t b) {
     return occ * g_grid.sms;
 }
 
-int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, cudaStream_t st) {
+// rho / coff non-null: lc_union's fused path (whole list, stores shifted by the insertions)
+int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, cudaStream_t st,
+                      const uint32_t* rho = nullptr, const uint32_t* coff = nullptr) {
     DecodeArgs a;
+    a.rho = rho;
+    a.coff = coff;
     a.sec = sections_of(v);
     a.out = d_out;
     a.i0 = (uint32_t)i0;
@@ -104,10 +112,12 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     const uint32_t smem = a.warp_bytes * kWarpsPerCta;
     const bool k64 = v->h.key_bits == 64;
     const bool sparse = v->h.n_seg * 64 < v->h.n;  // < 1 segment per 64 keys
-    const int full = persistent_grid(sparse, k64, b);
+    const int kind = coff ? 2 : sparse;
+    const int full = persistent_grid(kind, k64, b);
     const uint32_t need = (a.nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const uint32_t grid = need < (uint32_t)full ? need : (uint32_t)full;
-    kDecode[sparse][k64][b]<<<grid, kThreads, smem, st>>>(a);
+    if (coff) kDecodeUni[k64][b]<<<grid, kThreads, smem, st>>>(a);
+    else kDecode[sparse][k64][b]<<<grid, kThreads, smem, st>>>(a);
     lc_detail::count_launch(1);
     return cuda_status();
 }
@@ -184,6 +194,7 @@ int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64
     return cuda_status();
 }
 
+uint64_t r256(uint64_t x) { return (x + 255) & ~255ULL; }
 }  // namespace
 
 extern "C" {
@@ -294,7 +305,6 @@ uint64_t lc_intersect_scratch_bytes(const lc_view* a) {
     if (!a) return 0;
     const uint64_t na = a->h.n, kw = a->h.key_bits / 8;
     const uint64_t nblk = (na + 255) / 256;
-    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
     return r256(na * kw) + r256(4 * ((na + 31) / 32)) + r256(4 * (nblk + 1));
 }
 
@@ -304,7 +314,6 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_intersect_scratch_bytes(a) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
     const uint64_t na = a->h.n, kw = a->h.key_bits / 8;
-    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
     uint8_t* sc = (uint8_t*)d_scratch;
     IsectArgs g;
     g.sb = sections_of(b);
@@ -341,10 +350,11 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
 uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b) {
     if (!a || !b) return 0;
     const uint64_t na = a->h.n, nb = b->h.n, kw = a->h.key_bits / 8;
-    const uint64_t ns = na < nb ? na : nb;  // the shorter list is flagged and compacted
-    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
-    return r256(na * kw) + r256(nb * kw) + r256(ns * kw) + r256(4 * ((ns + 31) / 32)) +
-           r256(4 * ((ns + 255) / 256 + 1));
+    const uint64_t ns = na < nb ? na : nb, nl = na < nb ? nb : na;
+    const uint64_t nblk = (ns + 255) / 256;
+    // short keys, rank, flags, counts, rho, coff
+    return r256(ns * kw) + r256(4 * ns) + r256(4 * ((ns + 31) / 32)) + r256(4 * (nblk + 1)) +
+           r256(4 * ns) + r256(4 * ((nl + 1023) / 1024 + 1));
 }
 
 int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
@@ -352,39 +362,54 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_union_scratch_bytes(a, b) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
-    // union = long ∪ (short \ long): only the shorter list is searched and compacted
+    if ((uintptr_t)d_out % (a->h.key_bits / 8)) return LC_ERR_ARG;
+    // union = long ∪ (short \ long): only the shorter list is decoded, searched and compacted
     const lc_view* lg = a->h.n >= b->h.n ? a : b;
     const lc_view* sh = a->h.n >= b->h.n ? b : a;
     const uint64_t nl = lg->h.n, ns = sh->h.n, kw = a->h.key_bits / 8;
-    auto r256 = [](uint64_t x) { return (x + 255) & ~255ULL; };
-    uint8_t* sL = (uint8_t*)d_scratch;
-    uint8_t* sS = sL + r256(nl * kw);
-    uint8_t* sC = sS + r256(ns * kw);  // short \ long
-    uint32_t* flags = (uint32_t*)(sC + r256(ns * kw));
-    uint32_t* counts = (uint32_t*)((uint8_t*)flags + r256(4 * ((ns + 31) / 32)));
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool k64 = kw == 8;
+    uint8_t* p = (uint8_t*)d_scratch;
+    uint8_t* sS = p;
+    uint32_t* rank = (uint32_t*)(p += r256(ns * kw));
+    uint32_t* flags = (uint32_t*)(p += r256(4 * ns));
+    const uint64_t nblk = (ns + 255) / 256;
+    uint32_t* counts = (uint32_t*)(p += r256(4 * ((ns + 31) / 32)));
+    uint32_t* rho = (uint32_t*)(p += r256(4 * (nblk + 1)));
+    uint32_t* coff = (uint32_t*)(p += r256(4 * ns));
     IsectArgs g{};
+    g.sb = sections_of(lg);
     g.a_keys = sS;
     g.flags = flags;
     g.counts = counts;
-    g.out = sC;
-    g.d_count = d_count;  // overwritten by the merge with the union size
+    g.out = d_out;
+    g.d_count = d_count;  // |C| after the scan, then nl + |C|
     g.na = (uint32_t)ns;
-    g.nblk = (uint32_t)((ns + 255) / 256);
-    cudaStream_t st = (cudaStream_t)stream;
-    int32_t rc = launch_decode(lg, 0, nl, sL, st);
-    if (!rc) rc = launch_decode(sh, 0, ns, sS, st);
+    g.nb = (uint32_t)nl;
+    g.Lb = (uint32_t)lg->h.n_seg;
+    g.b = lg->h.res_bits;
+    g.bias = bias_of(lg);
+    g.band = 2 * (uint64_t)lg->h.eps;
+    g.mask = mask_of(g.b);
+    g.nblk = (uint32_t)nblk;
+    int32_t rc = launch_decode(sh, 0, ns, sS, st);
     if (rc) return rc;
-    const bool k64 = kw == 8;
-    if (k64) lc_union_flag_kernel<true><<<g.nblk, 256, 0, st>>>(g, sL, (uint32_t)nl);
-    else lc_union_flag_kernel<false><<<g.nblk, 256, 0, st>>>(g, sL, (uint32_t)nl);
+    if (is_free(lg)) {
+        if (k64) lc_union_rank_kernel<true, true><<<g.nblk, 256, 0, st>>>(g, rank);
+        else lc_union_rank_kernel<false, true><<<g.nblk, 256, 0, st>>>(g, rank);
+    } else {
+        if (k64) lc_union_rank_kernel<true, false><<<g.nblk, 256, 0, st>>>(g, rank);
+        else lc_union_rank_kernel<false, false><<<g.nblk, 256, 0, st>>>(g, rank);
+    }
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
-    if (k64) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
-    else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
-    const unsigned mgrid = (unsigned)((nl + ns + kMergeTile - 1) / kMergeTile);
-    if (k64) lc_merge_kernel<true><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
-    else lc_merge_kernel<false><<<mgrid, 256, 0, st>>>(sL, (uint32_t)nl, sC, counts + g.nblk, d_out, d_count);
-    lc_detail::count_launch(6);
-    return cuda_status();
+    if (k64) lc_union_place_kernel<true><<<g.nblk, 256, 0, st>>>(g, rank, rho);
+    else lc_union_place_kernel<false><<<g.nblk, 256, 0, st>>>(g, rank, rho);
+    const uint32_t H = (uint32_t)((nl + 1023) / 1024);
+    lc_union_coff_kernel<<<(H + 1 + 255) / 256, 256, 0, st>>>(rho, counts + g.nblk, H, coff, nl,
+                                                                d_count);
+    lc_detail::count_launch(4);
+    if ((rc = cuda_status())) return rc;
+    return launch_decode(lg, 0, nl, d_out, st, rho, coff);
 }
 
 int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, void* d_out,

@@ -1,4 +1,4 @@
-// lc_setops.cuh -- successor search, intersection, union (merge path)
+// lc_setops.cuh -- successor search, intersection, union (fused into the long list's decode)
 // Internal part of lc_kernels.cu: included inside its anonymous namespace (one translation
 // unit, so the launch tables and the bounds-check counter keep internal linkage).
 #pragma once
@@ -208,33 +208,27 @@ __global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) 
     }
 }
 
-// Union (OR query): both lists are decoded into scratch; the keys of the shorter
-// list that are absent from the longer one are flagged (binary search in the decoded longer
-// list) and compacted in order with the intersection's scan/scatter kernels; then one
-// merge-path pass merges the two disjoint sorted lists straight into the output.
-template <bool K64>
-__global__ void __launch_bounds__(256) lc_union_flag_kernel(const IsectArgs a, const void* a_sorted,
-                                                            uint32_t n_sorted) {
+// Union (OR query) of a short list s and a long list l, fused into l's decode:
+// no decoded copy of l and no merge pass.  Each key x of s (decoded into scratch) gets rank =
+// next_geq index in l (the number of l keys below x) from l's segments (skip pointers); the
+// keys absent from l are compacted in order (C, with rho_m = rank) and written straight to
+// their union slot m + rho_m; then l is decoded once with every key i stored at
+// i + #{m : rho_m <= i} (lc_decode_kernel<..., UNI>, Ins).
+template <bool K64, bool FREE>
+__global__ void __launch_bounds__(256) lc_union_rank_kernel(const IsectArgs a, uint32_t* rank) {
     __shared__ uint32_t warp_cnt[8];
     const uint32_t t = blockIdx.x * 256 + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    bool keep = false;
-    if (t < a.na) {  // a.a_keys = decoded B; keep keys of B not in A
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    bool absent = false;
+    if (t < a.na) {
         const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
-        uint32_t lo = 0, hi = n_sorted;  // first A[i] >= x
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            const uint64_t v = K64 ? __ldg((const uint64_t*)a_sorted + mid)
-                                   : __ldg((const uint32_t*)a_sorted + mid);
-            if (v < x) lo = mid + 1;
-            else hi = mid;
-        }
-        const uint64_t v = lo < n_sorted ? (K64 ? __ldg((const uint64_t*)a_sorted + lo)
-                                                : __ldg((const uint32_t*)a_sorted + lo))
-                                         : ~0ull;
-        keep = lo == n_sorted || v != x;
+        const SuccResult r =
+            next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, keep, once);
+        absent = !(r.idx < a.nb && r.key == x);
+        rank[t] = r.idx;
     }
-    const uint32_t bal = __ballot_sync(kFull, keep);
+    const uint32_t bal = __ballot_sync(kFull, absent);
     if (lane == 0) {
         if (t < a.na) a.flags[t >> 5] = bal;
         warp_cnt[warp] = __popc(bal);
@@ -247,61 +241,51 @@ __global__ void __launch_bounds__(256) lc_union_flag_kernel(const IsectArgs a, c
     }
 }
 
-constexpr uint32_t kMergeItems = 8;                 // output keys per thread
-constexpr uint32_t kMergeTile = 256 * kMergeItems;  // output keys per CTA
+// absent key t of s -> C position m (flags + scanned counts, as lc_isect_write_kernel):
+// rho[m] = rank[t], out[m + rank[t]] = key
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_union_place_kernel(const IsectArgs a,
+                                                             const uint32_t* rank, uint32_t* rho) {
+    __shared__ uint32_t warp_off[8];
+    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t bal = t < a.na ? a.flags[t >> 5] : 0;
+    if (lane == 0) warp_off[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = a.counts[blockIdx.x];
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t v = warp_off[w];
+            warp_off[w] = c;
+            c += v;
+        }
+    }
+    __syncthreads();
+    if ((bal >> lane) & 1) {
+        const uint32_t m = warp_off[warp] + __popc(bal & ((1u << lane) - 1));
+        const uint32_t r = rank[t];
+        rho[m] = r;
+        const size_t slot = (size_t)m + r;
+        if (K64) ((uint64_t*)a.out)[slot] = ((const uint64_t*)a.a_keys)[t];
+        else ((uint32_t*)a.out)[slot] = ((const uint32_t*)a.a_keys)[t];
+    }
+}
 
-// number of A keys among the first `diag` keys of merge(A, C) (disjoint sorted lists)
-template <typename K>
-__device__ __forceinline__ uint32_t merge_split(const K* a, uint32_t na, const K* c, uint32_t nc,
-                                                uint32_t diag) {
-    uint32_t lo = diag > nc ? diag - nc : 0, hi = min(diag, na);
+// coff[h] = #{m : rho_m < 1024 h} for h = 0..H (chunk insertion offsets); *d_count = nl + |C|
+__global__ void __launch_bounds__(256) lc_union_coff_kernel(const uint32_t* rho,
+                                                            const uint32_t* nc_ptr, uint32_t H,
+                                                            uint32_t* coff, uint64_t nl,
+                                                            uint64_t* d_count) {
+    const uint32_t h = blockIdx.x * 256 + threadIdx.x;
+    const uint32_t nc = *nc_ptr;
+    if (h == 0) *d_count = nl + nc;
+    if (h > H) return;
+    const uint64_t x = (uint64_t)h << 10;
+    uint32_t lo = 0, hi = nc;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (a[mid] < c[diag - 1 - mid]) lo = mid + 1;
+        if (__ldg(rho + mid) < x) lo = mid + 1;
         else hi = mid;
     }
-    return lo;
+    coff[h] = lo;
 }
-
-// Tiled merge path: CTA t produces outputs [t*2048, (t+1)*2048).  One thread finds the tile's
-// split on each input, the tile's slices of A and C are loaded coalesced into shared memory,
-// each thread merges 8 outputs from shared memory, and the tile is stored coalesced.
-template <bool K64>
-__global__ void __launch_bounds__(256) lc_merge_kernel(const void* A, uint32_t na, const void* C,
-                                                       const uint32_t* nc_ptr, void* out,
-                                                       uint64_t* d_count) {
-    using K = typename std::conditional<K64, uint64_t, uint32_t>::type;
-    __shared__ K sm[kMergeTile];   // A slice then C slice
-    __shared__ K so[kMergeTile];   // merged tile
-    __shared__ uint32_t bounds[4];
-    const K* a = (const K*)A;
-    const K* c = (const K*)C;
-    const uint32_t nc = *nc_ptr, total = na + nc;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = total;
-    const uint64_t t0 = (uint64_t)blockIdx.x * kMergeTile;
-    if (t0 >= total) return;
-    const uint32_t d0 = (uint32_t)t0, d1 = (uint32_t)min(t0 + kMergeTile, (uint64_t)total);
-    if (threadIdx.x < 2) {
-        const uint32_t d = threadIdx.x ? d1 : d0;
-        const uint32_t i = merge_split(a, na, c, nc, d);
-        bounds[2 * threadIdx.x] = i;
-        bounds[2 * threadIdx.x + 1] = d - i;
-    }
-    __syncthreads();
-    const uint32_t a0 = bounds[0], c0 = bounds[1], a1 = bounds[2], c1 = bounds[3];
-    const uint32_t la = a1 - a0, lcn = c1 - c0;  // la + lcn = d1 - d0
-    for (uint32_t k = threadIdx.x; k < la; k += 256) sm[k] = __ldg(a + a0 + k);
-    for (uint32_t k = threadIdx.x; k < lcn; k += 256) sm[la + k] = __ldg(c + c0 + k);
-    __syncthreads();
-    const uint32_t n = la + lcn;
-    const uint32_t dd = min(threadIdx.x * kMergeItems, n);
-    uint32_t i = merge_split(sm, la, sm + la, lcn, dd), j = dd - i;
-    for (uint32_t k = 0; k < kMergeItems && dd + k < n; ++k) {
-        const bool take_a = j >= lcn || (i < la && sm[i] < sm[la + j]);
-        so[dd + k] = take_a ? sm[i++] : sm[la + j++];
-    }
-    __syncthreads();
-    K* o = (K*)out + d0;
-    for (uint32_t k = threadIdx.x; k < n; k += 256) __stcs(o + k, so[k]);
-}
-

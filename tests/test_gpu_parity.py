@@ -429,6 +429,72 @@ def test_union_closed_form_and_edges(lc):
     _union_case(lc, a32, make_keys(1, 1_000_000), 15, 63)
 
 
+def _union_fused_case(lc, a, b, eps_a=31, eps_b=127, free=False):
+    """a short (fused path: |a| * 8 <= |b|), checked in both argument orders."""
+    assert a.size * 8 <= b.size
+    _union_case_v(lc, lc.View(lc.encode(a, eps_a), device=DEV),
+                  lc.View(lc.encode(b, eps_b, free=free), device=DEV), a, b)
+
+
+def _union_case_v(lc, va, vb, a, b):
+    want = setops.union(a, b)
+    for x, y in ((va, vb), (vb, va)):
+        out, cnt = lc.union(x, y)
+        torch.cuda.synchronize()
+        c = int(cnt.item())
+        assert c == want.size
+        assert np.array_equal(_host(out[:c], a.dtype), want)
+
+
+@pytest.mark.parametrize("free", [False, True])
+def test_union_fused_insertion_patterns(lc, free):
+    """lc_union's fused path (short list <= 1/8 of the long one): the long list is decoded once
+    with every key shifted by the number of absent short-list keys below it.  Cases: insertions
+    spread thin (<= 32 per 1024-key chunk, held in registers), clustered (> 32 per chunk and
+    > 32 per 32-key window: streamed), many absent keys between two consecutive long-list keys
+    (equal ranks), absent keys below / above every long-list key (rank 0 / n), ranks exactly at
+    chunk boundaries, long lists with n a multiple of 1024 and with a ragged tail."""
+    rng = np.random.default_rng(11)
+    for n in (1 << 16, 100_003):
+        b = np.arange(n, dtype=np.uint64) * np.uint64(16) + np.uint64(1000)
+        top = int(b[-1])
+        # thin: random keys, about half present
+        a = np.unique(np.concatenate([rng.choice(b, 300, replace=False),
+                                      rng.integers(0, top + 5000, 300).astype(np.uint64)]))
+        _union_fused_case(lc, a, b, free=free)
+        # clustered: 2000 absent keys inside one 1024-key chunk's key range
+        lo = int(b[5 * 1024 + 10])
+        a = np.unique(rng.integers(lo, lo + 16 * 300, 2000).astype(np.uint64))
+        a = a[a % 16 != 1000 % 16][: n // 10]
+        _union_fused_case(lc, a, b, free=free)
+        # equal ranks: all 15 absent keys between b[i] and b[i+1] for a few i (incl. chunk edges)
+        gaps = [0, 1023, 1024, 2047, n // 2, n - 2]
+        a = np.concatenate([b[i] + np.arange(1, 16, dtype=np.uint64) for i in gaps])
+        _union_fused_case(lc, np.sort(a), b, free=free)
+        # below and above everything, plus the key right before each chunk start (rank = 1024 h)
+        edge = b[np.arange(1024, n, 1024)] - np.uint64(1)
+        a = np.unique(np.concatenate([np.arange(0, 50, dtype=np.uint64), edge,
+                                      np.uint64(top) + np.arange(1, 60, dtype=np.uint64)]))
+        _union_fused_case(lc, a, b, free=free)
+        # a subset of b (nothing inserted) and a single key
+        _union_fused_case(lc, b[::9].copy(), b, free=free)
+        _union_fused_case(lc, np.array([3], np.uint64), b, free=free)
+
+
+def test_union_fused_u32_and_configs(lc):
+    """Fused path on u32 keys (config 1) and on a config-5-like long list with several residual
+    widths (b = 0, 5, 8, 13)."""
+    rng = np.random.default_rng(12)
+    b = make_keys(1, 1_000_000)
+    a = np.unique(rng.integers(0, int(b[-1]) + 100, 60_000).astype(np.uint32))
+    _union_fused_case(lc, a, b, 63, 63)
+    b = make_keys(5, 400_000)
+    a = np.unique(np.concatenate([b[rng.integers(0, b.size, 20_000)],
+                                  rng.integers(0, int(b[-1]), 20_000).astype(np.uint64)]))
+    for eps in (0, 17, 127, 4095):
+        _union_fused_case(lc, a, b, 7, eps)
+
+
 def test_max_size_u32(lc):
     """Maximum list size of the format (N = 2^32 - 1, FORMAT F1): u32 keys 0..N-1 at eps = 1,
     so residual bit offsets reach 8.6e9 (> 2^32) and key indices the top of the 32-bit range.

@@ -53,6 +53,16 @@ def main():
     out, cnt = lc.intersect(va, v5)
     ms = t(lambda: lc.intersect(va, v5, out=out, count=cnt))
     print(f"intersect {ms:.4f} ms count {int(cnt.item())}")
+    uo, uc = lc.union(va, v5)
+    want_u = np.union1d(a, k5)
+    assert int(uc.item()) == want_u.size, "union count mismatch"
+    assert np.array_equal(uo[:want_u.size].cpu().numpy().view(np.uint64), want_u), "union mismatch"
+    scr = torch.empty(lc.union_scratch_bytes(va, v5), dtype=torch.uint8, device="cuda")
+    ms = t(lambda: lc.union(va, v5, scr, uo, uc))
+    print(f"union {ms:.4f} ms keys_out {int(uc.item())}")
+    dec = torch.empty(k5.size, dtype=torch.int64, device="cuda")
+    ms = t(lambda: lc.decode(v5, dec))
+    print(f"decode (long list alone) {ms:.4f} ms")
 
 
 if __name__ == "__main__":
