@@ -100,6 +100,17 @@ def main():
     out, cnt = lc.intersect(va, vf)
     c = int(cnt.item())
     check("intersect-free", np.array_equal(h(out[:c], np.uint64), setops.intersect(a, k5)))
+    out, cnt = lc.union(va, vf)
+    c = int(cnt.item())
+    check("union-free", np.array_equal(h(out[:c], np.uint64), setops.union(a, k5)))
+    # fused union with > 32 insertions per window (streamed batches) and equal ranks
+    lo = int(k5[7 * 1024])
+    cl = np.unique(np.concatenate([rng.integers(lo, lo + 40_000, 3000).astype(np.uint64),
+                                   k5[-1] + np.arange(1, 40, dtype=np.uint64)]))
+    vc = lc.View(lc.encode(cl, 7), device=dev)
+    out, cnt = lc.union(vc, vb)
+    c = int(cnt.item())
+    check("union-clustered", np.array_equal(h(out[:c], np.uint64), setops.union(cl, k5)))
     print(f"bounds check ok: {checks} checks, 0 violations")
 
 
