@@ -138,11 +138,17 @@ __device__ __forceinline__ uint32_t pred_plus(uint64_t slope, uint32_t d, uint32
 }
 
 // ------------------------------------------------------------ shared per-key helpers
+// Residual of lane's key in staged window w (lw, ls: the lane's word and bit offset in a
+// window).  Widths dividing 32 never straddle a word: one load, and for b = 8 / 16 one byte
+// permute (PRMT) instead of shift + mask.
 template <uint32_t B>
 __device__ __forceinline__ uint32_t field(const uint32_t* sW, uint32_t w, uint32_t lw, uint32_t ls) {
     if (!B) return 0;
     constexpr uint32_t mask = B >= 32 ? 0xffffffffu : ((1u << (B & 31)) - 1);
     const uint32_t* wp = sW + w * B + lw;
+    if (B == 8) return __byte_perm(wp[0], 0, 0x4440 | (ls >> 3));
+    if (B == 16) return __byte_perm(wp[0], 0, 0x4400 | (((ls >> 3) + 1) << 4) | (ls >> 3));
+    if (32 % (B ? B : 1) == 0) return (wp[0] >> ls) & mask;
     return __funnelshift_r(wp[0], wp[1], ls) & mask;
 }
 
