@@ -286,7 +286,7 @@ int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t*
     a.b = v->h.res_bits;
     a.bias = bias_of(v);
     a.mask = mask_of(a.b);
-    const uint64_t grid = (m + 255) / 256;
+    const uint64_t grid = (m + 256 * kSuccQ - 1) / (256 * kSuccQ);
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (unsigned)grid;
@@ -334,11 +334,11 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     int32_t rc = launch_decode(a, 0, na, sc, st);
     if (rc) return rc;
     if (is_free(b)) {
-        if (kw == 8) lc_isect_flag_kernel<true, true><<<g.nblk, 256, 0, st>>>(g);
-        else lc_isect_flag_kernel<false, true><<<g.nblk, 256, 0, st>>>(g);
+        if (kw == 8) lc_isect_flag_kernel<true, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
+        else lc_isect_flag_kernel<false, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
     } else {
-        if (kw == 8) lc_isect_flag_kernel<true, false><<<g.nblk, 256, 0, st>>>(g);
-        else lc_isect_flag_kernel<false, false><<<g.nblk, 256, 0, st>>>(g);
+        if (kw == 8) lc_isect_flag_kernel<true, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
+        else lc_isect_flag_kernel<false, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
     }
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (kw == 8) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
@@ -395,11 +395,11 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     int32_t rc = launch_decode(sh, 0, ns, sS, st);
     if (rc) return rc;
     if (is_free(lg)) {
-        if (k64) lc_union_rank_kernel<true, true><<<g.nblk, 256, 0, st>>>(g, rank);
-        else lc_union_rank_kernel<false, true><<<g.nblk, 256, 0, st>>>(g, rank);
+        if (k64) lc_union_rank_kernel<true, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
+        else lc_union_rank_kernel<false, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
     } else {
-        if (k64) lc_union_rank_kernel<true, false><<<g.nblk, 256, 0, st>>>(g, rank);
-        else lc_union_rank_kernel<false, false><<<g.nblk, 256, 0, st>>>(g, rank);
+        if (k64) lc_union_rank_kernel<true, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
+        else lc_union_rank_kernel<false, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
     }
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (k64) lc_union_place_kernel<true><<<g.nblk, 256, 0, st>>>(g, rank, rho);

@@ -32,55 +32,124 @@ __device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, u
     return base + (b ? field_of(field_words(sec, s, b, once), s, b, mask) : 0);
 }
 
-// Key-space search over the segments' first keys (strictly increasing in both formats), then
-// a binary search inside the one segment.
-// For F7 blobs K[s_j] lies in [base_j, base_j + 2 eps] (the residual u <= 2 eps, bias 0), so
-// a search step decodes the first key only when x falls inside that band (band = 2 eps).
-template <bool FREE>
-__device__ SuccResult next_geq_one(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
-                                   uint32_t mask, uint32_t bias, uint64_t band, uint64_t x,
-                                   uint64_t keep, uint64_t once) {
+// next_geq(x) for Q independent probes per thread: a key-space binary search over the
+// segments' first keys (strictly increasing in both formats), then a binary search inside the
+// one segment.  For F7 blobs K[s_j] lies in [base_j, base_j + 2 eps] (the residual u <= 2 eps,
+// bias 0), so a search step decodes the first key only when x falls inside that band
+// (band = 2 eps).  Level-synchronous: each level issues the Q probes' loads before consuming
+// any of them, so a thread keeps Q dependent chains in flight (the sorted probe batches of
+// intersect / union are bound by chain latency x waves).  Probes with live[q] false are skipped.
+template <bool FREE, int Q>
+__device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
+                                           uint32_t mask, uint32_t bias, uint64_t band,
+                                           const uint64_t (&x)[Q], const bool (&live)[Q],
+                                           SuccResult (&res)[Q], uint64_t keep, uint64_t once) {
     const uint64_t k0 = seg_first<FREE>(sec, 0, b, mask, keep, once);
-    if (x <= k0) return {0u, k0};
-    uint32_t lo = 0, hi = L - 1;  // max{j : K[s_j] <= x}
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        bool le;
-        if (FREE) {
-            const uint64_t base = __ldg((const uint64_t*)sec.params + 2 * (size_t)mid);
-            if (base > x) le = false;
-            else if (x - base >= band) le = true;
-            else le = seg_first<FREE>(sec, mid, b, mask, keep, once) <= x;
-        } else {
-            le = seg_first<FREE>(sec, mid, b, mask, keep, once) <= x;
+    bool go[Q];
+    uint32_t lo[Q], hi[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        go[q] = live[q] && x[q] > k0;
+        lo[q] = 0;
+        hi[q] = go[q] ? L - 1 : 0;
+    }
+    // 1. j = max{t : K[s_t] <= x} over the segments' first keys
+    for (;;) {
+        bool act[Q], any = false;
+        uint32_t mid[Q];
+        uint64_t v[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            act[q] = lo[q] < hi[q];
+            any |= act[q];
+            mid[q] = (lo[q] + hi[q] + 1) >> 1;
+            v[q] = act[q] ? __ldg((const uint64_t*)sec.params + 2 * (size_t)mid[q]) : 0;
         }
-        if (le) lo = mid;
-        else hi = mid - 1;
-    }
-    const uint32_t j = lo;
-    const uint32_t s = ldh(sec.starts + j, keep), e = ldh(sec.starts + j + 1, keep);
-    const ulonglong2 pr = ldh(sec.params + j, once);
-    uint32_t l = s + 1, r = e;  // K[s] <= x; answer in (s, e]
-    if ((FREE ? key_at(sec, s, s, pr, b, mask, bias, once) : pr.x) == x) return {s, x};
-    uint64_t kr = 0;
-    bool have = false;
-    while (l < r) {
-        const uint32_t mid = (l + r) >> 1;
-        const uint64_t km = key_at(sec, mid, s, pr, b, mask, bias, once);
-        if (km >= x) {
-            r = mid;
-            kr = km;
-            have = true;
-        } else {
-            l = mid + 1;
+        if (!any) break;
+        if (FREE) {  // first key = base + u(s) only matters when x lies in [base, base + 2 eps)
+            bool nd[Q];
+            uint32_t sm[Q];
+            uint2 w[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                nd[q] = act[q] && v[q] <= x[q] && x[q] - v[q] < band;
+                sm[q] = nd[q] ? ldh(sec.starts + mid[q], keep) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) w[q] = nd[q] && b ? field_words(sec, sm[q], b, once) : make_uint2(0, 0);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (nd[q]) v[q] += b ? field_of(w[q], sm[q], b, mask) : 0;
         }
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (act[q]) {
+                if (v[q] <= x[q]) lo[q] = mid[q];
+                else hi[q] = mid[q] - 1;
+            }
     }
-    if (l < e) {
-        if (!have || r != l) kr = key_at(sec, l, s, pr, b, mask, bias, once);
-        return {l, kr};
+    // 2. inside segment j: first index in (s_j, s_{j+1}] with K >= x (K[s_j] <= x)
+    uint32_t s[Q], e[Q], l[Q], r[Q];
+    ulonglong2 pr[Q];
+    uint64_t ks[Q], kr[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        s[q] = go[q] ? ldh(sec.starts + lo[q], keep) : 0;
+        e[q] = go[q] ? ldh(sec.starts + lo[q] + 1, keep) : 0;
+        pr[q] = go[q] ? ldh(sec.params + lo[q], once) : make_ulonglong2(0, 0);
     }
-    if (e >= n) return {n, 0};
-    return {e, seg_first<FREE>(sec, j + 1, b, mask, keep, once)};  // K[e] = K[s_{j+1}] > x
+    if (FREE) {
+        uint2 w[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) w[q] = go[q] && b ? field_words(sec, s[q], b, once) : make_uint2(0, 0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            ks[q] = pr[q].x + pred_plus(pr[q].y, 0, (b ? field_of(w[q], s[q], b, mask) : 0) - bias);
+    } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) ks[q] = pr[q].x;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        l[q] = s[q] + 1;
+        r[q] = go[q] && ks[q] != x[q] ? e[q] : l[q];  // no search when K[s_j] == x
+        kr[q] = 0;
+    }
+    for (;;) {
+        bool act[Q], any = false;
+        uint32_t mid[Q];
+        uint2 w[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            act[q] = l[q] < r[q];
+            any |= act[q];
+            mid[q] = (l[q] + r[q]) >> 1;
+            w[q] = act[q] && b ? field_words(sec, mid[q], b, once) : make_uint2(0, 0);
+        }
+        if (!any) break;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (act[q]) {
+                const uint32_t u = b ? field_of(w[q], mid[q], b, mask) : 0;
+                const uint64_t km = pr[q].x + pred_plus(pr[q].y, mid[q] - s[q], u - bias);
+                if (km >= x[q]) {
+                    r[q] = mid[q];
+                    kr[q] = km;  // = K[r]: at the end l == r, so K[l] when l < e
+                } else {
+                    l[q] = mid[q] + 1;
+                }
+            }
+    }
+    // 3. results; x in the gap after segment j's last key: K[e] = first key of segment j + 1
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (!live[q]) continue;
+        if (!go[q]) res[q] = {0u, k0};
+        else if (ks[q] == x[q]) res[q] = {s[q], x[q]};
+        else if (l[q] < e[q]) res[q] = {l[q], kr[q]};
+        else if (e[q] >= n) res[q] = {n, 0};
+        else res[q] = {e[q], seg_first<FREE>(sec, lo[q] + 1, b, mask, keep, once)};
+    }
 }
 
 struct SuccArgs {
@@ -93,17 +162,43 @@ struct SuccArgs {
     uint32_t n, L, b, bias, mask;
 };
 
+// Probes per thread.  A/B on B200 (config 5, tools/prof_setops.py; Q = 1 / 2 / 4):
+// next_geq 1e7 random probes 0.974 / 1.05 / 1.16 ms, intersect 1e6 x 1e8 0.106 / 0.105 /
+// 0.119 ms, union 0.367 / 0.366 / 0.382 ms.  More chains per thread do not help: both run at
+// ~2.7e11 probe loads/s whatever Q (a cache request-rate limit, not chain latency), and
+// Q = 4 needs 80 registers.  Compile-time knobs for such A/B builds.
+#ifndef LC_NEXT_GEQ_Q
+#define LC_NEXT_GEQ_Q 1
+#endif
+#ifndef LC_ISECT_Q
+#define LC_ISECT_Q 1
+#endif
+constexpr int kSuccQ = LC_NEXT_GEQ_Q;   // lc_next_geq (random probes)
+constexpr int kIsectQ = LC_ISECT_Q;     // intersect / union ranks (sorted probes)
+
+// CTA c, thread t handles probes c * 256 Q + 256 q + t (q < Q): coalesced per q
 template <bool K64, bool FREE>
 __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
-    const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-    if (t >= a.m) return;
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    const uint64_t x = __ldg(a.x + t);
-    SuccResult r;
-    if (!K64 && x > 0xffffffffull) r = {a.n, 0};
-    else r = next_geq_one<FREE>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, keep, once);
-    if (a.out_idx) a.out_idx[t] = r.idx;
-    if (a.out_key) put<K64>((uint8_t*)a.out_key + t * (K64 ? 8 : 4), r.key, 0);
+    const uint64_t t0 = (uint64_t)blockIdx.x * 256 * kSuccQ + threadIdx.x;
+    uint64_t x[kSuccQ];
+    bool live[kSuccQ];
+    SuccResult r[kSuccQ];
+#pragma unroll
+    for (int q = 0; q < kSuccQ; ++q) {
+        const uint64_t t = t0 + 256 * q;
+        x[q] = t < a.m ? __ldg(a.x + t) : 0;
+        live[q] = t < a.m && (K64 || x[q] <= 0xffffffffull);
+        r[q] = {a.n, 0};
+    }
+    next_geq_q<FREE, kSuccQ>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, live, r, keep, once);
+#pragma unroll
+    for (int q = 0; q < kSuccQ; ++q) {
+        const uint64_t t = t0 + 256 * q;
+        if (t >= a.m) continue;
+        if (a.out_idx) a.out_idx[t] = r[q].idx;
+        if (a.out_key) put<K64>((uint8_t*)a.out_key + t * (K64 ? 8 : 4), r[q].key, 0);
+    }
 }
 
 // Intersection A ∩ B (AND query): A is decoded into scratch, each key of A is looked up in B
@@ -120,30 +215,52 @@ struct IsectArgs {
     uint32_t na, nb, Lb, b, bias, mask, nblk;
 };
 
-template <bool K64, bool FREE>
-__global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
-    __shared__ uint32_t warp_cnt[8];
-    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+// Probe flags of the searched list a against list b, Q probes per thread: CTA c covers the
+// 256-probe groups c Q .. c Q + Q - 1 (thread t: probe 256 (c Q + q) + t), so flags words and
+// per-group counts keep the layout the scan / write kernels expect (one count per 256 probes).
+// HIT = true: flag keys found in b (intersect); false: flag keys absent from b and store
+// rank[t] = their next_geq index (union).
+template <bool K64, bool FREE, bool HIT>
+__device__ __forceinline__ void flag_probes(const IsectArgs& a, uint32_t* rank) {
+    __shared__ uint32_t warp_cnt[kIsectQ][8];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    bool hit = false;
-    if (t < a.na) {
-        const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
-        const SuccResult r =
-            next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, keep, once);
-        hit = r.idx < a.nb && r.key == x;
+    uint64_t x[kIsectQ];
+    bool live[kIsectQ];
+    SuccResult r[kIsectQ];
+#pragma unroll
+    for (int q = 0; q < kIsectQ; ++q) {
+        const uint32_t t = (blockIdx.x * kIsectQ + q) * 256 + threadIdx.x;
+        live[q] = t < a.na;
+        x[q] = live[q] ? (K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t]) : 0;
+        r[q] = {a.nb, 0};
     }
-    const uint32_t bal = __ballot_sync(kFull, hit);
-    if (lane == 0) {
-        if (t < a.na) a.flags[t >> 5] = bal;
-        warp_cnt[warp] = __popc(bal);
+    next_geq_q<FREE, kIsectQ>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, live, r, keep,
+                              once);
+#pragma unroll
+    for (int q = 0; q < kIsectQ; ++q) {
+        const uint32_t g = blockIdx.x * kIsectQ + q, t = g * 256 + threadIdx.x;
+        const bool found = live[q] && r[q].idx < a.nb && r[q].key == x[q];
+        const bool flag = HIT ? found : live[q] && !found;
+        if (!HIT && live[q]) rank[t] = r[q].idx;
+        const uint32_t bal = __ballot_sync(kFull, flag);
+        if (lane == 0) {
+            if (t < a.na) a.flags[t >> 5] = bal;
+            warp_cnt[q][warp] = __popc(bal);
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < kIsectQ) {
+        const uint32_t g = blockIdx.x * kIsectQ + threadIdx.x;
         uint32_t c = 0;
-        for (int w = 0; w < 8; ++w) c += warp_cnt[w];
-        a.counts[blockIdx.x] = c;
+        for (int w = 0; w < 8; ++w) c += warp_cnt[threadIdx.x][w];
+        if (g < a.nblk) a.counts[g] = c;
     }
+}
+
+template <bool K64, bool FREE>
+__global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
+    flag_probes<K64, FREE, true>(a, nullptr);
 }
 
 // exclusive scan of the per-CTA counts in one CTA of 1024 threads; counts[nblk] = total
@@ -216,29 +333,7 @@ __global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) 
 // i + #{m : rho_m <= i} (lc_decode_kernel<..., UNI>, Ins).
 template <bool K64, bool FREE>
 __global__ void __launch_bounds__(256) lc_union_rank_kernel(const IsectArgs a, uint32_t* rank) {
-    __shared__ uint32_t warp_cnt[8];
-    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    bool absent = false;
-    if (t < a.na) {
-        const uint64_t x = K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t];
-        const SuccResult r =
-            next_geq_one<FREE>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, keep, once);
-        absent = !(r.idx < a.nb && r.key == x);
-        rank[t] = r.idx;
-    }
-    const uint32_t bal = __ballot_sync(kFull, absent);
-    if (lane == 0) {
-        if (t < a.na) a.flags[t >> 5] = bal;
-        warp_cnt[warp] = __popc(bal);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t c = 0;
-        for (int w = 0; w < 8; ++w) c += warp_cnt[w];
-        a.counts[blockIdx.x] = c;
-    }
+    flag_probes<K64, FREE, false>(a, rank);
 }
 
 // absent key t of s -> C position m (flags + scanned counts, as lc_isect_write_kernel):
