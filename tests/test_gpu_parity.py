@@ -394,6 +394,33 @@ def test_full_config5_quantile_next_geq(lc):
     assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, np.uint64), wk)
 
 
+def test_full_config5_intersect_union(lc):
+    """NEXT-2 at the bench's size: a 1e6-key list (half drawn from config 5's keys, half
+    uniform in its key range) intersected with and united with the full 1e8-key config-5 list,
+    anchored (F4) and free-intercept (F7) long lists, every output key checked against the
+    oracle's set definitions."""
+    k5 = make_keys(5)
+    rng = np.random.default_rng(55)
+    na = 1_000_000
+    a = np.unique(np.concatenate([k5[np.sort(rng.choice(k5.size, na // 2, replace=False))],
+                                  rng.integers(0, int(k5[-1]), na // 2, dtype=np.uint64)]))
+    va = lc.View(lc.encode(a, 127), device=DEV)
+    want_i = setops.intersect(a, k5)
+    want_u = setops.union(a, k5)
+    for free in (False, True):
+        vb = lc.View(lc.encode(k5, 127, free=free), device=DEV)
+        out, cnt = lc.intersect(va, vb)
+        torch.cuda.synchronize()
+        c = int(cnt.item())
+        assert c == want_i.size and np.array_equal(_host(out[:c], np.uint64), want_i)
+        for x, y in ((va, vb), (vb, va)):
+            out, cnt = lc.union(x, y)
+            torch.cuda.synchronize()
+            c = int(cnt.item())
+            assert c == want_u.size and np.array_equal(_host(out[:c], np.uint64), want_u)
+        del vb, out
+
+
 def _union_case(lc, a, b, eps_a, eps_b):
     va = lc.View(lc.encode(a, eps_a), device=DEV)
     vb = lc.View(lc.encode(b, eps_b), device=DEV)
