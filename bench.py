@@ -436,6 +436,27 @@ def run_gpu(args):
                                                          stream=stream), stream, reps, 2)
             _, pun = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt,
                                                      stream=stream), stream, reps, 2)
+        # the same three with the successor-search index attached to the long list
+        # (lc_search_index_build: a one-off device pass, timed separately)
+        idx_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        v5.build_search_index(stream=stream)  # warm-up (module load), then timed
+        with torch.cuda.stream(stream):
+            idx_ev[0].record(stream)
+            v5.build_search_index(stream=stream)
+            idx_ev[1].record(stream)
+        torch.cuda.synchronize()
+        idx_build_ms = idx_ev[0].elapsed_time(idx_ev[1])
+        p_idx2 = torch.empty_like(p_idx)
+        p_key2 = torch.empty_like(p_key)
+        with torch.cuda.stream(stream):
+            _, pngx = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx2, p_key2,
+                                                         stream=stream), stream, reps, 2)
+            _, pisx = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt,
+                                                          stream=stream), stream, reps, 2)
+            _, punx = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt,
+                                                      stream=stream), stream, reps, 2)
+        if not (torch.equal(p_idx2, p_idx) and torch.equal(p_key2, p_key)):
+            raise SystemExit("indexed next_geq mismatch")
         want_cnt = int(np.intersect1d(a_keys, k5, assume_unique=True).size)
         if int(i_cnt.item()) != want_cnt:
             raise SystemExit("intersection count mismatch")
@@ -457,6 +478,10 @@ def run_gpu(args):
                           "a_keys_per_s": a_keys.size / statistics.mean(pis)},
             "union": {"keys_out": int(u_cnt.item()), "ms": statistics.mean(pun) * 1e3,
                       "out_keys_per_s": int(u_cnt.item()) / statistics.mean(pun)},
+            "search_index": {"bytes": int(v5.d_first.numel() * 8), "build_ms": idx_build_ms,
+                             "next_geq_per_s": mq / statistics.mean(pngx),
+                             "intersect_ms": statistics.mean(pisx) * 1e3,
+                             "union_ms": statistics.mean(punx) * 1e3},
             "lookups_per_s": ws * idx.size / statistics.mean(pa),
             "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
             "ranges_per_s": ws * rs.size / statistics.mean(pr),
@@ -468,6 +493,7 @@ def run_gpu(args):
         if not (ok_a and ok_r):
             raise SystemExit("access/range mismatch")
         del v5, d_idx, a_out, d_rs, r_out, va, i_scr, i_out, d_ranks, q_out, d_probe, p_idx, p_key
+        del p_idx2, p_key2
         del u_scr, u_out
 
     if ws > 1:

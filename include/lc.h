@@ -63,6 +63,10 @@ typedef struct lc_header {
 typedef struct lc_view {
     lc_header h;
     const void* d_blob;
+    /* Optional successor-search index (lc_search_index_build): d_first[j] = K[s_j], the first
+     * key of segment j, as uint64, in caller-owned device memory.  NULL (lc_view_init's
+     * default): lc_next_geq / lc_intersect / lc_union search the params section directly. */
+    const uint64_t* d_first;
 } lc_view;
 
 /* A CUDA stream (binary-compatible with cudaStream_t / CUstream). */
@@ -144,6 +148,21 @@ int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t 
  * base_j = K[s_j] (FORMAT F2): binary search over the segment bases, then inside one segment. */
 int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,
                     void* d_out_key, lc_stream stream);
+
+/* Device bytes of v's successor-search index: the n_seg first keys (uint64, padded to a 256-byte
+ * multiple) followed by a sample of every 16th of them: about 8.5 bytes per segment. */
+uint64_t lc_search_index_bytes(const lc_view* v);
+
+/* Build v's successor-search index into d_index (>= lc_search_index_bytes(v) bytes, 128-byte
+ * aligned, caller-owned, kept alive while v is used) asynchronously on `stream`, and attach it
+ * (v->d_first = d_index).  The index is the auxiliary segment-localisation structure of
+ * PAPER.md:286 (§III-B) for key-space search (Fig. 4b): the segments' first
+ * keys in one dense array plus a sample of every 16th (one per 128-byte line), so a successor
+ * search binary-searches the small sample (kept in L2 with evict_last) and then one line of
+ * the first keys, instead of ~23 levels of 16-byte params records; F7 blobs no longer decode
+ * K[s_j] during the search.  Results of lc_next_geq / lc_intersect / lc_union are identical
+ * with and without it.  Errors: LC_ERR_ARG (null or misaligned d_index). */
+int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream);
 
 /* Device scratch bytes lc_intersect needs for list a (its decoded keys, a match bitmap and
  * per-CTA offsets). */

@@ -14,6 +14,7 @@ struct Sections {
     const ulonglong2* params;  // {base, slope_fx}
     const uint32_t* hint;
     const uint32_t* words;
+    const uint64_t* first;  // optional successor-search index (lc_view.d_first), may be null
     uint32_t L, W;  // segments, residual words (bounds of params / words)
 };
 
@@ -24,6 +25,7 @@ Sections sections_of(const lc_view* v) {
     s.params = (const ulonglong2*)(B + v->h.off_params);
     s.hint = (const uint32_t*)(B + v->h.off_hint);
     s.words = (const uint32_t*)(B + v->h.off_words);
+    s.first = v->d_first;
     s.L = (uint32_t)v->h.n_seg;
     s.W = (uint32_t)v->h.n_words;
     return s;
@@ -99,6 +101,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 __device__ __forceinline__ uint32_t ldh(const uint32_t* p, uint64_t pol) {
     uint32_t v;
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t ldh(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ ulonglong2 ldh(const ulonglong2* p, uint64_t pol) {

@@ -649,6 +649,7 @@ int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
     if (st) return st;
     v->h = h;
     v->d_blob = d_blob;
+    v->d_first = nullptr;
     return LC_OK;
 }
 

@@ -195,6 +195,20 @@ int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64
 }
 
 uint64_t r256(uint64_t x) { return (x + 255) & ~255ULL; }
+
+// f(K64, FREE, IDX) with the three flags as compile-time constants (std::bool_constant)
+template <typename F>
+void dispatch3(bool k64, bool free, bool idx, F&& f) {
+    using T = std::true_type;
+    using N = std::false_type;
+    if (k64) {
+        if (free) idx ? f(T{}, T{}, T{}) : f(T{}, T{}, N{});
+        else idx ? f(T{}, N{}, T{}) : f(T{}, N{}, N{});
+    } else {
+        if (free) idx ? f(N{}, T{}, T{}) : f(N{}, T{}, N{});
+        else idx ? f(N{}, N{}, T{}) : f(N{}, N{}, N{});
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -290,15 +304,32 @@ int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t*
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (unsigned)grid;
-    if (is_free(v)) {
-        if (v->h.key_bits == 64) lc_next_geq_kernel<true, true><<<g, 256, 0, st>>>(a);
-        else lc_next_geq_kernel<false, true><<<g, 256, 0, st>>>(a);
-    } else {
-        if (v->h.key_bits == 64) lc_next_geq_kernel<true, false><<<g, 256, 0, st>>>(a);
-        else lc_next_geq_kernel<false, false><<<g, 256, 0, st>>>(a);
-    }
+    dispatch3(v->h.key_bits == 64, is_free(v), v->d_first != nullptr, [&](auto K, auto F, auto I) {
+        lc_next_geq_kernel<decltype(K)::value, decltype(F)::value, decltype(I)::value>
+            <<<g, 256, 0, st>>>(a);
+    });
     lc_detail::count_launch(1);
     return cuda_status();
+}
+
+uint64_t lc_search_index_bytes(const lc_view* v) {
+    if (!v) return 0;
+    const uint64_t L = v->h.n_seg;
+    return 8 * (idx_sample_off(L) + (L + kIdxStride - 1) / kIdxStride);
+}
+
+int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream) {
+    if (!v || !v->d_blob || !d_index || ((uintptr_t)d_index & 127)) return LC_ERR_ARG;
+    const Sections sec = sections_of(v);
+    const uint32_t b = v->h.res_bits;
+    const unsigned grid = (unsigned)((v->h.n_seg + 255) / 256);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (is_free(v)) lc_first_kernel<true><<<grid, 256, 0, st>>>(sec, (uint64_t*)d_index, b, mask_of(b), bias_of(v));
+    else lc_first_kernel<false><<<grid, 256, 0, st>>>(sec, (uint64_t*)d_index, b, mask_of(b), bias_of(v));
+    lc_detail::count_launch(1);
+    const int32_t rc = cuda_status();
+    if (!rc) v->d_first = (const uint64_t*)d_index;
+    return rc;
 }
 
 uint64_t lc_intersect_scratch_bytes(const lc_view* a) {
@@ -333,13 +364,11 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     cudaStream_t st = (cudaStream_t)stream;
     int32_t rc = launch_decode(a, 0, na, sc, st);
     if (rc) return rc;
-    if (is_free(b)) {
-        if (kw == 8) lc_isect_flag_kernel<true, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
-        else lc_isect_flag_kernel<false, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
-    } else {
-        if (kw == 8) lc_isect_flag_kernel<true, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
-        else lc_isect_flag_kernel<false, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g);
-    }
+    const unsigned fgrid = (g.nblk + kIsectQ - 1) / kIsectQ;
+    dispatch3(kw == 8, is_free(b), b->d_first != nullptr, [&](auto K, auto F, auto I) {
+        lc_isect_flag_kernel<decltype(K)::value, decltype(F)::value, decltype(I)::value>
+            <<<fgrid, 256, 0, st>>>(g);
+    });
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (kw == 8) lc_isect_write_kernel<true><<<g.nblk, 256, 0, st>>>(g);
     else lc_isect_write_kernel<false><<<g.nblk, 256, 0, st>>>(g);
@@ -394,13 +423,11 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     g.nblk = (uint32_t)nblk;
     int32_t rc = launch_decode(sh, 0, ns, sS, st);
     if (rc) return rc;
-    if (is_free(lg)) {
-        if (k64) lc_union_rank_kernel<true, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
-        else lc_union_rank_kernel<false, true><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
-    } else {
-        if (k64) lc_union_rank_kernel<true, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
-        else lc_union_rank_kernel<false, false><<<(g.nblk + kIsectQ - 1) / kIsectQ, 256, 0, st>>>(g, rank);
-    }
+    const unsigned fgrid = (g.nblk + kIsectQ - 1) / kIsectQ;
+    dispatch3(k64, is_free(lg), lg->d_first != nullptr, [&](auto K, auto F, auto I) {
+        lc_union_rank_kernel<decltype(K)::value, decltype(F)::value, decltype(I)::value>
+            <<<fgrid, 256, 0, st>>>(g, rank);
+    });
     lc_isect_scan_kernel<<<1, 1024, 0, st>>>(g);
     if (k64) lc_union_place_kernel<true><<<g.nblk, 256, 0, st>>>(g, rank, rho);
     else lc_union_place_kernel<false><<<g.nblk, 256, 0, st>>>(g, rank, rho);

@@ -4,6 +4,11 @@
 #pragma once
 
 // ------------------------------------------------------ successor search and intersection
+// successor-search index layout (lc_search_index_build): L first keys, padded to a 256-byte
+// multiple, then ceil(L / 16) sampled first keys (one per 128-byte line of the first array)
+constexpr uint32_t kIdxStride = 16;
+__host__ __device__ constexpr uint64_t idx_sample_off(uint64_t L) { return (L + 31) & ~31ull; }
+
 // Key-space search uses the segments as skip pointers (Fig. 4b): segment j
 // covers exactly the keys [K[s_j], K[s_{j+1}]).  With the FORMAT F2 anchor K[s_j] = base_j (one
 // load per search step); F7 blobs decode K[s_j] = base_j + u(s_j).  next_geq(x) = binary search
@@ -23,9 +28,11 @@ struct SuccResult {
 
 // K[s_j]: base_j for anchored blobs (F2); base_j + u(s_j) for F7 blobs (bias 0, the base is
 // the band floor, not a key), one more dependent load (the starts and params loads overlap)
-template <bool FREE>
+// IDX: read it from the successor-search index (lc_search_index_build) instead
+template <bool FREE, bool IDX = false>
 __device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, uint32_t b,
                                               uint32_t mask, uint64_t keep, uint64_t once) {
+    if (IDX) return __ldg(sec.first + LC_BOUND(true, j, sec.L));
     const uint64_t base = __ldg((const uint64_t*)sec.params + 2 * (size_t)j);
     if (!FREE) return base;
     const uint32_t s = ldh(sec.starts + j, keep);
@@ -39,12 +46,12 @@ __device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, u
 // (band = 2 eps).  Level-synchronous: each level issues the Q probes' loads before consuming
 // any of them, so a thread keeps Q dependent chains in flight (the sorted probe batches of
 // intersect / union are bound by chain latency x waves).  Probes with live[q] false are skipped.
-template <bool FREE, int Q>
+template <bool FREE, bool IDX, int Q>
 __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
                                            uint32_t mask, uint32_t bias, uint64_t band,
                                            const uint64_t (&x)[Q], const bool (&live)[Q],
                                            SuccResult (&res)[Q], uint64_t keep, uint64_t once) {
-    const uint64_t k0 = seg_first<FREE>(sec, 0, b, mask, keep, once);
+    const uint64_t k0 = seg_first<FREE, IDX>(sec, 0, b, mask, keep, once);
     bool go[Q];
     uint32_t lo[Q], hi[Q];
 #pragma unroll
@@ -53,7 +60,38 @@ __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint
         lo[q] = 0;
         hi[q] = go[q] ? L - 1 : 0;
     }
-    // 1. j = max{t : K[s_t] <= x} over the segments' first keys
+    // 1. j = max{t : K[s_t] <= x} over the segments' first keys.  With the index: first over
+    // its sample (every 16th first key, L2-resident), then inside one 128-byte line of it
+    if (IDX) {
+        const uint32_t S = (L + kIdxStride - 1) / kIdxStride;
+        const uint64_t* sample = sec.first + idx_sample_off(L);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) hi[q] = go[q] ? S - 1 : 0;
+        for (;;) {
+            bool act[Q], any = false;
+            uint32_t mid[Q];
+            uint64_t v[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                act[q] = lo[q] < hi[q];
+                any |= act[q];
+                mid[q] = (lo[q] + hi[q] + 1) >> 1;
+                v[q] = act[q] ? ldh(sample + LC_BOUND(true, mid[q], S), keep) : 0;
+            }
+            if (!any) break;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (act[q]) {
+                    if (v[q] <= x[q]) lo[q] = mid[q];
+                    else hi[q] = mid[q] - 1;
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            lo[q] *= kIdxStride;
+            hi[q] = go[q] ? min(lo[q] + kIdxStride - 1, L - 1) : lo[q];
+        }
+    }
     for (;;) {
         bool act[Q], any = false;
         uint32_t mid[Q];
@@ -63,10 +101,11 @@ __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint
             act[q] = lo[q] < hi[q];
             any |= act[q];
             mid[q] = (lo[q] + hi[q] + 1) >> 1;
-            v[q] = act[q] ? __ldg((const uint64_t*)sec.params + 2 * (size_t)mid[q]) : 0;
+            if (IDX) v[q] = act[q] ? __ldg(sec.first + LC_BOUND(true, mid[q], sec.L)) : 0;
+            else v[q] = act[q] ? __ldg((const uint64_t*)sec.params + 2 * (size_t)mid[q]) : 0;
         }
         if (!any) break;
-        if (FREE) {  // first key = base + u(s) only matters when x lies in [base, base + 2 eps)
+        if (FREE && !IDX) {  // first key = base + u(s) only matters when x lies in [base, base + 2 eps)
             bool nd[Q];
             uint32_t sm[Q];
             uint2 w[Q];
@@ -98,7 +137,10 @@ __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint
         e[q] = go[q] ? ldh(sec.starts + lo[q] + 1, keep) : 0;
         pr[q] = go[q] ? ldh(sec.params + lo[q], once) : make_ulonglong2(0, 0);
     }
-    if (FREE) {
+    if (IDX) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) ks[q] = go[q] ? __ldg(sec.first + lo[q]) : 0;
+    } else if (FREE) {
         uint2 w[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) w[q] = go[q] && b ? field_words(sec, s[q], b, once) : make_uint2(0, 0);
@@ -148,7 +190,7 @@ __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint
         else if (ks[q] == x[q]) res[q] = {s[q], x[q]};
         else if (l[q] < e[q]) res[q] = {l[q], kr[q]};
         else if (e[q] >= n) res[q] = {n, 0};
-        else res[q] = {e[q], seg_first<FREE>(sec, lo[q] + 1, b, mask, keep, once)};
+        else res[q] = {e[q], seg_first<FREE, IDX>(sec, lo[q] + 1, b, mask, keep, once)};
     }
 }
 
@@ -177,7 +219,7 @@ constexpr int kSuccQ = LC_NEXT_GEQ_Q;   // lc_next_geq (random probes)
 constexpr int kIsectQ = LC_ISECT_Q;     // intersect / union ranks (sorted probes)
 
 // CTA c, thread t handles probes c * 256 Q + 256 q + t (q < Q): coalesced per q
-template <bool K64, bool FREE>
+template <bool K64, bool FREE, bool IDX>
 __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
     const uint64_t t0 = (uint64_t)blockIdx.x * 256 * kSuccQ + threadIdx.x;
@@ -191,7 +233,7 @@ __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
         live[q] = t < a.m && (K64 || x[q] <= 0xffffffffull);
         r[q] = {a.n, 0};
     }
-    next_geq_q<FREE, kSuccQ>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, live, r, keep, once);
+    next_geq_q<FREE, IDX, kSuccQ>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, live, r, keep, once);
 #pragma unroll
     for (int q = 0; q < kSuccQ; ++q) {
         const uint64_t t = t0 + 256 * q;
@@ -220,7 +262,7 @@ struct IsectArgs {
 // per-group counts keep the layout the scan / write kernels expect (one count per 256 probes).
 // HIT = true: flag keys found in b (intersect); false: flag keys absent from b and store
 // rank[t] = their next_geq index (union).
-template <bool K64, bool FREE, bool HIT>
+template <bool K64, bool FREE, bool IDX, bool HIT>
 __device__ __forceinline__ void flag_probes(const IsectArgs& a, uint32_t* rank) {
     __shared__ uint32_t warp_cnt[kIsectQ][8];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -235,7 +277,7 @@ __device__ __forceinline__ void flag_probes(const IsectArgs& a, uint32_t* rank) 
         x[q] = live[q] ? (K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t]) : 0;
         r[q] = {a.nb, 0};
     }
-    next_geq_q<FREE, kIsectQ>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, live, r, keep,
+    next_geq_q<FREE, IDX, kIsectQ>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, live, r, keep,
                               once);
 #pragma unroll
     for (int q = 0; q < kIsectQ; ++q) {
@@ -258,9 +300,9 @@ __device__ __forceinline__ void flag_probes(const IsectArgs& a, uint32_t* rank) 
     }
 }
 
-template <bool K64, bool FREE>
+template <bool K64, bool FREE, bool IDX>
 __global__ void __launch_bounds__(256) lc_isect_flag_kernel(const IsectArgs a) {
-    flag_probes<K64, FREE, true>(a, nullptr);
+    flag_probes<K64, FREE, IDX, true>(a, nullptr);
 }
 
 // exclusive scan of the per-CTA counts in one CTA of 1024 threads; counts[nblk] = total
@@ -331,9 +373,27 @@ __global__ void __launch_bounds__(256) lc_isect_write_kernel(const IsectArgs a) 
 // keys absent from l are compacted in order (C, with rho_m = rank) and written straight to
 // their union slot m + rho_m; then l is decoded once with every key i stored at
 // i + #{m : rho_m <= i} (lc_decode_kernel<..., UNI>, Ins).
-template <bool K64, bool FREE>
+template <bool K64, bool FREE, bool IDX>
 __global__ void __launch_bounds__(256) lc_union_rank_kernel(const IsectArgs a, uint32_t* rank) {
-    flag_probes<K64, FREE, false>(a, rank);
+    flag_probes<K64, FREE, IDX, false>(a, rank);
+}
+
+// successor-search index: first[j] = K[s_j] = base_j + u(s_j) - c (FORMAT F3 at d = 0) for
+// j < L, then (from idx_sample_off(L)) the sample first[kIdxStride * k]
+template <bool FREE>
+__global__ void __launch_bounds__(256) lc_first_kernel(const Sections sec, uint64_t* first,
+                                                       uint32_t b, uint32_t mask, uint32_t bias) {
+    const uint32_t j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= sec.L) return;
+    uint64_t k = __ldg((const uint64_t*)sec.params + 2 * (size_t)j);
+    if (FREE) {  // F2 anchor: u(s_j) = eps = c, so K[s_j] = base_j; F7: base_j + u(s_j)
+        const uint32_t s = __ldg(sec.starts + j);
+        const uint64_t pol = policy_evict_first();
+        const uint32_t u = b ? field_of(field_words(sec, s, b, pol), s, b, mask) : 0;
+        k += (uint32_t)(u - bias);
+    }
+    first[j] = k;
+    if (j % kIdxStride == 0) first[idx_sample_off(sec.L) + j / kIdxStride] = k;
 }
 
 // absent key t of s -> C position m (flags + scanned counts, as lc_isect_write_kernel):

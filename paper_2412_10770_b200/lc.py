@@ -41,7 +41,7 @@ assert C.sizeof(lc_header) == 128
 
 
 class lc_view(C.Structure):
-    _fields_ = [("h", lc_header), ("d_blob", C.c_void_p)]
+    _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p)]
 
 
 _p, _u64, _u32, _i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32
@@ -60,6 +60,8 @@ _sig = {
     "lc_intersect_scratch_bytes": ([C.POINTER(lc_view)], _u64),
     "lc_intersect": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_union_scratch_bytes": ([C.POINTER(lc_view), C.POINTER(lc_view)], _u64),
+    "lc_search_index_bytes": ([C.POINTER(lc_view)], _u64),
+    "lc_search_index_build": ([C.POINTER(lc_view), _p, _p], _i32),
     "lc_union": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
@@ -168,6 +170,17 @@ class View:
     def torch_dtype(self):
         import torch
         return torch.int64 if self.key_bits == 64 else torch.int32
+
+    def build_search_index(self, stream=None):
+        """lc_search_index_build: allocate the successor-search index (the segments' first keys
+        plus every 16th of them, about 8.5 bytes per segment) on the blob's device, build it on
+        `stream` and attach it to this view (next_geq / intersect / union then use it)."""
+        import torch
+        nbytes = int(_lib.lc_search_index_bytes(C.byref(self.v)))
+        self.d_first = torch.empty(max(nbytes // 8, 1), dtype=torch.int64, device=self.d_blob.device)
+        _check(_lib.lc_search_index_build(C.byref(self.v), self.d_first.data_ptr(), _stream(stream)),
+               "lc_search_index_build")
+        return self.d_first
 
     def out_tensor(self, count: int):
         import torch

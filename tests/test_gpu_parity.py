@@ -394,10 +394,44 @@ def test_full_config5_quantile_next_geq(lc):
     assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, np.uint64), wk)
 
 
+@pytest.mark.parametrize("free", [False, True])
+@pytest.mark.parametrize("cid,n", [(1, 300_000), (2, 400_003), (3, 500_000), (4, 700_001), (5, 300_000)])
+def test_search_index(lc, cid, n, free):
+    """lc_search_index_build: the index holds each segment's first key K[s_j] (checked against
+    the generator's keys at the blob's segment starts), and next_geq / intersect / union give
+    the same answers with the index attached as the oracle's set definitions."""
+    from tests import blobparse
+    keys = make_keys(cid, n)
+    eps = CONFIGS[cid].eps
+    blob = lc.encode(keys, eps, free=free)
+    view = lc.View(blob, device=DEV)
+    idx = _host(view.build_search_index(), np.uint64)
+    starts = blobparse.parse(blob).starts[:-1].astype(np.int64)
+    L = starts.size
+    assert np.array_equal(idx[:L], keys[starts].astype(np.uint64))
+    off = (L + 31) // 32 * 32  # then the sample: every 16th first key
+    assert np.array_equal(idx[off: off + (L + 15) // 16], keys[starts[::16]].astype(np.uint64))
+    rng = np.random.default_rng(cid)
+    x = _probes(keys, rng, 200_000)
+    gi, gk = lc.next_geq(view, _dev(x))
+    wi, wk = setops.next_geq(keys, x)
+    assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, keys.dtype), wk)
+    a = np.unique(np.concatenate([keys[rng.integers(0, keys.size, n // 20)],
+                                  rng.integers(0, int(keys[-1]) + 10, n // 20).astype(keys.dtype)]))
+    va = lc.View(lc.encode(a, 31), device=DEV)
+    out, cnt = lc.intersect(va, view)
+    uo, uc = lc.union(va, view)
+    torch.cuda.synchronize()
+    wi_, wu_ = setops.intersect(a, keys), setops.union(a, keys)
+    assert int(cnt.item()) == wi_.size and np.array_equal(_host(out[: wi_.size], keys.dtype), wi_)
+    assert int(uc.item()) == wu_.size and np.array_equal(_host(uo[: wu_.size], keys.dtype), wu_)
+
+
 def test_full_config5_intersect_union(lc):
     """NEXT-2 at the bench's size: a 1e6-key list (half drawn from config 5's keys, half
     uniform in its key range) intersected with and united with the full 1e8-key config-5 list,
-    anchored (F4) and free-intercept (F7) long lists, every output key checked against the
+    anchored (F4) and free-intercept (F7) long lists, without and with the successor-search
+    index (plus 1e6 next_geq probes through the index), every output key checked against the
     oracle's set definitions."""
     k5 = make_keys(5)
     rng = np.random.default_rng(55)
@@ -418,6 +452,19 @@ def test_full_config5_intersect_union(lc):
             torch.cuda.synchronize()
             c = int(cnt.item())
             assert c == want_u.size and np.array_equal(_host(out[:c], np.uint64), want_u)
+        vb.build_search_index()  # same answers through the successor-search index
+        out, cnt = lc.intersect(va, vb)
+        torch.cuda.synchronize()
+        c = int(cnt.item())
+        assert c == want_i.size and np.array_equal(_host(out[:c], np.uint64), want_i)
+        out, cnt = lc.union(va, vb)
+        torch.cuda.synchronize()
+        c = int(cnt.item())
+        assert c == want_u.size and np.array_equal(_host(out[:c], np.uint64), want_u)
+        x = _probes(k5, rng, 1_000_000)
+        gi, gk = lc.next_geq(vb, _dev(x))
+        wi, wk = setops.next_geq(k5, x)
+        assert np.array_equal(_host(gi, np.uint64), wi) and np.array_equal(_host(gk, np.uint64), wk)
         del vb, out
 
 

@@ -60,6 +60,29 @@ def main():
     scr = torch.empty(lc.union_scratch_bytes(va, v5), dtype=torch.uint8, device="cuda")
     ms = t(lambda: lc.union(va, v5, scr, uo, uc))
     print(f"union {ms:.4f} ms keys_out {int(uc.item())}")
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_b[0].record()
+    v5.build_search_index()
+    ev_b[1].record()
+    torch.cuda.synchronize()
+    print(f"search index build {ev_b[0].elapsed_time(ev_b[1]):.4f} ms ({v5.d_first.numel() * 8 / 1e6:.1f} MB)")
+    gi2, gk2 = lc.next_geq(v5, d_probe)
+    assert torch.equal(gi2, gi) and torch.equal(gk2, gk), "indexed next_geq mismatch"
+    ms = t(lambda: lc.next_geq(v5, d_probe, gi, gk))
+    print(f"next_geq+index {ms:.3f} ms {probes.size / ms / 1e6:.3e} probes/s")
+    ms = t(lambda: lc.intersect(va, v5, out=out, count=cnt))
+    print(f"intersect+index {ms:.4f} ms count {int(cnt.item())}")
+    ms = t(lambda: lc.union(va, v5, scr, uo, uc))
+    print(f"union+index {ms:.4f} ms keys_out {int(uc.item())}")
+    assert np.array_equal(uo[:want_u.size].cpu().numpy().view(np.uint64), want_u), "union mismatch"
+    v5f = lc.View(lc.encode(k5, 127, free=True))
+    gf, kf = lc.next_geq(v5f, d_probe)
+    ms = t(lambda: lc.next_geq(v5f, d_probe, gf, kf))
+    print(f"F7 next_geq {ms:.3f} ms {probes.size / ms / 1e6:.3e} probes/s")
+    v5f.build_search_index()
+    ms = t(lambda: lc.next_geq(v5f, d_probe, gf, kf))
+    assert torch.equal(gf, gi), "F7 indexed next_geq mismatch"
+    print(f"F7 next_geq+index {ms:.3f} ms {probes.size / ms / 1e6:.3e} probes/s")
     dec = torch.empty(k5.size, dtype=torch.int64, device="cuda")
     ms = t(lambda: lc.decode(v5, dec))
     print(f"decode (long list alone) {ms:.4f} ms")
