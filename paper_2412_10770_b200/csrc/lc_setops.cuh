@@ -6,7 +6,7 @@
 // ------------------------------------------------------ successor search and intersection
 // successor-search index layout (lc_search_index_build): L first keys, padded to a 256-byte
 // multiple, then ceil(L / 16) sampled first keys (one per 128-byte line of the first array)
-constexpr uint32_t kIdxStride = 16;
+constexpr uint32_t kIdxStride = 16;  // A/B: 8 measured 2-4% slower for next_geq
 __host__ __device__ constexpr uint64_t idx_sample_off(uint64_t L) { return (L + 31) & ~31ull; }
 
 // Key-space search uses the segments as skip pointers (Fig. 4b): segment j
@@ -50,7 +50,8 @@ template <bool FREE, bool IDX, int Q>
 __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
                                            uint32_t mask, uint32_t bias, uint64_t band,
                                            const uint64_t (&x)[Q], const bool (&live)[Q],
-                                           SuccResult (&res)[Q], uint64_t keep, uint64_t once) {
+                                           SuccResult (&res)[Q], uint64_t keep, uint64_t once,
+                                           uint64_t spol) {
     const uint64_t k0 = seg_first<FREE, IDX>(sec, 0, b, mask, keep, once);
     bool go[Q];
     uint32_t lo[Q], hi[Q];
@@ -133,8 +134,8 @@ __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint
     uint64_t ks[Q], kr[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        s[q] = go[q] ? ldh(sec.starts + lo[q], keep) : 0;
-        e[q] = go[q] ? ldh(sec.starts + lo[q] + 1, keep) : 0;
+        s[q] = go[q] ? ldh(sec.starts + lo[q], spol) : 0;
+        e[q] = go[q] ? ldh(sec.starts + lo[q] + 1, spol) : 0;
         pr[q] = go[q] ? ldh(sec.params + lo[q], once) : make_ulonglong2(0, 0);
     }
     if (IDX) {
@@ -233,7 +234,8 @@ __global__ void __launch_bounds__(256) lc_next_geq_kernel(const SuccArgs a) {
         live[q] = t < a.m && (K64 || x[q] <= 0xffffffffull);
         r[q] = {a.n, 0};
     }
-    next_geq_q<FREE, IDX, kSuccQ>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, live, r, keep, once);
+    next_geq_q<FREE, IDX, kSuccQ>(a.sec, a.n, a.L, a.b, a.mask, a.bias, a.band, x, live, r, keep, once,
+                                  keep);
 #pragma unroll
     for (int q = 0; q < kSuccQ; ++q) {
         const uint64_t t = t0 + 256 * q;
@@ -277,8 +279,10 @@ __device__ __forceinline__ void flag_probes(const IsectArgs& a, uint32_t* rank) 
         x[q] = live[q] ? (K64 ? ((const uint64_t*)a.a_keys)[t] : ((const uint32_t*)a.a_keys)[t]) : 0;
         r[q] = {a.nb, 0};
     }
+    // sorted probes: with the index, the segment's starts pair is a one-touch gather
+    // (evict_first: intersect 0.097 -> 0.086 ms on config 5; random next_geq prefers evict_last)
     next_geq_q<FREE, IDX, kIsectQ>(a.sb, a.nb, a.Lb, a.b, a.mask, a.bias, a.band, x, live, r, keep,
-                              once);
+                                   once, IDX ? once : keep);
 #pragma unroll
     for (int q = 0; q < kIsectQ; ++q) {
         const uint32_t g = blockIdx.x * kIsectQ + q, t = g * 256 + threadIdx.x;
