@@ -111,6 +111,20 @@ def main():
     out, cnt = lc.union(vc, vb)
     c = int(cnt.item())
     check("union-clustered", np.array_equal(h(out[:c], np.uint64), setops.union(cl, k5)))
+    # the same through the successor-search index (anchored and F7 long lists)
+    for vv, nm in ((vb, "idx"), (vf, "idx-free")):
+        vv.build_search_index()
+        xs = np.concatenate([k5[rng.integers(0, k5.size, 3000)],
+                             rng.integers(0, int(k5[-1]) + 100, 3000, dtype=np.uint64)])
+        gi, gk = lc.next_geq(vv, d(xs))
+        wi, wk = setops.next_geq(k5, xs)
+        check(f"next_geq-{nm}", np.array_equal(h(gi, np.uint64), wi) and np.array_equal(h(gk, np.uint64), wk))
+        out, cnt = lc.intersect(va, vv)
+        c = int(cnt.item())
+        check(f"intersect-{nm}", np.array_equal(h(out[:c], np.uint64), setops.intersect(a, k5)))
+        out, cnt = lc.union(vc, vv)
+        c = int(cnt.item())
+        check(f"union-{nm}", np.array_equal(h(out[:c], np.uint64), setops.union(cl, k5)))
     print(f"bounds check ok: {checks} checks, 0 violations")
 
 
