@@ -439,10 +439,10 @@ def run_gpu(args):
         # the same three with the successor-search index attached to the long list
         # (lc_search_index_build: a one-off device pass, timed separately)
         idx_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        v5.build_search_index(stream=stream)  # warm-up (module load), then timed
+        idx_buf = v5.build_search_index(stream=stream)  # warm-up (module load), then timed
         with torch.cuda.stream(stream):
             idx_ev[0].record(stream)
-            v5.build_search_index(stream=stream)
+            v5.build_search_index(stream=stream, out=idx_buf)
             idx_ev[1].record(stream)
         torch.cuda.synchronize()
         idx_build_ms = idx_ev[0].elapsed_time(idx_ev[1])

@@ -171,13 +171,20 @@ class View:
         import torch
         return torch.int64 if self.key_bits == 64 else torch.int32
 
-    def build_search_index(self, stream=None):
+    def search_index_bytes(self) -> int:
+        return int(_lib.lc_search_index_bytes(C.byref(self.v)))
+
+    def build_search_index(self, stream=None, out=None):
         """lc_search_index_build: allocate the successor-search index (the segments' first keys
         plus every 16th of them, about 8.5 bytes per segment) on the blob's device, build it on
         `stream` and attach it to this view (next_geq / intersect / union then use it)."""
         import torch
-        nbytes = int(_lib.lc_search_index_bytes(C.byref(self.v)))
-        self.d_first = torch.empty(max(nbytes // 8, 1), dtype=torch.int64, device=self.d_blob.device)
+        nbytes = self.search_index_bytes()
+        if out is None:
+            out = torch.empty(max(nbytes // 8, 1), dtype=torch.int64, device=self.d_blob.device)
+        if out.numel() * out.element_size() < nbytes:
+            raise ValueError("search index buffer too small")
+        self.d_first = out
         _check(_lib.lc_search_index_build(C.byref(self.v), self.d_first.data_ptr(), _stream(stream)),
                "lc_search_index_build")
         return self.d_first
