@@ -135,6 +135,27 @@ def test_header_struct_matches_format(lc):
         bl.o_starts, bl.o_params, bl.o_hint, bl.o_words, len(blob))
 
 
+@pytest.mark.parametrize("n", [2, 17, 5000, 70_001])
+def test_view_and_search_index_sizes(lc, n):
+    """lc_view_init leaves the search index detached; lc_search_index_bytes = the L first keys
+    padded to 32 entries plus ceil(L/16) samples (8 bytes each); lc_search_index_build rejects a
+    null or misaligned buffer before touching the device.  No device memory is dereferenced
+    (the view's device pointer is only recorded)."""
+    import ctypes as C
+    keys = make_keys(2, n)
+    blob = lc.encode(keys, 127)
+    L = lc.header(blob).n_seg
+    v = lc.lc_view()
+    host = np.frombuffer(blob, np.uint8)
+    assert lc._lib.lc_view_init(C.byref(v), host.ctypes.data, 1 << 20, host.nbytes) == 0
+    assert v.d_first is None
+    assert lc._lib.lc_search_index_bytes(C.byref(v)) == 8 * ((L + 31) // 32 * 32 + (L + 15) // 16)
+    assert lc._lib.lc_search_index_build(C.byref(v), None, None) == -1
+    assert lc._lib.lc_search_index_build(C.byref(v), 1 << 20 | 8, None) == -1
+    assert v.d_first is None
+    assert lc._lib.lc_view_init(C.byref(v), host.ctypes.data, (1 << 20) + 8, host.nbytes) == -1
+
+
 # ------------------------------------------------------------ FORMAT F7 (NEXT-3, free intercept)
 @pytest.mark.parametrize("seed", range(5000, 5120))
 def test_free_blob_equals_oracle_fuzz(lc, seed):
