@@ -247,7 +247,9 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
 // dense lists keep 5 resident CTAs (<= 48 registers).
 // UNI: lc_union's fused path (stores shifted by Ins; dense settings)
 template <bool K64, uint32_t B, bool SPARSE, bool UNI = false>
-__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 5) lc_decode_kernel(const DecodeArgs a) {
+// UNI: 4 CTAs / 64 registers (the insertion state spilled at 48: A/B union 0.367 -> 0.358 ms)
+__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : (UNI ? 4 : 5))
+    lc_decode_kernel(const DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* base = smem + warp * a.warp_bytes;
