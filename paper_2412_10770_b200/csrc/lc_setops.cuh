@@ -14,12 +14,6 @@ __host__ __device__ constexpr uint64_t idx_sample_off(uint64_t L) { return (L + 
 // load per search step); F7 blobs decode K[s_j] = base_j + u(s_j).  next_geq(x) = binary search
 // over the first keys, then a binary search inside the one segment, decoding only the probed
 // keys (never a whole segment).
-__device__ __forceinline__ uint64_t key_at(const Sections& sec, uint32_t i, uint32_t s,
-                                           ulonglong2 pr, uint32_t b, uint32_t mask, uint32_t bias,
-                                           uint64_t once) {
-    const uint32_t u = b ? field_of(field_words(sec, i, b, once), i, b, mask) : 0;
-    return pr.x + pred_plus(pr.y, i - s, u - bias);
-}
 
 struct SuccResult {
     uint32_t idx;  // first index with K[idx] >= x, n if none
@@ -44,8 +38,8 @@ __device__ __forceinline__ uint64_t seg_first(const Sections& sec, uint32_t j, u
 // one segment.  For F7 blobs K[s_j] lies in [base_j, base_j + 2 eps] (the residual u <= 2 eps,
 // bias 0), so a search step decodes the first key only when x falls inside that band
 // (band = 2 eps).  Level-synchronous: each level issues the Q probes' loads before consuming
-// any of them, so a thread keeps Q dependent chains in flight (the sorted probe batches of
-// intersect / union are bound by chain latency x waves).  Probes with live[q] false are skipped.
+// any of them, so a thread can keep Q dependent chains in flight (Q = 1 by default: the
+// searches are DRAM-gather bound, see kSuccQ).  Probes with live[q] false are skipped.
 template <bool FREE, bool IDX, int Q>
 __device__ __forceinline__ void next_geq_q(const Sections& sec, uint32_t n, uint32_t L, uint32_t b,
                                            uint32_t mask, uint32_t bias, uint64_t band,
