@@ -172,8 +172,9 @@ uint64_t lc_intersect_scratch_bytes(const lc_view* a);
  * (§III-A): d_out receives the sorted keys present in both lists and
  * *d_count (device uint64) their number.  a is decoded into d_scratch (>=
  * lc_intersect_scratch_bytes(a) bytes, 256-byte aligned) and each of its keys is searched in b
- * with next_geq, so segments of b that hold none of a's keys are never read: pass the shorter
- * list as a.  d_out capacity: a->h.n keys.  Both lists must have the same key_bits. */
+ * with next_geq, so segments of b that hold none of a's keys are never read.  When b is the
+ * shorter list the roles are swapped internally (the scratch and d_out sized for a suffice).
+ * d_out capacity: a->h.n keys.  Both lists must have the same key_bits. */
 int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                      void* d_out, uint64_t* d_count, lc_stream stream);
 

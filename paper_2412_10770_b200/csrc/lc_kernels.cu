@@ -344,6 +344,9 @@ int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64
     if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_intersect_scratch_bytes(a) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
+    // symmetric: decode the shorter list and search the longer one (the scratch and output sized
+    // for a also hold the shorter list and the intersection)
+    if (b->h.n < a->h.n) std::swap(a, b);
     const uint64_t na = a->h.n, kw = a->h.key_bits / 8;
     uint8_t* sc = (uint8_t*)d_scratch;
     IsectArgs g;

@@ -350,6 +350,7 @@ def test_intersect_subset_plus_noise(lc, na):
     noise = rng.integers(0, int(b[-1]) + 1000, na, dtype=np.uint64)
     a = np.unique(np.concatenate([pick, noise]))[:na]
     _isect_case(lc, a, b, 63, 127)
+    _isect_case(lc, b, a, 127, 63)  # longer list first: decoded / searched roles swap inside
 
 
 def test_intersect_closed_form_and_edges(lc):
