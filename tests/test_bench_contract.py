@@ -1,0 +1,50 @@
+"""bench.py's JSON-line contract (the driver parses it): the reference arm (the CPU oracle) runs
+here without a GPU; the product arm runs under -m gpu.  Config 1 keeps both runs short."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+             "cpu_baseline"}
+
+
+def _run(*args: str, timeout: int = 900) -> dict:
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                       capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run("--impl", "reference", "--config", "1", "--steps", "2", "--warmup", "3")
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] >= 3
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["unit"] == "GB/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert "workload" in d["config"] and "model" not in d["config"]
+
+
+@pytest.mark.gpu
+def test_product_arm_line():
+    d = _run("--config", "1", "--steps", "5", "--warmup", "3", "--no-access", "--no-cpu",
+             "--no-free")
+    assert BASE_KEYS - {"cpu_baseline"} <= set(d)
+    assert {"roofline", "gpu_launches", "clocks"} <= set(d)
+    assert d["value"] > 0 and d["gpu_launches"] >= d["steps"]
+    rl = d["roofline"]
+    assert rl["bound"] == "hbm" and rl["unit"] == "GB/s" and 0 < rl["frac"] < 1.2
+    assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-6
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 4_000_000
+    assert d["dtype"] == "u32" and d["config"]["n"] == 1_000_000
