@@ -205,7 +205,7 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
 // Four windows at once: keys [wb, wb + 128), lane handles wb + 32 q + lane (q = 0..3).  One
 // candidate load / advance vote serves four quarters when fewer than 32 segment starts fall
 // inside; otherwise two pair steps.  w4 = quad index (windows 4 w4 .. 4 w4 + 3).
-template <bool K64, uint32_t B, bool CHECK, bool UNI>
+template <bool K64, uint32_t B, bool CHECK, bool UNI, bool FAST = false>
 __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w4, uint32_t lane, uint32_t lmask,
@@ -216,7 +216,21 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         stage(pg, sec, jb, jlast, nullptr, 0, lane);
     const uint32_t cand = min(jb + 1 + lane, jlast + 1);
     const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
-    if (__ballot_sync(kFull, x < 128) == kFull) {  // >= 32 boundaries in 128 keys
+    const uint32_t inq = __ballot_sync(kFull, x < 128);
+    if (FAST && inq == 0) {  // sparse lists: no segment starts inside the 128 keys, one segment
+        const ulonglong2 pr = pg.sP[LC_BOUND(true, jb - pg.pj, pg.cp)];
+        const uint32_t d0 = (wb - sb) + lane;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+            LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
+            put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
+                     pred_plus(pr.y, d0 + 32 * q, field<B>(pg.sW, 4 * w4 + q, lw, ls) - bias));
+        }
+        jb = min(jb + __popc(__ballot_sync(kFull, x == 128)), jlast + 1);  // a start at wb + 128
+        sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+        return;
+    }
+    if (inq == kFull) {  // >= 32 boundaries in 128 keys
         decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls,
                                         bias, outw, ins);
         decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask,
@@ -313,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, SPARSE ? 6 : (UNI ? 4 : 5))
             for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
 #pragma unroll
                 for (uint32_t k = 0; k < 2; ++k)
-                    decode_quad<K64, B, false, UNI>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k),
+                    decode_quad<K64, B, false, UNI, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k),
                                                     g + k, lane, lmask, lw, ls, a.bias,
                                                     outl + 128 * kw * k, ins);
                 if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
