@@ -144,8 +144,11 @@ int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t 
 /* Successor search (NEXT-2; segments as skip pointers, Fig. 4b): for t < m,
  * d_out_idx[t] = min{i : K[i] >= x_t} (n if none) and d_out_key[t] = that key (0 if none).
  * d_x: m uint64 probe keys (for a 32-bit list a probe >= 2^32 is past every key).  Either
- * output pointer may be NULL (not both).  m == 0 is a no-op.  Uses the anchor invariant
- * base_j = K[s_j] (FORMAT F2): binary search over the segment bases, then inside one segment. */
+ * output pointer may be NULL (not both).  m == 0 is a no-op.  Binary search over the
+ * segments' first keys K[s_j] — the bases for anchored blobs (FORMAT F2), base + u(s_j) for F7
+ * blobs (decoded only when the probe lies in the band [base_j, base_j + 2 eps)), or the search
+ * index when one is attached (lc_search_index_build) — then inside one segment, decoding only
+ * the probed keys. */
 int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,
                     void* d_out_key, lc_stream stream);
 
