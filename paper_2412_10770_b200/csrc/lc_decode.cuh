@@ -257,12 +257,13 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
 
 // SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key, so the
 // kernel is issue-bound: cap registers at 40 for 6 resident CTAs and skip the L2 prefetch
-// (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch);
-// dense lists keep 5 resident CTAs (<= 48 registers).
+// (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch).
 // UNI: lc_union's fused path (stores shifted by Ins; dense settings)
+// Dense (and UNI): 4 CTAs / <= 64 registers.  A/B on B200 against 5 CTAs / 48 registers:
+// bench config 2 5370 -> 5430 GB/s (three alternating pairs), config 5 -1.4% time, config 3
+// flat; the union's shifted decode spilled at 48 (0.367 -> 0.358 ms).
 template <bool K64, uint32_t B, bool SPARSE, bool UNI = false>
-// UNI: 4 CTAs / 64 registers (the insertion state spilled at 48: A/B union 0.367 -> 0.358 ms)
-__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : (UNI ? 4 : 5))
+__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 4)
     lc_decode_kernel(const DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
