@@ -255,15 +255,16 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
     sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
 
-// SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key, so the
-// kernel is issue-bound: cap registers at 40 for 6 resident CTAs and skip the L2 prefetch
-// (A/B on B200: -4.7% time on config 4, +0.5-0.8% on dense configs, hence the switch).
-// UNI: lc_union's fused path (stores shifted by Ins; dense settings)
-// Dense (and UNI): 4 CTAs / <= 64 registers.  A/B on B200 against 5 CTAs / 48 registers:
-// bench config 2 5370 -> 5430 GB/s (three alternating pairs), config 5 -1.4% time, config 3
-// flat; the union's shifted decode spilled at 48 (0.367 -> 0.358 ms).
+// SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key: no L2
+// prefetch of the next chunk (A/B: it costs config 4 +1.4% time) and the per-quad
+// single-segment fast path (config 4 -2.3%; it costs dense lists, so dense kernels omit it).
+// UNI: lc_union's fused path (stores shifted by Ins; dense settings).
+// All: 4 CTAs / <= 64 registers per SM.  A/B on B200 against the former 5 CTAs / 48 registers
+// (dense) and 6 / 40 (sparse): bench config 2 5370 -> 5430 GB/s (three alternating pairs),
+// config 5 -1.4% time, config 3 flat, config 4 5530 -> 5562 GB/s; the union's shifted decode
+// spilled at 48 (0.367 -> 0.358 ms).
 template <bool K64, uint32_t B, bool SPARSE, bool UNI = false>
-__global__ void __launch_bounds__(kThreads, SPARSE ? 6 : 4)
+__global__ void __launch_bounds__(kThreads, 4)
     lc_decode_kernel(const DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
