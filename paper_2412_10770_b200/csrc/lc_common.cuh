@@ -53,6 +53,16 @@ __device__ __forceinline__ uint32_t lc_bound(bool live, uint32_t i, uint32_t n, 
 }
 #define LC_BOUND(live, i, n) lc_bound((live), (i), (n), __LINE__)
 #define LC_CHECK(live, i, n) ((void)lc_bound((live), (i), (n), __LINE__))
+// this translation unit's violation count since the previous call (reset), and where3 = line,
+// index, limit of its last violation (each .cu file has its own counter)
+uint32_t debug_take(uint32_t* where3) {
+    uint32_t v = 0, z = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&v, g_lc_violations, sizeof v);
+    cudaMemcpyToSymbol(g_lc_violations, &z, sizeof z);
+    if (v && where3) cudaMemcpyFromSymbol(where3, g_lc_where, 3 * sizeof(uint32_t));
+    return v;
+}
 #else
 #define LC_BOUND(live, i, n) (i)
 #define LC_CHECK(live, i, n) ((void)0)

@@ -46,23 +46,20 @@ uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
 
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? LC_OK : LC_ERR_CUDA; }
 
-using DecodeFn = void (*)(DecodeArgs);
-
-template <bool K64, bool SPARSE, bool UNI = false, uint32_t... Bs>
-constexpr std::array<DecodeFn, sizeof...(Bs)> decode_table(std::integer_sequence<uint32_t, Bs...>) {
-    return {{&lc_decode_kernel<K64, Bs, SPARSE, UNI>...}};
+// lc_decode_kernel<K64, b, SPARSE, UNI>: one instantiation per residual width b = 0..32
+// (compile-time field offsets and masks), key width and kind (0 dense, 1 sparse, 2 lc_union's
+// shifted decode), built in six parallel translation units (lc_decode_inst.cu)
+const void* decode_kernel(int kind, bool k64, uint32_t b) {
+    using namespace lc_detail;
+    switch (kind * 2 + k64) {
+        case 0: return decode_kernel_0_0(b);
+        case 1: return decode_kernel_0_1(b);
+        case 2: return decode_kernel_1_0(b);
+        case 3: return decode_kernel_1_1(b);
+        case 4: return decode_kernel_2_0(b);
+        default: return decode_kernel_2_1(b);
+    }
 }
-// one instantiation per residual width b = 0..32 (compile-time field offsets and masks),
-// key width and segment density: kDecode[sparse][k64][b]
-const std::array<DecodeFn, 33> kDecode[2][2] = {
-    {decode_table<false, false>(std::make_integer_sequence<uint32_t, 33>{}),
-     decode_table<true, false>(std::make_integer_sequence<uint32_t, 33>{})},
-    {decode_table<false, true>(std::make_integer_sequence<uint32_t, 33>{}),
-     decode_table<true, true>(std::make_integer_sequence<uint32_t, 33>{})}};
-// lc_union's fused path: stores shifted by the short list's insertions, kDecodeUni[k64][b]
-const std::array<DecodeFn, 33> kDecodeUni[2] = {
-    decode_table<false, false, true>(std::make_integer_sequence<uint32_t, 33>{}),
-    decode_table<true, false, true>(std::make_integer_sequence<uint32_t, 33>{})};
 
 struct GridCache {
     std::mutex mu;
@@ -84,7 +81,7 @@ int persistent_grid(int kind, bool k64, uint32_t b) {
     }
     int& occ = g_grid.occ[kind][k64][b];
     if (occ == 0) {
-        const void* fn = (const void*)(kind == 2 ? kDecodeUni[k64][b] : kDecode[kind][k64][b]);
+        const void* fn = decode_kernel(kind, k64, b);
         const int smem = (int)(warp_bytes_for(b) * kWarpsPerCta);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
@@ -116,8 +113,10 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     const int full = persistent_grid(kind, k64, b);
     const uint32_t need = (a.nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const uint32_t grid = need < (uint32_t)full ? need : (uint32_t)full;
-    if (coff) kDecodeUni[k64][b]<<<grid, kThreads, smem, st>>>(a);
-    else kDecode[sparse][k64][b]<<<grid, kThreads, smem, st>>>(a);
+    void* args[] = {&a};
+    if (cudaLaunchKernel(decode_kernel(kind, k64, b), dim3(grid), dim3(kThreads), args, smem, st) !=
+        cudaSuccess)
+        return LC_ERR_CUDA;
     lc_detail::count_launch(1);
     return cuda_status();
 }
@@ -501,16 +500,19 @@ int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, vo
 }
 
 #ifdef LC_DEBUG_BOUNDS
-// bounds-checked builds only: violations counted since the previous call (and reset)
+// bounds-checked builds only: violations counted since the previous call (and reset), summed
+// over the translation units; g_where = source line / index / limit of the last one seen
+static uint32_t g_where[3];
 uint32_t lc_debug_violations(void) {
-    uint32_t v = 0, z = 0;
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(&v, g_lc_violations, sizeof v);
-    cudaMemcpyToSymbol(g_lc_violations, &z, sizeof z);
+    using namespace lc_detail;
+    uint32_t (*const tus[])(uint32_t*) = {debug_violations_0_0, debug_violations_0_1,
+                                          debug_violations_1_0, debug_violations_1_1,
+                                          debug_violations_2_0, debug_violations_2_1};
+    uint32_t v = debug_take(g_where);
+    for (auto f : tus) v += f(g_where);
     return v;
 }
-// source line / index / limit of the last violation
-void lc_debug_where(uint32_t* out3) { cudaMemcpyFromSymbol(out3, g_lc_where, 3 * sizeof(uint32_t)); }
+void lc_debug_where(uint32_t* out3) { std::memcpy(out3, g_where, sizeof g_where); }
 #endif
 
 }  // extern "C"

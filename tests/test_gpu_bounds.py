@@ -17,9 +17,8 @@ def test_bounds_checked_build():
     from paper_2412_10770_b200 import _build
     lib = os.path.join(ROOT, "build", "liblc_bounds.so")
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    if not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in _build.DEPS):
-        subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, "-DLC_DEBUG_BOUNDS", "-I",
-                               os.path.join(ROOT, "include"), *_build.SRCS, "-o", lib])
+    if _build.stale(lib):
+        _build.build_lib(lib, defines=["-DLC_DEBUG_BOUNDS"])
     env = dict(os.environ, LC_LIB=lib)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bounds_check.py")], env=env,
                        capture_output=True, text=True, timeout=1200)
