@@ -67,6 +67,15 @@ typedef struct lc_view {
      * key of segment j, as uint64, in caller-owned device memory.  NULL (lc_view_init's
      * default): lc_next_geq / lc_intersect / lc_union search the params section directly. */
     const uint64_t* d_first;
+    /* Shard views only (lc_shard_upload; both 0 for a whole-blob view): the view holds the
+     * slices of keys [span_lo, span_hi) and nothing else.  Only lc_decode (which then decodes
+     * the shard) and lc_decode_span (spans inside the shard) accept a shard view; every other
+     * device call returns LC_ERR_ARG for it. */
+    uint64_t span_lo, span_hi;
+    /* Shard views: device addresses of starts[0], params[0], hint[0], words[0] as if the whole
+     * sections were present (only the shard's slices are backed by memory, at d_blob).  Not
+     * meant to be dereferenced by callers; zero for whole-blob views. */
+    uint64_t sec_base[4];
 } lc_view;
 
 /* A CUDA stream (binary-compatible with cudaStream_t / CUstream). */
@@ -112,10 +121,35 @@ int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
 int32_t lc_decode(const lc_view* v, void* d_out, lc_stream stream);
 
 /* Decode the key span [i0, i1) into d_out[0 .. i1-i0): the shard of a multi-GPU decode
- * (SURVEY §8(e)).  i0 must be a multiple of 1024 (unless i0 == i1: an empty span is a no-op);
- * i1 <= n.  LC_ERR_ARG otherwise. */
+ * (the paper's §IV-E ① "reduce the data dependencies ... to maximize
+ * parallelism").  i0 must be a multiple of 1024 (unless i0 == i1: an empty span
+ * is a no-op); i1 <= n, and for a shard view [i0, i1) inside [span_lo, span_hi).  LC_ERR_ARG
+ * otherwise. */
 int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out,
                        lc_stream stream);
+
+/* ---------------------------------------------------------------- shards (multi-GPU decode)
+ * A shard of keys [i0, i1) is what one GPU needs to decode that span and nothing more
+ * (SURVEY §8(e)): the hint slice hint[i0/1024 .. ceil(i1/1024)], the segments the span touches
+ * (starts and params from hint[i0/1024] to hint[ceil(i1/1024)], the straddling segment
+ * duplicated across neighbouring shards) and the residual words [i0 b / 32, i1 b / 32 + 1),
+ * each slice 256-byte aligned in one device buffer.  i0 must be a multiple of 1024 and
+ * i0 < i1 <= n. */
+
+/* Device bytes of the shard [i0, i1) of the host blob h_blob (header and hint slice read).
+ * LC_ERR_FORMAT for a bad header or a hint slice that is not non-decreasing within [0, L-1]
+ * (the slice bounds come from it), LC_ERR_ARG for a bad span. */
+int32_t lc_shard_bytes(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_t i1,
+                       uint64_t* shard_bytes);
+
+/* Copy the shard [i0, i1) of the host blob h_blob (pinned memory for true asynchrony) into the
+ * caller's device buffer d_shard (>= lc_shard_bytes, 256-byte aligned) asynchronously on
+ * `stream`, and fill *v as a shard view of it (span_lo = i0, span_hi = i1).  lc_decode(v, d_out)
+ * then writes keys [i0, i1) to d_out[0 .. i1 - i0).  h_blob must stay valid until the copies
+ * complete.  Errors as lc_shard_bytes, plus LC_ERR_ARG (null pointers, buffer too small or
+ * misaligned) and LC_ERR_CUDA. */
+int32_t lc_shard_upload(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_t i1,
+                        void* d_shard, uint64_t shard_bytes, lc_view* v, lc_stream stream);
 
 /* Batched random access Dec(K^c)[i] ("f(j) + Delta[j]"; Table I caption
  * PAPER.md:309, binary search for the segment).  d_idx: q uint64 indices (device);

@@ -15,19 +15,29 @@ struct Sections {
     const uint32_t* hint;
     const uint32_t* words;
     const uint64_t* first;  // optional successor-search index (lc_view.d_first), may be null
-    uint32_t L, W;  // segments, residual words (bounds of params / words)
+    uint32_t L;  // segments (bound of params)
+    uint64_t W;  // residual words (bound of words; up to 2^32 + 4 at N = 2^32 - 1, b = 32)
 };
+
+bool is_shard(const lc_view* v) { return v->span_hi != 0; }
 
 Sections sections_of(const lc_view* v) {
     const uint8_t* B = (const uint8_t*)v->d_blob;
     Sections s;
-    s.starts = (const uint32_t*)(B + v->h.off_starts);
-    s.params = (const ulonglong2*)(B + v->h.off_params);
-    s.hint = (const uint32_t*)(B + v->h.off_hint);
-    s.words = (const uint32_t*)(B + v->h.off_words);
+    if (is_shard(v)) {  // lc_shard_upload: rebased slice pointers (only the span's slices exist)
+        s.starts = (const uint32_t*)(uintptr_t)v->sec_base[0];
+        s.params = (const ulonglong2*)(uintptr_t)v->sec_base[1];
+        s.hint = (const uint32_t*)(uintptr_t)v->sec_base[2];
+        s.words = (const uint32_t*)(uintptr_t)v->sec_base[3];
+    } else {
+        s.starts = (const uint32_t*)(B + v->h.off_starts);
+        s.params = (const ulonglong2*)(B + v->h.off_params);
+        s.hint = (const uint32_t*)(B + v->h.off_hint);
+        s.words = (const uint32_t*)(B + v->h.off_words);
+    }
     s.first = v->d_first;
     s.L = (uint32_t)v->h.n_seg;
-    s.W = (uint32_t)v->h.n_words;
+    s.W = v->h.n_words;
     return s;
 }
 
@@ -41,12 +51,13 @@ uint32_t bias_of(const lc_view* v) { return is_free(v) ? 0u : v->h.eps; }
 #ifdef LC_DEBUG_BOUNDS
 __device__ uint32_t g_lc_violations;
 __device__ uint32_t g_lc_where[3];  // source line, index, limit of the last violation
-__device__ __forceinline__ uint32_t lc_bound(bool live, uint32_t i, uint32_t n, uint32_t line) {
-    if (live && i >= n) {
+template <typename T>
+__device__ __forceinline__ T lc_bound(bool live, T i, uint64_t n, uint32_t line) {
+    if (live && (uint64_t)i >= n) {
         atomicAdd(&g_lc_violations, 1u);
         g_lc_where[0] = line;
-        g_lc_where[1] = i;
-        g_lc_where[2] = n;
+        g_lc_where[1] = (uint32_t)i;
+        g_lc_where[2] = (uint32_t)n;
         return 0;
     }
     return i;

@@ -12,7 +12,7 @@ struct DecodeArgs {
     uint32_t nchunks;  // ceil((i1 - i0) / 1024)
     uint32_t bias;
     uint32_t warp_bytes;  // shared memory per warp
-    uint32_t nwords;      // W (words section length)
+    uint64_t nwords;      // W (words section length; > 2^32 possible at N ~ 2^32, b = 32)
     const uint32_t* rho;   // lc_union fused path only (UNI kernels): see Ins
     const uint32_t* coff;  // [h] = #{m : rho_m < 1024 h}
 };
@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 4)
         const bool has_next = !SPARSE && c + nwarps < a.nchunks;
         if (B && has_next && lane == 0)  // next chunk's residual words -> L2 now
             bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
-                             min(32 * B * 4 + 16, (a.nwords - (h + nwarps) * 32 * B) * 4));
+                             (uint32_t)min((uint64_t)(32 * B * 4 + 16),
+                                       (a.nwords - (uint64_t)(h + nwarps) * 32 * B) * 4));
         uint32_t jb = j0;                // segment holding the window's first key
         uint32_t sb = pg.sS[LC_BOUND(true, j0 - pg.pj, pg.cs)];  // its start
         uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot

@@ -11,7 +11,7 @@ struct RangeArgs {
     uint32_t* err;
     uint64_t q;
     uint32_t len, n, L, b, bias, mask;
-    uint32_t nwords;  // W
+    uint64_t nwords;  // W
 };
 
 // j = max{t in [hint[i>>10], hint[(i>>10)+1]] : starts[t] <= i} (Table I caption)
@@ -29,7 +29,7 @@ __device__ __forceinline__ uint32_t seg_search(const Sections& sec, uint32_t i, 
 __device__ __forceinline__ uint2 field_words(const Sections& sec, uint32_t i, uint32_t b,
                                              uint64_t pol) {
     const uint64_t bit = (uint64_t)i * b;
-    uint32_t wi = (uint32_t)(bit >> 5);
+    uint64_t wi = bit >> 5;
     if (LC_BOUND(true, wi + 1, sec.W) == 0) wi = 0;  // (only a checked build can take this)
     const uint32_t* wp = sec.words + wi;
     return make_uint2(ldh(wp, pol), ldh(wp + 1, pol));
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         const uint64_t off = r.kind == 0 ? (uint64_t)jk * 16 : r.kind == 1 ? (uint64_t)s0 * 4
                                                                             : (uint64_t)w0 * 4;
         const bool valid = r.kind == 0 ? jk + r.t < L
-                                       : (r.kind == 1 || w0 + 4 * r.t + 4 <= a.nwords);
+                                       : (r.kind == 1 || (uint64_t)w0 + 4 * r.t + 4 <= a.nwords);
         cp16(slot + r.dst, r.src + off, valid);
     };
     auto issue = [&](uint32_t k) {

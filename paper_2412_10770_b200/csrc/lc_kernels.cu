@@ -30,6 +30,7 @@
 #include <mutex>
 #include <type_traits>
 #include <utility>
+#include <vector>
 
 #include "lc.h"
 #include "lc_internal.h"
@@ -103,7 +104,7 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     a.chunk0 = (uint32_t)(i0 >> 10);
     a.nchunks = (uint32_t)((i1 - i0 + 1023) >> 10);
     a.bias = bias_of(v);
-    a.nwords = (uint32_t)v->h.n_words;
+    a.nwords = v->h.n_words;
     const uint32_t b = v->h.res_bits;
     a.warp_bytes = warp_bytes_for(b);
     const uint32_t smem = a.warp_bytes * kWarpsPerCta;
@@ -121,40 +122,121 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     return cuda_status();
 }
 
-// lc_decode_host pipeline resources, created once per device: an H2D and a D2H copy stream and
-// one event per span and stage.
+// lc_decode_host pipeline resources: an H2D and a D2H copy stream plus one event per span and
+// stage.  Pipes are pooled per device: a call takes a free pipe of its device (creating one
+// when every pipe is busy enqueueing), so concurrent callers never share events and never hold
+// a lock while they enqueue; pipes live until process exit.
 constexpr uint32_t kMaxSpans = 64;
 struct HostPipe {
-    std::mutex mu;
     int dev = -1;
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t up[kMaxSpans] = {}, dec[kMaxSpans] = {}, done = nullptr;
 };
-HostPipe g_pipe;
+std::mutex g_pipe_mu;
+std::vector<HostPipe*> g_pipe_free;  // idle pipes of every device
 
-int32_t pipe_init() {
+void pipe_destroy(HostPipe* p) {
+    if (p->h2d) cudaStreamDestroy(p->h2d);
+    if (p->d2h) cudaStreamDestroy(p->d2h);
+    if (p->done) cudaEventDestroy(p->done);
+    for (uint32_t k = 0; k < kMaxSpans; ++k) {
+        if (p->up[k]) cudaEventDestroy(p->up[k]);
+        if (p->dec[k]) cudaEventDestroy(p->dec[k]);
+    }
+    delete p;
+}
+
+HostPipe* pipe_acquire() {
     int dev = 0;
-    cudaGetDevice(&dev);
-    if (g_pipe.dev == dev) return LC_OK;
-    if (cudaStreamCreateWithFlags(&g_pipe.h2d, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&g_pipe.d2h, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_pipe.done, cudaEventDisableTiming) != cudaSuccess)
-        return LC_ERR_CUDA;
-    for (uint32_t k = 0; k < kMaxSpans; ++k)
-        if (cudaEventCreateWithFlags(&g_pipe.up[k], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&g_pipe.dec[k], cudaEventDisableTiming) != cudaSuccess)
-            return LC_ERR_CUDA;
-    g_pipe.dev = dev;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_pipe_mu);
+        for (size_t k = 0; k < g_pipe_free.size(); ++k)
+            if (g_pipe_free[k]->dev == dev) {
+                HostPipe* p = g_pipe_free[k];
+                g_pipe_free.erase(g_pipe_free.begin() + k);
+                return p;
+            }
+    }
+    HostPipe* p = new HostPipe;
+    p->dev = dev;
+    bool ok = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) == cudaSuccess;
+    for (uint32_t k = 0; ok && k < kMaxSpans; ++k)
+        ok = cudaEventCreateWithFlags(&p->up[k], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&p->dec[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {  // partially created: release what exists
+        pipe_destroy(p);
+        return nullptr;
+    }
+    return p;
+}
+
+void pipe_release(HostPipe* p) {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    g_pipe_free.push_back(p);
+}
+
+// host->device copy of `bytes` bytes
+int32_t copy_up(void* d, const void* h, uint64_t bytes, cudaStream_t st) {
+    if (!bytes) return LC_OK;
+    return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess ? LC_OK
+                                                                                : LC_ERR_CUDA;
+}
+
+// The blob slices the decode of keys [i0, i1) reads (FORMAT F2 sections; exactly what
+// lc_decode_kernel stages and prefetches for chunks [c0, c1)): hint[c0 .. c1], starts
+// [s_lo, s_hi), params [p_lo, p_hi), words [w_lo, w_hi).  The bounds come from the hint
+// values, so the hint slice is checked (non-decreasing, within [0, L - 1]) before use: a
+// corrupt hint returns LC_ERR_FORMAT instead of sizing copies past the sections.
+struct SpanSlices {
+    uint64_t c0, c1, s_lo, s_hi, p_lo, p_hi, w_lo, w_hi;
+};
+int32_t span_slices(const lc_header& h, const uint8_t* blob, uint64_t i0, uint64_t i1,
+                    SpanSlices* o) {
+    const uint32_t* hint = (const uint32_t*)(blob + h.off_hint);
+    const uint64_t H = h.n_hint - 1, L = h.n_seg, b = h.res_bits;
+    o->c0 = i0 >> 10;
+    o->c1 = (i1 + 1023) >> 10;  // <= H
+    for (uint64_t c = o->c0; c <= o->c1; ++c)
+        if (hint[c] >= L || (c > o->c0 && hint[c] < hint[c - 1])) return LC_ERR_FORMAT;
+    const uint64_t j0 = hint[o->c0], j1 = hint[o->c1 < H ? o->c1 : H];
+    const uint64_t r4 = (L + 1 + 3) & ~3ULL;  // starts entries inside the 256-byte-padded section
+    o->s_lo = j0 & ~3ULL;
+    o->s_hi = ((j1 + 2 + 3) & ~3ULL) < r4 ? ((j1 + 2 + 3) & ~3ULL) : r4;
+    o->p_lo = j0 & ~3ULL;
+    o->p_hi = j1 + 1;
+    o->w_lo = b ? o->c0 * 32 * b : 0;
+    o->w_hi = b ? (o->c1 * 32 * b + 4 < h.n_words ? o->c1 * 32 * b + 4 : h.n_words) : 0;
     return LC_OK;
 }
 
-// host->device copy of blob bytes [a, b) (same offsets on both sides)
-int32_t up_bytes(const void* h, void* d, uint64_t a, uint64_t b, cudaStream_t st) {
-    if (b <= a) return LC_OK;
-    return cudaMemcpyAsync((uint8_t*)d + a, (const uint8_t*)h + a, b - a, cudaMemcpyHostToDevice,
-                           st) == cudaSuccess
-               ? LC_OK
-               : LC_ERR_CUDA;
+// shard buffer layout: hint | starts | params | words slices, each 256-byte aligned
+struct ShardLayout {
+    uint64_t o_hint, o_starts, o_params, o_words, total;
+};
+ShardLayout shard_layout(const SpanSlices& sl) {
+    auto r256_ = [](uint64_t x) { return (x + 255) & ~255ULL; };
+    ShardLayout y;
+    y.o_hint = 0;
+    y.o_starts = r256_(4 * (sl.c1 - sl.c0 + 1));
+    y.o_params = y.o_starts + r256_(4 * (sl.s_hi - sl.s_lo));
+    y.o_words = y.o_params + r256_(16 * (sl.p_hi - sl.p_lo));
+    y.total = y.o_words + r256_(4 * (sl.w_hi - sl.w_lo));
+    return y;
+}
+
+// header + span checks shared by lc_shard_bytes / lc_shard_upload
+int32_t shard_plan(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_t i1,
+                   lc_header* h, SpanSlices* sl) {
+    if (!h_blob) return LC_ERR_ARG;
+    if (blob_bytes < sizeof(lc_header)) return LC_ERR_FORMAT;
+    std::memcpy(h, h_blob, sizeof *h);
+    int32_t st = lc_detail::check_header(h, blob_bytes);
+    if (st) return st;
+    if ((i0 & 1023) || i0 >= i1 || i1 > h->n) return LC_ERR_ARG;
+    return span_slices(*h, (const uint8_t*)h_blob, i0, i1, sl);
 }
 
 int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64_t qdiv, int mode,
@@ -216,6 +298,7 @@ int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, 
     if (!v || !v->d_blob) return LC_ERR_ARG;
     if (i0 > i1 || i1 > v->h.n) return LC_ERR_ARG;
     if (i0 == i1) return LC_OK;  // an empty span (e.g. a shard past the end) is a no-op
+    if (is_shard(v) && (i0 < v->span_lo || i1 > v->span_hi)) return LC_ERR_ARG;
     if (i0 & 1023) return LC_ERR_ARG;
     if (!d_out || ((uintptr_t)d_out & 15)) return LC_ERR_ARG;
     return launch_decode(v, i0, i1, d_out, (cudaStream_t)stream);
@@ -223,12 +306,13 @@ int32_t lc_decode_span(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, 
 
 int32_t lc_decode(const lc_view* v, void* d_out, lc_stream stream) {
     if (!v) return LC_ERR_ARG;
+    if (is_shard(v)) return lc_decode_span(v, v->span_lo, v->span_hi, d_out, stream);
     return lc_decode_span(v, 0, v->h.n, d_out, stream);
 }
 
 int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_out,
                   uint32_t* d_err, lc_stream stream) {
-    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (!v || !v->d_blob || is_shard(v)) return LC_ERR_ARG;
     if (q == 0) return LC_OK;
     if (!d_idx || !d_out) return LC_ERR_ARG;
     return launch_access(v, d_idx, q, 1, kAccess, d_out, d_err, (cudaStream_t)stream);
@@ -236,7 +320,7 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
 
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
                         void* d_out, uint32_t* d_err, lc_stream stream) {
-    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (!v || !v->d_blob || is_shard(v)) return LC_ERR_ARG;
     if (len == 0 || len > (1u << 20)) return LC_ERR_ARG;
     if (q == 0) return LC_OK;
     if (!d_start || !d_out) return LC_ERR_ARG;
@@ -252,7 +336,7 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     a.b = v->h.res_bits;
     a.bias = bias_of(v);
     a.mask = mask_of(a.b);
-    a.nwords = (uint32_t)v->h.n_words;
+    a.nwords = v->h.n_words;
     const uint64_t grid = (q + 255) / 256;  // 8 warps x 32 ranges per CTA
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
@@ -274,7 +358,7 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
 
 int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t q,
                     int32_t exact, void* d_out, uint32_t* d_err, lc_stream stream) {
-    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (!v || !v->d_blob || is_shard(v)) return LC_ERR_ARG;
     if (q == 0 || q > 0xffffffffULL) return LC_ERR_ARG;  // N k < 2^64 for k <= q
     if (m == 0) return LC_OK;
     if (!d_k || !d_out) return LC_ERR_ARG;
@@ -284,7 +368,7 @@ int32_t lc_quantile(const lc_view* v, const uint64_t* d_k, uint64_t m, uint64_t 
 
 int32_t lc_next_geq(const lc_view* v, const uint64_t* d_x, uint64_t m, uint64_t* d_out_idx,
                     void* d_out_key, lc_stream stream) {
-    if (!v || !v->d_blob) return LC_ERR_ARG;
+    if (!v || !v->d_blob || is_shard(v)) return LC_ERR_ARG;
     if (m == 0) return LC_OK;
     if (!d_x || (!d_out_idx && !d_out_key)) return LC_ERR_ARG;
     SuccArgs a;
@@ -318,7 +402,7 @@ uint64_t lc_search_index_bytes(const lc_view* v) {
 }
 
 int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream) {
-    if (!v || !v->d_blob || !d_index || ((uintptr_t)d_index & 127)) return LC_ERR_ARG;
+    if (!v || !v->d_blob || is_shard(v) || !d_index || ((uintptr_t)d_index & 127)) return LC_ERR_ARG;
     const Sections sec = sections_of(v);
     const uint32_t b = v->h.res_bits;
     const unsigned grid = (unsigned)((v->h.n_seg + 255) / 256);
@@ -341,6 +425,7 @@ uint64_t lc_intersect_scratch_bytes(const lc_view* a) {
 int32_t lc_intersect(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                      void* d_out, uint64_t* d_count, lc_stream stream) {
     if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
+    if (is_shard(a) || is_shard(b)) return LC_ERR_ARG;
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_intersect_scratch_bytes(a) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
     // symmetric: decode the shorter list and search the longer one (the scratch and output sized
@@ -391,6 +476,7 @@ uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b) {
 int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                  void* d_out, uint64_t* d_count, lc_stream stream) {
     if (!a || !b || !a->d_blob || !b->d_blob || !d_scratch || !d_out || !d_count) return LC_ERR_ARG;
+    if (is_shard(a) || is_shard(b)) return LC_ERR_ARG;
     if (a->h.key_bits != b->h.key_bits) return LC_ERR_ARG;
     if (scratch_bytes < lc_union_scratch_bytes(a, b) || ((uintptr_t)d_scratch & 255)) return LC_ERR_ARG;
     if ((uintptr_t)d_out % (a->h.key_bits / 8)) return LC_ERR_ARG;
@@ -441,6 +527,49 @@ int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t s
     return launch_decode(lg, 0, nl, d_out, st, rho, coff);
 }
 
+int32_t lc_shard_bytes(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_t i1,
+                       uint64_t* shard_bytes) {
+    if (!shard_bytes) return LC_ERR_ARG;
+    lc_header h;
+    SpanSlices sl;
+    const int32_t st = shard_plan(h_blob, blob_bytes, i0, i1, &h, &sl);
+    if (st) return st;
+    *shard_bytes = shard_layout(sl).total;
+    return LC_OK;
+}
+
+int32_t lc_shard_upload(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_t i1,
+                        void* d_shard, uint64_t shard_bytes, lc_view* v, lc_stream stream) {
+    if (!v || !d_shard || ((uintptr_t)d_shard & 255)) return LC_ERR_ARG;
+    lc_header h;
+    SpanSlices sl;
+    int32_t st = shard_plan(h_blob, blob_bytes, i0, i1, &h, &sl);
+    if (st) return st;
+    const ShardLayout y = shard_layout(sl);
+    if (shard_bytes < y.total) return LC_ERR_ARG;
+    const uint8_t* B = (const uint8_t*)h_blob;
+    uint8_t* D = (uint8_t*)d_shard;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = copy_up(D + y.o_hint, B + h.off_hint + 4 * sl.c0, 4 * (sl.c1 - sl.c0 + 1), s)) ||
+        (st = copy_up(D + y.o_starts, B + h.off_starts + 4 * sl.s_lo, 4 * (sl.s_hi - sl.s_lo), s)) ||
+        (st = copy_up(D + y.o_params, B + h.off_params + 16 * sl.p_lo, 16 * (sl.p_hi - sl.p_lo), s)) ||
+        (st = copy_up(D + y.o_words, B + h.off_words + 4 * sl.w_lo, 4 * (sl.w_hi - sl.w_lo), s)))
+        return st;
+    v->h = h;
+    v->d_blob = d_shard;
+    v->d_first = nullptr;
+    v->span_lo = i0;
+    v->span_hi = i1;
+    // section base addresses as if the whole sections were present (wrapping 64-bit address
+    // arithmetic; the kernels only dereference indices inside the uploaded slices)
+    const uint64_t d = (uint64_t)(uintptr_t)d_shard;
+    v->sec_base[0] = d + y.o_starts - 4 * sl.s_lo;
+    v->sec_base[1] = d + y.o_params - 16 * sl.p_lo;
+    v->sec_base[2] = d + y.o_hint - 4 * sl.c0;
+    v->sec_base[3] = d + y.o_words - 4 * sl.w_lo;
+    return cuda_status();
+}
+
 int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, void* d_out,
                        void* h_out, lc_stream stream) {
     if (!h_blob || !d_blob || !d_out || !h_out) return LC_ERR_ARG;
@@ -448,55 +577,58 @@ int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, vo
     lc_view v;
     int32_t st = lc_view_init(&v, h_blob, d_blob, blob_bytes);
     if (st) return st;
-    cudaStream_t s = (cudaStream_t)stream;
-    std::lock_guard<std::mutex> lk(g_pipe.mu);
-    if ((st = pipe_init())) return st;
-    // order the pipeline after whatever the caller queued on its stream
-    cudaEventRecord(g_pipe.done, s);
-    cudaStreamWaitEvent(g_pipe.h2d, g_pipe.done, 0);
-    cudaStreamWaitEvent(g_pipe.d2h, g_pipe.done, 0);
-
     const lc_header& h = v.h;
     const uint8_t* B = (const uint8_t*)h_blob;
-    const uint32_t* hint = (const uint32_t*)(B + h.off_hint);
-    const uint64_t n = h.n, w = h.key_bits / 8, L = h.n_seg, b = h.res_bits;
-    const uint64_t H = h.n_hint - 1;
+    const uint64_t n = h.n, w = h.key_bits / 8;
     // spans of >= 4 Mi keys (multiples of 1024), at most kMaxSpans (a ramped 1/4, 1/2, ... span
     // schedule measured 0.35 ms slower on config 2: the gap to the PCIe floor is the two
     // directions sharing the link, not pipeline fill)
     uint64_t per = (n + kMaxSpans - 1) / kMaxSpans;
     if (per < (4u << 20)) per = 4u << 20;
     per = (per + 1023) & ~1023ULL;
-    uint32_t k = 0;
-    for (uint64_t i0 = 0; i0 < n; i0 += per, ++k) {
-        const uint64_t i1 = i0 + per < n ? i0 + per : n;
-        const uint64_t c0 = i0 >> 10, c1 = (i1 + 1023) >> 10;  // chunks [c0, c1)
-        const uint64_t j0 = hint[c0], j1 = hint[c1 < H ? c1 : H];
-        // exactly the slices the span's kernel stages (FORMAT F2 sections, 16-byte rounded)
-        const uint64_t s_lo = (j0 & ~3ULL), s_hi = ((j1 + 2 + 3) & ~3ULL) < ((L + 1 + 3) & ~3ULL)
-                                                     ? ((j1 + 2 + 3) & ~3ULL)
-                                                     : ((L + 1 + 3) & ~3ULL);
-        const uint64_t w_lo = c0 * 32 * b, w_hi = (c1 * 32 * b + 4) < h.n_words ? c1 * 32 * b + 4
-                                                                                  : h.n_words;
-        if ((st = up_bytes(B, d_blob, h.off_hint + 4 * c0, h.off_hint + 4 * (c1 + 1), g_pipe.h2d)) ||
-            (st = up_bytes(B, d_blob, h.off_starts + 4 * s_lo, h.off_starts + 4 * s_hi, g_pipe.h2d)) ||
-            (st = up_bytes(B, d_blob, h.off_params + 16 * (j0 & ~3ULL), h.off_params + 16 * (j1 + 1),
-                           g_pipe.h2d)) ||
-            (b && (st = up_bytes(B, d_blob, h.off_words + 4 * w_lo, h.off_words + 4 * w_hi,
-                                 g_pipe.h2d))))
-            return st;
-        cudaEventRecord(g_pipe.up[k], g_pipe.h2d);
-        cudaStreamWaitEvent(s, g_pipe.up[k], 0);
-        if ((st = launch_decode(&v, i0, i1, (uint8_t*)d_out + i0 * w, s))) return st;
-        cudaEventRecord(g_pipe.dec[k], s);
-        cudaStreamWaitEvent(g_pipe.d2h, g_pipe.dec[k], 0);
+    // every span's slices first: a corrupt hint fails before anything is enqueued
+    SpanSlices sl[kMaxSpans];
+    uint32_t ns = 0;
+    for (uint64_t i0 = 0; i0 < n; i0 += per, ++ns)
+        if ((st = span_slices(h, B, i0, i0 + per < n ? i0 + per : n, &sl[ns]))) return st;
+    HostPipe* p = pipe_acquire();
+    if (!p) return LC_ERR_CUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    // order the pipeline after whatever the caller queued on its stream
+    cudaEventRecord(p->done, s);
+    cudaStreamWaitEvent(p->h2d, p->done, 0);
+    cudaStreamWaitEvent(p->d2h, p->done, 0);
+    uint8_t* D = (uint8_t*)d_blob;
+    for (uint32_t k = 0; k < ns && !st; ++k) {
+        const uint64_t i0 = k * per, i1 = i0 + per < n ? i0 + per : n;
+        const SpanSlices& q = sl[k];
+        // exactly the slices the span's kernel stages, at their offsets in the device blob
+        if ((st = copy_up(D + h.off_hint + 4 * q.c0, B + h.off_hint + 4 * q.c0,
+                          4 * (q.c1 - q.c0 + 1), p->h2d)) ||
+            (st = copy_up(D + h.off_starts + 4 * q.s_lo, B + h.off_starts + 4 * q.s_lo,
+                          4 * (q.s_hi - q.s_lo), p->h2d)) ||
+            (st = copy_up(D + h.off_params + 16 * q.p_lo, B + h.off_params + 16 * q.p_lo,
+                          16 * (q.p_hi - q.p_lo), p->h2d)) ||
+            (st = copy_up(D + h.off_words + 4 * q.w_lo, B + h.off_words + 4 * q.w_lo,
+                          4 * (q.w_hi - q.w_lo), p->h2d)))
+            break;
+        cudaEventRecord(p->up[k], p->h2d);
+        cudaStreamWaitEvent(s, p->up[k], 0);
+        if ((st = launch_decode(&v, i0, i1, (uint8_t*)d_out + i0 * w, s))) break;
+        cudaEventRecord(p->dec[k], s);
+        cudaStreamWaitEvent(p->d2h, p->dec[k], 0);
         if (cudaMemcpyAsync((uint8_t*)h_out + i0 * w, (uint8_t*)d_out + i0 * w, (i1 - i0) * w,
-                            cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
-            return LC_ERR_CUDA;
+                            cudaMemcpyDeviceToHost, p->d2h) != cudaSuccess)
+            st = LC_ERR_CUDA;
     }
-    cudaEventRecord(g_pipe.done, g_pipe.d2h);
-    cudaStreamWaitEvent(s, g_pipe.done, 0);
-    return cuda_status();
+    // join the copy streams back into the caller's stream (also after an error, so the pipe
+    // is idle before it is reused)
+    cudaEventRecord(p->done, p->d2h);
+    cudaStreamWaitEvent(s, p->done, 0);
+    cudaEventRecord(p->done, p->h2d);
+    cudaStreamWaitEvent(s, p->done, 0);
+    pipe_release(p);
+    return st ? st : cuda_status();
 }
 
 #ifdef LC_DEBUG_BOUNDS

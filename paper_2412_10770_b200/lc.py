@@ -41,7 +41,8 @@ assert C.sizeof(lc_header) == 128
 
 
 class lc_view(C.Structure):
-    _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p)]
+    _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p),
+                ("span_lo", C.c_uint64), ("span_hi", C.c_uint64), ("sec_base", C.c_uint64 * 4)]
 
 
 _p, _u64, _u32, _i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32
@@ -64,6 +65,8 @@ _sig = {
     "lc_search_index_build": ([C.POINTER(lc_view), _p, _p], _i32),
     "lc_union": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
+    "lc_shard_bytes": ([_p, _u64, _u64, _u64, C.POINTER(_u64)], _i32),
+    "lc_shard_upload": ([_p, _u64, _u64, _u64, _p, _u64, C.POINTER(lc_view), _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
 }
@@ -91,6 +94,48 @@ def _stream(stream) -> int | None:
         import torch
         return torch.cuda.current_stream().cuda_stream
     return getattr(stream, "cuda_stream", stream)
+
+
+class _On:
+    """Stream discipline of one call that launches on `stream` (a torch.cuda.Stream, a raw
+    cudaStream_t handle, or None = the current stream).
+
+    When `stream` is a torch stream other than the current one: it first waits for the current
+    stream (inputs staged there are ready), every device tensor the call reads or writes is
+    marked used on it (record_stream: the caching allocator will not hand that memory to other
+    work while the kernels may still run), and tensors allocated inside the `with` block
+    (outputs, scratch) are allocated on it, so dropping a scratch right after the call is
+    safe.  A raw handle leaves this to the caller."""
+
+    def __init__(self, stream, *tensors):
+        import torch
+        cur = torch.cuda.current_stream()
+        self.handle = _stream(stream)
+        self.ts = stream if isinstance(stream, torch.cuda.Stream) else None
+        self.other = self.ts is not None and self.ts != cur
+        self._ctx = None
+        if self.other:
+            self.ts.wait_stream(cur)
+            self.use(*tensors)
+
+    def use(self, *tensors):
+        if self.other:
+            for t in tensors:
+                if t is not None and getattr(t, "is_cuda", False):
+                    t.record_stream(self.ts)
+        return tensors[0] if len(tensors) == 1 else tensors
+
+    def __enter__(self):
+        if self.other:
+            import torch
+            self._ctx = torch.cuda.stream(self.ts)
+            self._ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self._ctx is not None:
+            self._ctx.__exit__(*exc)
+        return False
 
 
 def launch_count() -> int:
@@ -154,13 +199,52 @@ class View:
         if d_blob is None:
             d_blob = torch.from_numpy(host.copy()).to(device)
         self.d_blob = d_blob
+        self.d_first = None
         self.v = lc_view()
         _check(_lib.lc_view_init(C.byref(self.v), host.ctypes.data, d_blob.data_ptr(),
                                  host.nbytes), "lc_view_init")
 
+    @classmethod
+    def shard(cls, h_blob, i0: int, i1: int, device="cuda", stream=None, out=None):
+        """lc_shard_upload: a shard view holding only the slices of keys [i0, i1) of the host
+        blob h_blob (bytes, numpy uint8 or a pinned CPU uint8 tensor); decode() then writes
+        keys [i0, i1).  The host buffer is kept referenced by the view until it is dropped."""
+        import torch
+        hp, hn, keep = _host_ptr(h_blob)
+        nb = C.c_uint64()
+        _check(_lib.lc_shard_bytes(hp, hn, i0, i1, C.byref(nb)), "lc_shard_bytes")
+        self = cls.__new__(cls)
+        self.d_first = None
+        self._host_keep = keep
+        with _On(stream) as on:
+            if out is None:
+                out = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=device)
+            on.use(out)
+            if out.numel() < nb.value:
+                raise ValueError("shard buffer too small")
+            self.d_blob = out
+            self.v = lc_view()
+            _check(_lib.lc_shard_upload(hp, hn, i0, i1, out.data_ptr(), out.numel(),
+                                        C.byref(self.v), on.handle), "lc_shard_upload")
+        return self
+
+    @staticmethod
+    def shard_bytes(h_blob, i0: int, i1: int) -> int:
+        hp, hn, _keep = _host_ptr(h_blob)
+        nb = C.c_uint64()
+        _check(_lib.lc_shard_bytes(hp, hn, i0, i1, C.byref(nb)), "lc_shard_bytes")
+        return int(nb.value)
+
     @property
     def n(self) -> int:
         return int(self.v.h.n)
+
+    @property
+    def span(self) -> tuple[int, int]:
+        """Keys this view decodes: (0, n), or a shard's (span_lo, span_hi)."""
+        if self.v.span_hi:
+            return int(self.v.span_lo), int(self.v.span_hi)
+        return 0, self.n
 
     @property
     def key_bits(self) -> int:
@@ -180,69 +264,89 @@ class View:
         `stream` and attach it to this view (next_geq / intersect / union then use it)."""
         import torch
         nbytes = self.search_index_bytes()
-        if out is None:
-            out = torch.empty(max(nbytes // 8, 1), dtype=torch.int64, device=self.d_blob.device)
-        if out.numel() * out.element_size() < nbytes:
-            raise ValueError("search index buffer too small")
-        self.d_first = out
-        _check(_lib.lc_search_index_build(C.byref(self.v), self.d_first.data_ptr(), _stream(stream)),
-               "lc_search_index_build")
+        with _On(stream, self.d_blob) as on:
+            if out is None:
+                out = torch.empty(max(nbytes // 8, 1), dtype=torch.int64, device=self.d_blob.device)
+            if out.numel() * out.element_size() < nbytes:
+                raise ValueError("search index buffer too small")
+            self.d_first = on.use(out)
+            _check(_lib.lc_search_index_build(C.byref(self.v), self.d_first.data_ptr(), on.handle),
+                   "lc_search_index_build")
         return self.d_first
+
+    def tensors(self):
+        """Device tensors the view's calls read (for stream bookkeeping)."""
+        return (self.d_blob, self.d_first)
 
     def out_tensor(self, count: int):
         import torch
         return torch.empty(count, dtype=self.torch_dtype, device=self.d_blob.device)
 
 
+def _ptr(t) -> int | None:
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
 def decode(view: View, out=None, stream=None):
-    """lc_decode: all N keys into a device tensor (int64/int32 storage of u64/u32 keys)."""
-    if out is None:
-        out = view.out_tensor(view.n)
-    _check(_lib.lc_decode(C.byref(view.v), out.data_ptr(), _stream(stream)), "lc_decode")
+    """lc_decode: all N keys (or a shard view's span) into a device tensor (int64/int32 storage
+    of u64/u32 keys)."""
+    with _On(stream, *view.tensors()) as on:
+        if out is None:
+            lo, hi = view.span
+            out = view.out_tensor(hi - lo)
+        on.use(out)
+        _check(_lib.lc_decode(C.byref(view.v), out.data_ptr(), on.handle), "lc_decode")
     return out
 
 
 def decode_span(view: View, i0: int, i1: int, out=None, stream=None):
-    if out is None:
-        out = view.out_tensor(max(i1 - i0, 0))
-    _check(_lib.lc_decode_span(C.byref(view.v), i0, i1, out.data_ptr() if out.numel() else None,
-                               _stream(stream)), "lc_decode_span")
+    with _On(stream, *view.tensors()) as on:
+        if out is None:
+            out = view.out_tensor(max(i1 - i0, 0))
+        on.use(out)
+        _check(_lib.lc_decode_span(C.byref(view.v), i0, i1, _ptr(out), on.handle),
+               "lc_decode_span")
     return out
 
 
 def access(view: View, idx, out=None, err=None, stream=None):
     """lc_access: Dec(K^c)[idx] for a device int64 tensor of indices."""
     q = idx.numel()
-    if out is None:
-        out = view.out_tensor(q)
-    _check(_lib.lc_access(C.byref(view.v), idx.data_ptr() if q else None, q,
-                          out.data_ptr() if q else None,
-                          err.data_ptr() if err is not None else None, _stream(stream)),
-           "lc_access")
+    with _On(stream, *view.tensors(), idx, err) as on:
+        if out is None:
+            out = view.out_tensor(q)
+        on.use(out)
+        _check(_lib.lc_access(C.byref(view.v), _ptr(idx), q, _ptr(out) if q else None,
+                              err.data_ptr() if err is not None else None, on.handle),
+               "lc_access")
     return out
 
 
 def range_decode(view: View, starts, length: int, out=None, err=None, stream=None):
     """lc_range_decode: out[r, k] = K[starts[r] + k]."""
     q = starts.numel()
-    if out is None:
-        out = view.out_tensor(q * length)
-    _check(_lib.lc_range_decode(C.byref(view.v), starts.data_ptr() if q else None, q, length,
-                                out.data_ptr() if q else None,
-                                err.data_ptr() if err is not None else None, _stream(stream)),
-           "lc_range_decode")
+    with _On(stream, *view.tensors(), starts, err) as on:
+        if out is None:
+            out = view.out_tensor(q * length)
+        on.use(out)
+        _check(_lib.lc_range_decode(C.byref(view.v), _ptr(starts), q, length,
+                                    _ptr(out) if q else None,
+                                    err.data_ptr() if err is not None else None, on.handle),
+               "lc_range_decode")
     return out.view(q, length)
 
 
 def quantile(view: View, ranks, q: int, exact: bool = True, out=None, err=None, stream=None):
     """lc_quantile: the ranks[t]-th q-quantiles (exact, or the segments-only approximation)."""
     m = ranks.numel()
-    if out is None:
-        out = view.out_tensor(m)
-    _check(_lib.lc_quantile(C.byref(view.v), ranks.data_ptr() if m else None, m, q,
-                            1 if exact else 0, out.data_ptr() if m else None,
-                            err.data_ptr() if err is not None else None, _stream(stream)),
-           "lc_quantile")
+    with _On(stream, *view.tensors(), ranks, err) as on:
+        if out is None:
+            out = view.out_tensor(m)
+        on.use(out)
+        _check(_lib.lc_quantile(C.byref(view.v), _ptr(ranks), m, q, 1 if exact else 0,
+                                _ptr(out) if m else None,
+                                err.data_ptr() if err is not None else None, on.handle),
+               "lc_quantile")
     return out
 
 
@@ -250,13 +354,14 @@ def next_geq(view: View, x, out_idx=None, out_key=None, stream=None):
     """lc_next_geq: (first index with K[i] >= x_t, that key) for a device int64 tensor of probes."""
     import torch
     m = x.numel()
-    if out_idx is None:
-        out_idx = torch.empty(m, dtype=torch.int64, device=x.device)
-    if out_key is None:
-        out_key = view.out_tensor(m)
-    _check(_lib.lc_next_geq(C.byref(view.v), x.data_ptr() if m else None, m,
-                            out_idx.data_ptr() if m else None, out_key.data_ptr() if m else None,
-                            _stream(stream)), "lc_next_geq")
+    with _On(stream, *view.tensors(), x) as on:
+        if out_idx is None:
+            out_idx = torch.empty(m, dtype=torch.int64, device=x.device)
+        if out_key is None:
+            out_key = view.out_tensor(m)
+        on.use(out_idx, out_key)
+        _check(_lib.lc_next_geq(C.byref(view.v), _ptr(x), m, _ptr(out_idx) if m else None,
+                                _ptr(out_key) if m else None, on.handle), "lc_next_geq")
     return out_idx, out_key
 
 
@@ -278,15 +383,17 @@ def intersect(a: View, b: View, scratch=None, out=None, count=None, stream=None)
     import torch
     dev = a.d_blob.device
     need = int(_lib.lc_intersect_scratch_bytes(C.byref(a.v)))
-    if scratch is None:
-        scratch = torch.empty(need, dtype=torch.uint8, device=dev)
-    if out is None:
-        out = a.out_tensor(a.n)
-    if count is None:
-        count = torch.zeros(1, dtype=torch.int64, device=dev)
-    _check(_lib.lc_intersect(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
-                             scratch.numel() * scratch.element_size(), out.data_ptr(),
-                             count.data_ptr(), _stream(stream)), "lc_intersect")
+    with _On(stream, *a.tensors(), *b.tensors()) as on:
+        if scratch is None:
+            scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+        if out is None:
+            out = a.out_tensor(a.n)
+        if count is None:
+            count = torch.zeros(1, dtype=torch.int64, device=dev)
+        on.use(scratch, out, count)
+        _check(_lib.lc_intersect(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
+                                 scratch.numel() * scratch.element_size(), out.data_ptr(),
+                                 count.data_ptr(), on.handle), "lc_intersect")
     return out, count
 
 
@@ -295,20 +402,23 @@ def union(a: View, b: View, scratch=None, out=None, count=None, stream=None):
     import torch
     dev = a.d_blob.device
     need = int(_lib.lc_union_scratch_bytes(C.byref(a.v), C.byref(b.v)))
-    if scratch is None:
-        scratch = torch.empty(need, dtype=torch.uint8, device=dev)
-    if out is None:
-        out = a.out_tensor(a.n + b.n)
-    if count is None:
-        count = torch.zeros(1, dtype=torch.int64, device=dev)
-    _check(_lib.lc_union(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
-                         scratch.numel() * scratch.element_size(), out.data_ptr(),
-                         count.data_ptr(), _stream(stream)), "lc_union")
+    with _On(stream, *a.tensors(), *b.tensors()) as on:
+        if scratch is None:
+            scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+        if out is None:
+            out = a.out_tensor(a.n + b.n)
+        if count is None:
+            count = torch.zeros(1, dtype=torch.int64, device=dev)
+        on.use(scratch, out, count)
+        _check(_lib.lc_union(C.byref(a.v), C.byref(b.v), scratch.data_ptr(),
+                             scratch.numel() * scratch.element_size(), out.data_ptr(),
+                             count.data_ptr(), on.handle), "lc_union")
     return out, count
 
 
 def decode_host(h_blob, d_blob, d_out, h_out, stream=None) -> None:
     """lc_decode_host: pinned host blob -> device -> decode -> pinned host keys (async)."""
-    _check(_lib.lc_decode_host(h_blob.data_ptr(), h_blob.numel(), d_blob.data_ptr(),
-                               d_out.data_ptr(), h_out.data_ptr(), _stream(stream)),
-           "lc_decode_host")
+    with _On(stream, d_blob, d_out) as on:
+        _check(_lib.lc_decode_host(h_blob.data_ptr(), h_blob.numel(), d_blob.data_ptr(),
+                                   d_out.data_ptr(), h_out.data_ptr(), on.handle),
+               "lc_decode_host")

@@ -1,9 +1,11 @@
 """Multi-GPU host logic: full decode shards with no exchange step.
 
 The key index space is cut at multiples of 1024 (hint-block boundaries, FORMAT F2), so every
-shard is a legal `lc_decode_span` and each GPU decodes its span from its own copy of the
-(small) compressed blob.  No collective touches the data path; `max_over_ranks` is only for
-timing.
+shard is a legal `lc_decode_span`.  Each GPU uploads only its shard of the compressed blob
+(`lc_shard_upload`: the span's hint, starts, params and residual-word slices; the straddling
+segment is duplicated) and decodes it independently (§IV-E ① "reduce the data
+dependencies ... to maximize parallelism").  No collective touches the data path;
+`max_over_ranks` is only for timing.
 """
 from __future__ import annotations
 
@@ -26,10 +28,25 @@ def shard_spans(n: int, world: int) -> list[tuple[int, int]]:
     return spans
 
 
-def decode_shard(view, rank: int, world: int, out=None, stream=None):
-    """Decode this rank's span of the list on its GPU (lc_decode_span)."""
+def upload_shard(h_blob, rank: int, world: int, device="cuda", stream=None):
+    """This rank's shard view (lc_shard_upload): only the slices its span reads are copied to
+    `device`.  Returns (view or None for an empty span, (i0, i1))."""
     from . import lc
+    i0, i1 = shard_spans(int(lc.header(h_blob).n), world)[rank]
+    if i0 == i1:
+        return None, (i0, i1)
+    return lc.View.shard(h_blob, i0, i1, device=device, stream=stream), (i0, i1)
+
+
+def decode_shard(view, rank: int, world: int, out=None, stream=None):
+    """Decode this rank's span of the list on its GPU: `view` is the rank's shard view
+    (upload_shard) or a whole-blob view (lc_decode_span over the rank's span)."""
+    from . import lc
+    if view is None:  # empty span
+        return None, (0, 0)
     i0, i1 = shard_spans(view.n, world)[rank]
+    if view.v.span_hi and view.span != (i0, i1):
+        raise ValueError(f"shard view holds {view.span}, rank {rank} of {world} needs {(i0, i1)}")
     return lc.decode_span(view, i0, i1, out=out, stream=stream), (i0, i1)
 
 

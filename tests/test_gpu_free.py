@@ -94,10 +94,11 @@ def test_free_decode_top_and_bottom_of_range(lc):
             assert _decode_equal(lc, _enc(lc, low, eps), low)
 
 
-@pytest.mark.parametrize("cid", [1, 2, 5])
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
 def test_free_full_config(lc, cid):
-    """Full-size configs 1, 2, 5 encoded with F7: every element on device, sampled indices
-    against the oracle's access of the same blob."""
+    """Every full-size config encoded with F7: every element on device, 1e7 random accesses
+    against the generator's keys on device, sampled indices against the oracle's access of the
+    same blob."""
     keys = make_keys(cid)
     blob = _enc(lc, keys, CONFIGS[cid].eps)
     view = lc.View(blob, device=DEV)
@@ -111,6 +112,8 @@ def test_free_full_config(lc, cid):
     assert err == 0
     got = lc.access(view, _dev(idx))
     assert np.array_equal(_host(got, keys.dtype), want)
+    d_idx = torch.from_numpy(rng.integers(0, keys.size, 10_000_000)).to(DEV)
+    assert torch.equal(lc.access(view, d_idx), out[d_idx])
 
 
 def test_free_access_range(lc):
