@@ -192,7 +192,9 @@ def header(blob) -> lc_header:
 class View:
     """A blob resident on the GPU: lc_view (host header + device pointer) plus the tensor."""
 
-    def __init__(self, blob, device="cuda", d_blob=None):
+    def __init__(self, blob, device="cuda", d_blob=None, blob_bytes=None):
+        """`blob`: the host blob (or at least its 128-byte header when `d_blob`, a device copy
+        of `blob_bytes` bytes, is given)."""
         import torch
         raw = bytes(blob) if not isinstance(blob, (bytes, np.ndarray)) else blob
         host = np.frombuffer(raw, np.uint8) if isinstance(raw, bytes) else raw.view(np.uint8)
@@ -201,8 +203,9 @@ class View:
         self.d_blob = d_blob
         self.d_first = None
         self.v = lc_view()
-        _check(_lib.lc_view_init(C.byref(self.v), host.ctypes.data, d_blob.data_ptr(),
-                                 host.nbytes), "lc_view_init")
+        nbytes = host.nbytes if blob_bytes is None else int(blob_bytes)
+        _check(_lib.lc_view_init(C.byref(self.v), host.ctypes.data, d_blob.data_ptr(), nbytes),
+               "lc_view_init")
 
     @classmethod
     def shard(cls, h_blob, i0: int, i1: int, device="cuda", stream=None, out=None):

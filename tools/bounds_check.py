@@ -53,6 +53,22 @@ def main():
         fb = np.zeros(n, np.uint8)
         fb[:: {"all": 1, "every2": 2, "tile": 1024}[brk]] = 1
         cases.append((k5, 127, 64, "adv-" + brk, orc.encode(k5, 127, force_break=fb)))
+    # sparse fast path edges: segment starts exactly at quad ends and chunk edges, N a
+    # multiple of 128 / 1024 (clamped candidates repeat N)
+    for ns in (1024 * 9, 1024 * 9 + 128, 1024 * 9 + 1):
+        ks = np.arange(ns, dtype=np.uint64) * np.uint64(5) + np.uint64(11)
+        for step in (128, 1024, 256):
+            fb = np.zeros(ns, np.uint8)
+            fb[(step - 1 if step == 256 else 0)::step] = 1
+            cases.append((ks, 2, 64, f"sparse-{ns}-{step}", orc.encode(ks, 2, force_break=fb)))
+    # shard views: the slices of one span only
+    from paper_2412_10770_b200 import shard as _shard
+    kb4 = make_keys(4, 70_001)
+    b4 = lc.encode(kb4, 31)
+    for r in range(3):
+        sv, (i0, i1) = _shard.upload_shard(b4, r, 3, device=dev)
+        so, _ = _shard.decode_shard(sv, r, 3)
+        check(f"shard {r}/3", np.array_equal(h(so, np.uint64), kb4[i0:i1]))
     for cid in (1, 2, 3, 4):
         keys = make_keys(cid, 70_001)
         cases.append((keys, CONFIGS[cid].eps, CONFIGS[cid].key_bits, f"cfg{cid}"))
