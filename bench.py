@@ -1,16 +1,19 @@
 #!/usr/bin/env python
 """bench.py -- full-decode throughput of the learned-compression decoder on B200.
 
-One step = one lc_decode launch over the whole BASELINE config-2 list (N = 1e8 u64 keys,
-geometric gaps mean 100, eps = 127): read the compressed blob once, write N keys once.
+One step = one lc_decode launch over the whole BASELINE config-4 list (N = 5e8 u64 keys, Zipf
+clusters, eps = 31; the largest config): read the compressed blob once, write N keys once.
 Metric (BASELINE.json): full-decode GB/s = (compressed bytes + N * 8) / t, plus keys/s and the
-fraction of the measured HBM copy peak; random-access lookups/s and range decodes on config 5.
+fraction of the measured HBM copy peak.  Beside the headline, `decode_configs` times configs 2
+and 3 (the other 1e8+-key configs of the north-star target), `access` times config 5's random
+access and range decodes (plus quantiles, successor search, intersection, union) and
+`free_intercept` config 2 under FORMAT F7.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config 1..5]
 
-Under torchrun (N > 1) every rank decodes its own replica of the workload (weak scaling, no
-collective: the decode shards with no exchange step); the time is the
-max over ranks of the device-timed region.
+Under torchrun (N > 1) the list is sharded (strong scaling): every rank uploads only its
+1024-aligned span's slices of the blob (lc_shard_upload) and decodes them, with no collective
+on the data path; the time is the max over ranks of the device-timed region.
 """
 from __future__ import annotations
 
@@ -111,6 +114,29 @@ def _workload_name(cid):
     return f"config{cid}: N={s.n:.0e} u{s.key_bits} keys, {s.desc}, eps={s.eps}"
 
 
+def _config_dict(cid, n, blob_len, L, b, ws):
+    """The line's `config` (identical for both arms: same workload, same blob bytes)."""
+    spec = _spec(cid)
+    w = spec.key_bits // 8
+    alg = blob_len + n * w
+    return {"workload": _workload_name(cid), "n": n, "key_bits": spec.key_bits, "eps": spec.eps,
+            "res_bits": b, "segments": L, "blob_bytes": blob_len, "bits_per_int": 8 * blob_len / n,
+            "ratio_r": blob_len / (n * w), "bytes_per_step": alg,
+            "l2": ("no flush: every step reads+writes %.2f GB >> 126 MB L2" % (alg / 1e9))
+            if alg > 4 * 126e6 else "L2 not flushed: the step's %.1f MB are not >> the 126 MB L2 "
+            "(small informational config)" % (alg / 1e6),
+            "parallelism": "single GPU" if ws == 1 else
+            f"shards x{ws} (strong: each GPU holds and decodes 1/{ws} of the list)"}
+
+
+def _kernel_name(h):
+    """Symbol of the full-decode instantiation lc_decode picks for header h (lc_kernels.cu:
+    dense / sparse by segment density, one instantiation per key width and residual width)."""
+    k64 = int(h.key_bits == 64)
+    sparse = int(h.n_seg * 64 < h.n)
+    return f"lc_decode_kernel<{k64},{int(h.res_bits)},{sparse},0>"
+
+
 def _env_dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -131,6 +157,7 @@ def run_reference(args):
     spec = _spec(cid)
     keys = make_keys(cid)
     blob = orc.encode(keys, spec.eps)  # oracle's own encoder
+    oh = orc.header(blob)
     n = keys.size
     w = spec.key_bits // 8
     out = np.empty(n, keys.dtype)
@@ -171,11 +198,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic",
-        "config": {"workload": _workload_name(cid), "n": n, "eps": spec.eps,
-                   "blob_bytes": len(blob), "sample_keys": m},
-        "keys_per_s": m / t,
+        "higher_is_better": True, "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None,
+        "dtype": "u64" if w == 8 else "u32", "data": "synthetic",
+        "config": _config_dict(cid, n, len(blob), int(oh.L), int(oh.b), ws),
+        "sample_keys": m, "keys_per_s": m / t,
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nt, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -184,8 +210,14 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------- GPU arm
-def _cpu_baseline(blob, keys, reps=3):
+def _cpu_baseline(cid, blob, keys, t_enc_product, reps=3):
+    """The oracle on the host cores (BASELINE.md CPU-baseline plan): full decode on all cores
+    (OpenMP over 65536-key spans, median of `reps`), plus single-threaded decode and encode on
+    bounded samples of the same list."""
     from oracle import native as orc
+    n = keys.size
+    w = keys.dtype.itemsize
+    alg = len(blob) + n * w
     out = np.empty_like(keys)
     ts, nt = [], 1
     for _ in range(reps):
@@ -193,8 +225,28 @@ def _cpu_baseline(blob, keys, reps=3):
         _, nt = orc.decode_mt(blob, out)
         ts.append(time.perf_counter() - t0)
     assert np.array_equal(out, keys)
+    del out
     t = statistics.median(ts)
-    return t, nt
+    # single thread: decode of the first m keys (one oracle_decode_span call), encode of the
+    # first me keys
+    m = min(n, 1 << 25)
+    t0 = time.perf_counter()
+    part = orc.decode_span(blob, 0, m)
+    t_st = time.perf_counter() - t0
+    assert np.array_equal(part, keys[:m])
+    me = min(n, 20_000_000)
+    t0 = time.perf_counter()
+    orc.encode(keys[:me], _spec(cid).eps)
+    t_est = time.perf_counter() - t0
+    return {"value": alg / t / 1e9, "unit": "GB/s", "cores": nt, "kind": "oracle",
+            "sample": f"oracle_decode_mt of the full {_workload_name(cid)} (median of {reps}); "
+                      f"single thread: oracle_decode_span of the first {m} keys, oracle_encode "
+                      f"of the first {me} keys",
+            "keys_per_s": n / t,
+            "single_thread": {"decode_keys_per_s": m / t_st,
+                              "decode_GBps": (len(blob) * m / n + m * w) / t_st / 1e9,
+                              "encode_keys_per_s": me / t_est, "cores": 1},
+            "product_encode_keys_per_s": n / t_enc_product}
 
 
 def _cpu_rows(blob, keys, idx, rs, a_keys, probes):
@@ -227,12 +279,17 @@ def _cpu_rows(blob, keys, idx, rs, a_keys, probes):
     }
 
 
-def _time_launches(fn, stream, steps, warmup):
-    """W untimed + K timed launches of fn on `stream`; per-launch CUDA events. Returns
-    (total seconds of the timed region, per-launch seconds list)."""
+def _time_launches(fn, stream, steps, warmup, ws=1):
+    """W untimed + K timed calls of fn on `stream`, bracketed by a barrier (ws > 1) and a
+    device synchronize on both sides; per-call CUDA events on `stream`.  Returns (seconds of
+    the timed region on this rank, per-call seconds list)."""
     import torch
+    import torch.distributed as dist
     for _ in range(warmup):
         fn()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     evs[0].record(stream)
@@ -240,16 +297,242 @@ def _time_launches(fn, stream, steps, warmup):
         fn()
         evs[k + 1].record(stream)
     torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
     per = [evs[k].elapsed_time(evs[k + 1]) / 1e3 for k in range(steps)]
     return evs[0].elapsed_time(evs[-1]) / 1e3, per
 
 
+def _free_block(keys, dev, stream, reps, peak):
+    """NEXT-3: the config-2 keys under FORMAT F7 (free-intercept segments), same kernels."""
+    import torch
+
+    from paper_2412_10770_b200 import lc
+    n, w = keys.size, 8
+    t0 = time.perf_counter()
+    blob_a = lc.encode(keys, 127)
+    t_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    blob_f = lc.encode(keys, 127, free=True)
+    t_encf = time.perf_counter() - t0
+    ha, hf = lc.header(blob_a), lc.header(blob_f)
+    view_a, view_f = lc.View(blob_a, device=dev), lc.View(blob_f, device=dev)
+    out = view_f.out_tensor(n)
+    alg_f, alg_a = len(blob_f) + n * w, len(blob_a) + n * w
+    frng = np.random.default_rng(77)
+    d_fi = torch.from_numpy(frng.integers(0, n, 10_000_000).astype(np.int64)).to(dev)
+    fa_out = torch.empty(d_fi.numel(), dtype=out.dtype, device=dev)
+    d_fx = torch.from_numpy(frng.integers(0, int(keys[-1]), 10_000_000, dtype=np.uint64)
+                            .view(np.int64)).to(dev)
+    f_idx = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
+    f_key = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        _, pa = _time_launches(lambda: lc.decode(view_a, out, stream=stream), stream, reps, 3)
+        _, pf = _time_launches(lambda: lc.decode(view_f, out, stream=stream), stream, reps, 3)
+        _, pfa = _time_launches(lambda: lc.access(view_f, d_fi, fa_out, stream=stream),
+                                stream, reps, 2)
+        _, pfn = _time_launches(lambda: lc.next_geq(view_f, d_fx, f_idx, f_key, stream=stream),
+                                stream, reps, 2)
+        _, pan = _time_launches(lambda: lc.next_geq(view_a, d_fx, f_idx, f_key, stream=stream),
+                                stream, reps, 2)
+    ref = _ref_dev(keys, dev)
+    ok_f = torch.equal(out, ref) and torch.equal(fa_out, ref[d_fi])
+    del ref
+    if not ok_f:
+        raise SystemExit("F7 decode/access mismatch")
+    kf, ka = statistics.mean(pf), statistics.mean(pa)
+    return {
+        "workload": _workload_name(2),
+        "format": "FORMAT F7: free integer intercept (O'Rourke rule on the lattice), header "
+                  "flag 1, decode bias 0",
+        "segments": int(hf.n_seg), "segments_anchored": int(ha.n_seg),
+        "segment_reduction": 1 - hf.n_seg / ha.n_seg,
+        "blob_bytes": len(blob_f), "bits_per_int": 8 * len(blob_f) / n,
+        "ratio_r": len(blob_f) / (n * w),
+        "decode_GBps": alg_f / kf / 1e9, "decode_keys_per_s": n / kf,
+        "decode_GBps_anchored": alg_a / ka / 1e9, "decode_keys_per_s_anchored": n / ka,
+        "hbm_frac": alg_f / kf / 1e9 / peak,
+        "lookups_per_s": d_fi.numel() / statistics.mean(pfa),
+        "next_geq_per_s": d_fx.numel() / statistics.mean(pfn),
+        "next_geq_per_s_anchored": d_fx.numel() / statistics.mean(pan),
+        "encode_keys_per_s_host": n / t_encf, "encode_keys_per_s_host_anchored": n / t_enc,
+        "bit_exact": True,
+    }
+
+
+def _access_block(dev, stream, reps, no_cpu):
+    """Config 5: random access, range decodes, quantiles, successor search, intersection and
+    union (with and without the successor-search index), each verified."""
+    import torch
+
+    from paper_2412_10770_b200 import lc
+    from synth import make_queries
+    k5, idx, rs = make_queries()
+    b5 = lc.encode(k5, 127)
+    v5 = lc.View(b5, device=dev)
+    d_idx = torch.from_numpy(idx.view(np.int64)).to(dev)
+    a_out = torch.empty(idx.size, dtype=torch.int64, device=dev)
+    d_rs = torch.from_numpy(rs.view(np.int64)).to(dev)
+    r_out = torch.empty(rs.size * 64, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        _, pa = _time_launches(lambda: lc.access(v5, d_idx, a_out, stream=stream), stream, reps, 2)
+        _, pr = _time_launches(lambda: lc.range_decode(v5, d_rs, 64, r_out, stream=stream),
+                               stream, reps, 2)
+    d5 = torch.from_numpy(k5.view(np.int64)).to(dev)
+    ok_a = torch.equal(a_out, d5[d_idx])
+    sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
+    ok_r = torch.equal(r_out, d5[sel])
+    del d5, sel
+    if not (ok_a and ok_r):
+        raise SystemExit("access/range mismatch")
+    # NEXT-1 quantiles and NEXT-2 successor search / intersection / union on the same list
+    qrng = np.random.default_rng(55)
+    mq = 10_000_000
+    d_ranks = torch.from_numpy(qrng.integers(0, (1 << 32) - 1, mq, endpoint=True)
+                               .astype(np.uint64).view(np.int64)).to(dev)
+    q_out = torch.empty(mq, dtype=torch.int64, device=dev)
+    d_probe = torch.from_numpy(qrng.integers(0, int(k5[-1]), mq, dtype=np.uint64)
+                               .view(np.int64)).to(dev)
+    p_idx = torch.empty(mq, dtype=torch.int64, device=dev)
+    p_key = torch.empty(mq, dtype=torch.int64, device=dev)
+    na = 1_000_000
+    a_keys = np.unique(np.concatenate([
+        k5[np.sort(qrng.choice(k5.size, na // 2, replace=False))],
+        qrng.integers(0, int(k5[-1]), na // 2, dtype=np.uint64)]))
+    va = lc.View(lc.encode(a_keys, 127), device=dev)
+    i_scr = torch.empty(lc.intersect_scratch_bytes(va), dtype=torch.uint8, device=dev)
+    i_out = va.out_tensor(va.n)
+    i_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    u_scr = torch.empty(lc.union_scratch_bytes(va, v5), dtype=torch.uint8, device=dev)
+    u_out = va.out_tensor(va.n + v5.n)
+    u_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        _, pqe = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, True, q_out,
+                                                    stream=stream), stream, reps, 2)
+        _, pqa = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, False, q_out,
+                                                    stream=stream), stream, reps, 2)
+        _, png = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx, p_key, stream=stream),
+                                stream, reps, 2)
+        _, pis = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt, stream=stream),
+                                stream, reps, 2)
+        _, pun = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt, stream=stream),
+                                stream, reps, 2)
+    # the same three with the successor-search index attached to the long list
+    # (lc_search_index_build: a one-off device pass, timed separately)
+    idx_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    idx_buf = v5.build_search_index(stream=stream)  # warm-up (module load), then timed
+    with torch.cuda.stream(stream):
+        idx_ev[0].record(stream)
+        v5.build_search_index(stream=stream, out=idx_buf)
+        idx_ev[1].record(stream)
+    torch.cuda.synchronize()
+    idx_build_ms = idx_ev[0].elapsed_time(idx_ev[1])
+    p_idx2 = torch.empty_like(p_idx)
+    p_key2 = torch.empty_like(p_key)
+    with torch.cuda.stream(stream):
+        _, pngx = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx2, p_key2, stream=stream),
+                                 stream, reps, 2)
+        _, pisx = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt, stream=stream),
+                                 stream, reps, 2)
+        _, punx = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt, stream=stream),
+                                 stream, reps, 2)
+    if not (torch.equal(p_idx2, p_idx) and torch.equal(p_key2, p_key)):
+        raise SystemExit("indexed next_geq mismatch")
+    want_cnt = int(np.intersect1d(a_keys, k5, assume_unique=True).size)
+    if int(i_cnt.item()) != want_cnt:
+        raise SystemExit("intersection count mismatch")
+    if int(u_cnt.item()) != a_keys.size + k5.size - want_cnt:
+        raise SystemExit("union count mismatch")
+    cpu_rows = None
+    if not no_cpu:
+        cpu_rows = _cpu_rows(b5, k5, idx, rs, a_keys,
+                             d_probe[:2_000_000].cpu().numpy().view(np.uint64))
+    return {
+        "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
+                    "lookups; 1e7 ranges x 64 keys",
+        "cpu_oracle": cpu_rows,
+        "lookups_per_s": idx.size / statistics.mean(pa),
+        "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
+        "ranges_per_s": rs.size / statistics.mean(pr),
+        "range_keys_per_s": rs.size * 64 / statistics.mean(pr),
+        "range_out_GBps": rs.size * 64 * 8 / statistics.mean(pr) / 1e9,
+        "quantiles_exact_per_s": mq / statistics.mean(pqe),
+        "quantiles_approx_per_s": mq / statistics.mean(pqa),
+        "next_geq_per_s": mq / statistics.mean(png),
+        "intersect": {"a_keys": int(a_keys.size), "b_keys": int(k5.size),
+                      "matches": want_cnt, "ms": statistics.mean(pis) * 1e3,
+                      "a_keys_per_s": a_keys.size / statistics.mean(pis)},
+        "union": {"keys_out": int(u_cnt.item()), "ms": statistics.mean(pun) * 1e3,
+                  "out_keys_per_s": int(u_cnt.item()) / statistics.mean(pun)},
+        "search_index": {"bytes": int(v5.d_first.numel() * 8), "build_ms": idx_build_ms,
+                         "next_geq_per_s": mq / statistics.mean(pngx),
+                         "intersect_ms": statistics.mean(pisx) * 1e3,
+                         "union_ms": statistics.mean(punx) * 1e3},
+        "bit_exact": True,
+        "blob_bytes": len(b5),
+    }
+
+
+def _ref_dev(keys, dev):
+    import torch
+    return torch.from_numpy(keys.view(np.int64) if keys.dtype.itemsize == 8
+                            else keys.view(np.int32)).to(dev)
+
+
+def _sync_barrier(ws):
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(x, ws, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _decode_config(cid, keys, dev, stream, steps, warmup, peak):
+    """One extra full-decode line (configs 2 / 3 beside the headline): GB/s, keys/s, fraction
+    of the HBM peak, every key verified on device."""
+    import torch
+
+    from paper_2412_10770_b200 import lc
+    spec = _spec(cid)
+    n, w = keys.size, spec.key_bits // 8
+    blob = lc.encode(keys, spec.eps)
+    h = lc.header(blob)
+    view = lc.View(blob, device=dev)
+    out = view.out_tensor(n)
+    alg = len(blob) + n * w
+    with torch.cuda.stream(stream):
+        total, per = _time_launches(lambda: lc.decode(view, out, stream=stream), stream, steps,
+                                    warmup)
+    ref = _ref_dev(keys, dev)
+    ok = bool(torch.equal(out, ref))
+    del ref, out, view
+    if not ok:
+        raise SystemExit(f"config {cid}: decoded keys differ from the input keys")
+    kern = statistics.mean(per)
+    return {"workload": _workload_name(cid), "n": n, "segments": int(h.n_seg),
+            "blob_bytes": len(blob), "bytes_per_step": alg, "ms_per_step": total / steps * 1e3,
+            "GBps": alg * steps / total / 1e9, "keys_per_s": n * steps / total,
+            "frac": alg * steps / total / 1e9 / peak, "kernel_GBps": alg / kern / 1e9,
+            "kernel": _kernel_name(h), "traffic": _ncu_traffic(cid), "bit_exact": ok}
+
+
 def run_gpu(args):
+    import concurrent.futures as cf
+
     import torch
     import torch.distributed as dist
 
-    from paper_2412_10770_b200 import lc
-    from synth import make_keys, make_queries
+    from paper_2412_10770_b200 import lc, shard
+    from synth import make_keys
 
     ws, rank, local = _env_dist()
     torch.cuda.set_device(local)
@@ -259,8 +542,14 @@ def run_gpu(args):
     stream = torch.cuda.Stream(dev)
     cid = args.config
     spec = _spec(cid)
+    peak, peak_src = _peaks()
+    extra = [c for c in (2, 3, 4) if c != cid] if ws == 1 and not args.no_configs else []
+    # the next configs' keys are generated on a host thread while the GPU runs (numpy's
+    # generators and sort release the GIL); the CPU baselines run after it finished
+    pool = cf.ThreadPoolExecutor(1)
+    pending = {c: pool.submit(make_keys, c) for c in extra[:1]}
 
-    # ---- inputs (host generation + host encode: not timed)
+    # ---- headline: inputs (host generation + host encode: not timed)
     keys = make_keys(cid)
     n = keys.size
     w = spec.key_bits // 8
@@ -268,233 +557,121 @@ def run_gpu(args):
     blob = lc.encode(keys, spec.eps)
     t_enc = time.perf_counter() - t_enc
     h = lc.header(blob)
-    view = lc.View(blob, device=dev)
-    out = view.out_tensor(n)
-    alg_bytes = len(blob) + n * w  # compressed read once + keys written once
+    alg_bytes = len(blob) + n * w  # the whole list: compressed read once + keys written once
+    h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
+    if ws == 1:
+        view, (i0, i1) = lc.View(blob, device=dev), (0, n)
+    else:  # this rank holds and decodes only its shard (lc_shard_upload)
+        view, (i0, i1) = shard.upload_shard(h_blob, rank, ws, device=dev, stream=stream)
+    span = i1 - i0
+    shard_bytes = 0 if view is None else view.d_blob.numel()
+    rank_bytes = (shard_bytes if ws > 1 else len(blob)) + span * w
+    out = torch.empty(max(span, 1), dtype=torch.int64 if w == 8 else torch.int32, device=dev)
 
     def step():
-        lc.decode(view, out, stream=stream)
+        if view is not None:
+            lc.decode(view, out, stream=stream)
 
-    peak, peak_src = _peaks()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    _sync_barrier(ws)
     c0 = lc.launch_count()
-    with ClockSampler(local) as clk, torch.cuda.stream(stream):
-        total, per = _time_launches(step, stream, args.steps, args.warmup)
-    launches = lc.launch_count() - c0 - args.warmup
-    if ws > 1:
-        dist.barrier()
-    t = torch.tensor([total], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
-    # correctness of what was timed: every key, on device, against the generator's array
-    ref = torch.from_numpy(keys.view(np.int64) if w == 8 else keys.view(np.int32)).to(dev)
-    ok = torch.equal(out, ref)
-    del ref
-    if not ok:
-        raise SystemExit(f"rank {rank}: decoded keys differ from the input keys")
+    with torch.cuda.stream(stream):
+        with ClockSampler(local) as clk:
+            total, per = _time_launches(step, stream, args.steps, args.warmup, ws)
+        launches = lc.launch_count() - c0 - args.warmup * (view is not None)
+        t_max = _max_over_ranks(total, ws, dev)
+        # correctness of what was timed: every key of the span, on device
+        ref = _ref_dev(keys[i0:i1], dev)
+        ok = span == 0 or bool(torch.equal(out[:span], ref))
+        del ref
+        if not ok:
+            raise SystemExit(f"rank {rank}: decoded keys differ from the input keys")
+        ms = t_max / args.steps * 1e3
+        value = alg_bytes * args.steps / t_max / 1e9
+        kern = statistics.mean(per) if per else float("nan")
+        achieved = rank_bytes / kern / 1e9
 
-    ms = t_max / args.steps * 1e3
-    value = ws * alg_bytes * args.steps / t_max / 1e9
-    kern = statistics.mean(per)
-    achieved = alg_bytes / kern / 1e9
+        # ---- end to end through the C ABI with host buffers (pinned), copies inside the
+        # timed region: lc_decode_host (1 GPU) or shard upload + decode + D2H of the span
+        h_out = torch.empty(max(span, 1), dtype=out.dtype).pin_memory()
+        e2e_steps = max(1, min(args.steps, 5))
+        if ws == 1:
+            d_blob = torch.empty(len(blob), dtype=torch.uint8, device=dev)
 
-    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
-    h_blob = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory()
-    d_blob = torch.empty(len(blob), dtype=torch.uint8, device=dev)
-    h_out = torch.empty(n, dtype=out.dtype).pin_memory()
-    e2e_steps = max(1, min(args.steps, 5))
+            def e2e_step():
+                lc.decode_host(h_blob, d_blob, out, h_out, stream=stream)
+            api = "lc_decode_host (pinned host blob -> device -> decode -> pinned host keys)"
+            h2d = len(blob)
+        else:
+            d_blob = torch.empty(max(shard_bytes, 1), dtype=torch.uint8, device=dev)
 
-    def e2e_step():
-        lc.decode_host(h_blob, d_blob, out, h_out, stream=stream)
-
-    e2e_total, _ = _time_launches(e2e_step, stream, e2e_steps, 1)
-    if not np.array_equal(h_out.numpy().view(keys.dtype), keys):
+            def e2e_step():
+                if span:
+                    sv = lc.View.shard(h_blob, i0, i1, device=dev, stream=stream, out=d_blob)
+                    lc.decode(sv, out, stream=stream)
+                    h_out[:span].copy_(out[:span], non_blocking=True)
+            api = ("lc_shard_upload (pinned host blob slices of the rank's span -> device) + "
+                   "lc_decode + D2H of the span's keys")
+            h2d = shard_bytes
+        _sync_barrier(ws)
+        e2e_total, _ = _time_launches(e2e_step, stream, e2e_steps, 1, ws)
+    if not np.array_equal(h_out.numpy()[:span].view(keys.dtype), keys[i0:i1]):
         raise SystemExit("e2e decode mismatch")
-    e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = ws * alg_bytes * e2e_steps / float(e2e_t.item()) / 1e9
+    e2e_t = _max_over_ranks(e2e_total, ws, dev)
+    h2d_all = h2d
+    if ws > 1:  # bytes every rank uploads per step (its shard)
+        tt = torch.tensor([float(h2d)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt)
+        h2d_all = int(tt.item())
+    e2e_value = alg_bytes * e2e_steps / e2e_t / 1e9
     # PCIe ceiling of the same transfers: plain pinned copies, each direction alone
-    cp_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    cp_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     with torch.cuda.stream(stream):
         for _ in range(2):
             cp_ev[0].record(stream)
-            d_blob.copy_(h_blob, non_blocking=True)
+            d_blob[:h2d].copy_(h_blob[:h2d], non_blocking=True)
             cp_ev[1].record(stream)
             h_out.copy_(out, non_blocking=True)
             cp_ev[2].record(stream)
     torch.cuda.synchronize()
-    h2d_gbps = len(blob) / (cp_ev[0].elapsed_time(cp_ev[1]) * 1e-3) / 1e9
-    d2h_gbps = n * w / (cp_ev[1].elapsed_time(cp_ev[2]) * 1e-3) / 1e9
-    e2e_floor_ms = max(len(blob) / h2d_gbps, n * w / d2h_gbps) / 1e6  # full-duplex overlap
-    del h_blob, d_blob, h_out
+    h2d_gbps = h2d / max(cp_ev[0].elapsed_time(cp_ev[1]) * 1e-3, 1e-9) / 1e9
+    d2h_gbps = span * w / max(cp_ev[1].elapsed_time(cp_ev[2]) * 1e-3, 1e-9) / 1e9
+    e2e_floor_ms = max(h2d / max(h2d_gbps, 1e-9), span * w / max(d2h_gbps, 1e-9)) / 1e6
+    del d_blob, h_out, out, view
 
-    # ---- NEXT-3: the same keys under FORMAT F7 (free-intercept segments), same kernels
+    # ---- configs 2 / 3 (the other >= 1e8-key configs of the north-star target), 1 GPU
+    decode_configs = {}
+    if ws == 1:
+        decode_configs[f"config{cid}"] = {
+            "workload": _workload_name(cid), "n": n, "segments": int(h.n_seg),
+            "blob_bytes": len(blob), "bytes_per_step": alg_bytes, "ms_per_step": ms,
+            "GBps": value, "keys_per_s": n * args.steps / t_max, "frac": value / peak,
+            "kernel_GBps": achieved, "kernel": _kernel_name(h), "traffic": _ncu_traffic(cid),
+            "bit_exact": True}
+    cfg_steps = max(3, min(args.steps, 20))
+    keys2 = keys if cid == 2 else None
+    for k, c in enumerate(extra):
+        kc = pending.pop(c).result()
+        if c == 2:
+            keys2 = kc
+        if k + 1 < len(extra):
+            pending[extra[k + 1]] = pool.submit(make_keys, extra[k + 1])
+        with ClockSampler(local) as clk_c:
+            decode_configs[f"config{c}"] = _decode_config(c, kc, dev, stream, cfg_steps, 3, peak)
+        decode_configs[f"config{c}"]["clocks"] = clk_c.summary()
+        del kc
+    pool.shutdown()
+
+    # ---- NEXT-3: config 2 under FORMAT F7 (free-intercept segments), same kernels
     free = None
-    if not args.no_free:
-        t_encf = time.perf_counter()
-        blob_f = lc.encode(keys, spec.eps, free=True)
-        t_encf = time.perf_counter() - t_encf
-        hf = lc.header(blob_f)
-        view_f = lc.View(blob_f, device=dev)
-        alg_f = len(blob_f) + n * w
-        reps = max(5, min(args.steps, 50))
-        with torch.cuda.stream(stream):
-            tf, pf = _time_launches(lambda: lc.decode(view_f, out, stream=stream), stream, reps, 3)
-        ref = torch.from_numpy(keys.view(np.int64) if w == 8 else keys.view(np.int32)).to(dev)
-        ok_f = torch.equal(out, ref)
-        frng = np.random.default_rng(77)
-        d_fi = torch.from_numpy(frng.integers(0, n, 10_000_000).astype(np.int64)).to(dev)
-        fa_out = torch.empty(d_fi.numel(), dtype=out.dtype, device=dev)
-        d_fx = torch.from_numpy(frng.integers(0, int(keys[-1]), 10_000_000, dtype=np.uint64)
-                                .view(np.int64)).to(dev)
-        f_idx = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
-        f_key = torch.empty(d_fx.numel(), dtype=torch.int64, device=dev)
-        with torch.cuda.stream(stream):
-            _, pfa = _time_launches(lambda: lc.access(view_f, d_fi, fa_out, stream=stream),
-                                    stream, reps, 2)
-            _, pfn = _time_launches(lambda: lc.next_geq(view_f, d_fx, f_idx, f_key,
-                                                        stream=stream), stream, reps, 2)
-            _, pan = _time_launches(lambda: lc.next_geq(view, d_fx, f_idx, f_key,
-                                                        stream=stream), stream, reps, 2)
-        ok_f = ok_f and torch.equal(fa_out, ref[d_fi])
-        del ref
-        if not ok_f:
-            raise SystemExit("F7 decode/access mismatch")
-        kf = statistics.mean(pf)
-        free = {
-            "format": "FORMAT F7: free integer intercept (O'Rourke rule on the lattice), "
-                      "header flag 1, decode bias 0",
-            "segments": int(hf.n_seg), "segments_anchored": int(h.n_seg),
-            "segment_reduction": 1 - hf.n_seg / h.n_seg,
-            "blob_bytes": len(blob_f), "bits_per_int": 8 * len(blob_f) / n,
-            "ratio_r": len(blob_f) / (n * w),
-            "decode_GBps": alg_f / kf / 1e9, "decode_keys_per_s": n / kf,
-            "decode_keys_per_s_anchored": n / kern, "hbm_frac": alg_f / kf / 1e9 / peak,
-            "lookups_per_s": d_fi.numel() / statistics.mean(pfa),
-            "next_geq_per_s": d_fx.numel() / statistics.mean(pfn),
-            "next_geq_per_s_anchored": d_fx.numel() / statistics.mean(pan),
-            "encode_keys_per_s_host": n / t_encf, "encode_keys_per_s_host_anchored": n / t_enc,
-            "bit_exact": True,
-        }
-        del view_f, d_fi, fa_out, d_fx, f_idx, f_key
+    if ws == 1 and not args.no_free:
+        free = _free_block(keys2 if keys2 is not None else make_keys(2), dev, stream,
+                           max(5, min(args.steps, 50)), peak)
+    del keys2
 
     # ---- random access + range decodes (config 5), reported beside the headline
     access = None
-    if not args.no_access:
-        k5, idx, rs = make_queries()
-        b5 = lc.encode(k5, 127)
-        v5 = lc.View(b5, device=dev)
-        d_idx = torch.from_numpy(idx.view(np.int64)).to(dev)
-        a_out = torch.empty(idx.size, dtype=torch.int64, device=dev)
-        d_rs = torch.from_numpy(rs.view(np.int64)).to(dev)
-        r_out = torch.empty(rs.size * 64, dtype=torch.int64, device=dev)
-        with torch.cuda.stream(stream):
-            ta, pa = _time_launches(lambda: lc.access(v5, d_idx, a_out, stream=stream), stream,
-                                    max(3, min(args.steps, 20)), 2)
-            tr, pr = _time_launches(lambda: lc.range_decode(v5, d_rs, 64, r_out, stream=stream),
-                                    stream, max(3, min(args.steps, 20)), 2)
-        d5 = torch.from_numpy(k5.view(np.int64)).to(dev)
-        ok_a = torch.equal(a_out, d5[d_idx])
-        sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
-        ok_r = torch.equal(r_out, d5[sel])
-        del d5, sel
-        # NEXT-1 quantiles and NEXT-2 successor search / intersection on the same list
-        qrng = np.random.default_rng(55)
-        mq = 10_000_000
-        d_ranks = torch.from_numpy(qrng.integers(0, (1 << 32) - 1, mq, endpoint=True)
-                                   .astype(np.uint64).view(np.int64)).to(dev)
-        q_out = torch.empty(mq, dtype=torch.int64, device=dev)
-        d_probe = torch.from_numpy(qrng.integers(0, int(k5[-1]), mq, dtype=np.uint64)
-                                   .view(np.int64)).to(dev)
-        p_idx = torch.empty(mq, dtype=torch.int64, device=dev)
-        p_key = torch.empty(mq, dtype=torch.int64, device=dev)
-        na = 1_000_000
-        a_keys = np.unique(np.concatenate([
-            k5[np.sort(qrng.choice(k5.size, na // 2, replace=False))],
-            qrng.integers(0, int(k5[-1]), na // 2, dtype=np.uint64)]))
-        va = lc.View(lc.encode(a_keys, 127), device=dev)
-        i_scr = torch.empty(lc.intersect_scratch_bytes(va), dtype=torch.uint8, device=dev)
-        i_out = va.out_tensor(va.n)
-        i_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        u_scr = torch.empty(lc.union_scratch_bytes(va, v5),
-                            dtype=torch.uint8, device=dev)
-        u_out = va.out_tensor(va.n + v5.n)
-        u_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        reps = max(3, min(args.steps, 20))
-        with torch.cuda.stream(stream):
-            _, pqe = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, True, q_out,
-                                                        stream=stream), stream, reps, 2)
-            _, pqa = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, False, q_out,
-                                                        stream=stream), stream, reps, 2)
-            _, png = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx, p_key, stream=stream),
-                                    stream, reps, 2)
-            _, pis = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt,
-                                                         stream=stream), stream, reps, 2)
-            _, pun = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt,
-                                                     stream=stream), stream, reps, 2)
-        # the same three with the successor-search index attached to the long list
-        # (lc_search_index_build: a one-off device pass, timed separately)
-        idx_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        idx_buf = v5.build_search_index(stream=stream)  # warm-up (module load), then timed
-        with torch.cuda.stream(stream):
-            idx_ev[0].record(stream)
-            v5.build_search_index(stream=stream, out=idx_buf)
-            idx_ev[1].record(stream)
-        torch.cuda.synchronize()
-        idx_build_ms = idx_ev[0].elapsed_time(idx_ev[1])
-        p_idx2 = torch.empty_like(p_idx)
-        p_key2 = torch.empty_like(p_key)
-        with torch.cuda.stream(stream):
-            _, pngx = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx2, p_key2,
-                                                         stream=stream), stream, reps, 2)
-            _, pisx = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt,
-                                                          stream=stream), stream, reps, 2)
-            _, punx = _time_launches(lambda: lc.union(va, v5, u_scr, u_out, u_cnt,
-                                                      stream=stream), stream, reps, 2)
-        if not (torch.equal(p_idx2, p_idx) and torch.equal(p_key2, p_key)):
-            raise SystemExit("indexed next_geq mismatch")
-        want_cnt = int(np.intersect1d(a_keys, k5, assume_unique=True).size)
-        if int(i_cnt.item()) != want_cnt:
-            raise SystemExit("intersection count mismatch")
-        if int(u_cnt.item()) != a_keys.size + k5.size - want_cnt:
-            raise SystemExit("union count mismatch")
-        cpu_rows = None
-        if ws == 1 and not args.no_cpu:
-            cpu_rows = _cpu_rows(b5, k5, idx, rs, a_keys,
-                                 d_probe[:2_000_000].cpu().numpy().view(np.uint64))
-        access = {
-            "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
-                        "lookups; 1e7 ranges x 64 keys",
-            "cpu_oracle": cpu_rows,
-            "quantiles_exact_per_s": mq / statistics.mean(pqe),
-            "quantiles_approx_per_s": mq / statistics.mean(pqa),
-            "next_geq_per_s": mq / statistics.mean(png),
-            "intersect": {"a_keys": int(a_keys.size), "b_keys": int(k5.size),
-                          "matches": want_cnt, "ms": statistics.mean(pis) * 1e3,
-                          "a_keys_per_s": a_keys.size / statistics.mean(pis)},
-            "union": {"keys_out": int(u_cnt.item()), "ms": statistics.mean(pun) * 1e3,
-                      "out_keys_per_s": int(u_cnt.item()) / statistics.mean(pun)},
-            "search_index": {"bytes": int(v5.d_first.numel() * 8), "build_ms": idx_build_ms,
-                             "next_geq_per_s": mq / statistics.mean(pngx),
-                             "intersect_ms": statistics.mean(pisx) * 1e3,
-                             "union_ms": statistics.mean(punx) * 1e3},
-            "lookups_per_s": ws * idx.size / statistics.mean(pa),
-            "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
-            "ranges_per_s": ws * rs.size / statistics.mean(pr),
-            "range_keys_per_s": ws * rs.size * 64 / statistics.mean(pr),
-            "range_out_GBps": rs.size * 64 * 8 / statistics.mean(pr) / 1e9,
-            "bit_exact": bool(ok_a and ok_r),
-            "blob_bytes": len(b5),
-        }
-        if not (ok_a and ok_r):
-            raise SystemExit("access/range mismatch")
-        del v5, d_idx, a_out, d_rs, r_out, va, i_scr, i_out, d_ranks, q_out, d_probe, p_idx, p_key
-        del p_idx2, p_key2
-        del u_scr, u_out
+    if ws == 1 and not args.no_access:
+        access = _access_block(dev, stream, max(3, min(args.steps, 20)), args.no_cpu)
 
     if ws > 1:
         dist.barrier()
@@ -502,42 +679,35 @@ def run_gpu(args):
         if ws > 1:
             dist.destroy_process_group()
         return
-    t_cpu, cores = _cpu_baseline(blob, keys) if ws == 1 and not args.no_cpu else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64" if w == 8 else "u32", "data": "synthetic",
-        "config": {"workload": _workload_name(cid), "n": n, "key_bits": spec.key_bits,
-                   "eps": spec.eps, "res_bits": int(h.res_bits), "segments": int(h.n_seg),
-                   "blob_bytes": len(blob), "bits_per_int": 8 * len(blob) / n,
-                   "ratio_r": len(blob) / (n * w), "bytes_per_step": alg_bytes,
-                   "l2": "no flush: every step reads+writes %.2f GB >> 126 MB L2" % (alg_bytes / 1e9),
-                   "parallelism": f"replica x{ws} (weak)"},
-        "keys_per_s": ws * n * args.steps / t_max,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None,
+        "dtype": "u64" if w == 8 else "u32", "data": "synthetic",
+        "config": _config_dict(cid, n, len(blob), int(h.n_seg), int(h.res_bits), ws),
+        "keys_per_s": n * args.steps / t_max,
         "hbm_frac": value / ws / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _ncu_traffic(cid),
+                     "frac": achieved / peak, "traffic": _ncu_traffic(cid) if ws == 1 else None,
                      "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes of one "
-                                       "ncu --set full launch; L2 keeps part of the output dirty "
-                                       "at kernel end)",
-                     "kernel": "lc_decode_kernel<true>", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_bytes},
-        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": len(blob),
-                "d2h_bytes_per_step": n * w, "api": "lc_decode_host (pinned host blob -> "
-                "device -> decode -> pinned host keys)",
-                "ms_per_step": float(e2e_t.item()) / e2e_steps * 1e3,
+                                       "ncu --set full launch of this config's decode)",
+                     "kernel": _kernel_name(h), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": rank_bytes,
+                     "algorithmic_bytes": "blob bytes read once + N * key bytes written once "
+                                          "(rank 0's shard under --gpus > 1)"},
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d_all,
+                "d2h_bytes_per_step": n * w, "api": api,
+                "ms_per_step": e2e_t / e2e_steps * 1e3,
                 "pcie_h2d_GBps": h2d_gbps, "pcie_d2h_GBps": d2h_gbps,
                 "pcie_floor_ms": e2e_floor_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "decode_configs": decode_configs or None,
         "access": access,
         "free_intercept": free,
     }
-    if t_cpu is not None:
-        line["cpu_baseline"] = {
-            "value": alg_bytes / t_cpu / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"oracle_decode_mt of the full {_workload_name(cid)} (median of 3)",
-            "keys_per_s": n / t_cpu}
+    if ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = _cpu_baseline(cid, blob, keys, t_enc)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -549,7 +719,10 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="headline workload (default: config 4, the largest)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the decode_configs lines of the other 1e8+ configs")
     ap.add_argument("--no-access", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-free", action="store_true", help="skip the FORMAT F7 block")

@@ -38,7 +38,7 @@ def test_reference_arm_line():
 @pytest.mark.gpu
 def test_product_arm_line():
     d = _run("--config", "1", "--steps", "5", "--warmup", "3", "--no-access", "--no-cpu",
-             "--no-free")
+             "--no-free", "--no-configs")
     assert BASE_KEYS - {"cpu_baseline"} <= set(d)
     assert {"roofline", "gpu_launches", "clocks"} <= set(d)
     assert d["value"] > 0 and d["gpu_launches"] >= d["steps"]
@@ -48,3 +48,7 @@ def test_product_arm_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 4_000_000
     assert d["dtype"] == "u32" and d["config"]["n"] == 1_000_000
+    assert d["roofline"]["kernel"].startswith("lc_decode_kernel<0,7,")
+    # both arms name the same workload with the same config dict
+    r = _run("--impl", "reference", "--config", "1", "--steps", "2", "--warmup", "3")
+    assert r["config"] == d["config"]
