@@ -15,6 +15,7 @@ struct Sections {
     const uint32_t* hint;
     const uint32_t* words;
     const uint64_t* first;  // optional successor-search index (lc_view.d_first), may be null
+    const ulonglong2* acc;  // optional access layout (lc_view.d_acc), may be null
     uint32_t L;  // segments (bound of params)
     uint64_t W;  // residual words (bound of words; up to 2^32 + 4 at N = 2^32 - 1, b = 32)
 };
@@ -36,6 +37,7 @@ Sections sections_of(const lc_view* v) {
         s.words = (const uint32_t*)(B + v->h.off_words);
     }
     s.first = v->d_first;
+    s.acc = (const ulonglong2*)v->d_acc;
     s.L = (uint32_t)v->h.n_seg;
     s.W = v->h.n_words;
     return s;

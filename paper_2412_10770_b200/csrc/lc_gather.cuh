@@ -329,13 +329,40 @@ __host__ __device__ constexpr uint32_t access_per_thread(int mode) {
     return mode == kQuantileApprox ? 1 : 2;
 }
 
+// Access layout (lc_access_layout_build): record j starts at 16-byte unit 2 j + floor(s_j b / 128)
+// and holds {base_j, slope_j} followed by the residual units floor(s_j b / 128) ..
+// floor(s_{j+1} b / 128) (every unit of the words section that holds a bit of the segment's
+// keys).  The offset needs only j and s_j, both known after the search: no offset array.
+__host__ __device__ __forceinline__ uint64_t acc_unit(uint32_t j, uint32_t s, uint32_t b) {
+    return 2 * (uint64_t)j + (((uint64_t)s * b) >> 7);
+}
+
+// One warp per segment (grid-stride): copy params[j] and the segment's residual units.
+__global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, ulonglong2* acc,
+                                                           uint32_t b) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * 8;
+    const ulonglong2* W16 = (const ulonglong2*)sec.words;  // 16-byte units of the words
+    for (uint32_t j = blockIdx.x * 8 + (threadIdx.x >> 5); j < sec.L; j += nw) {
+        const uint32_t s0 = __ldg(sec.starts + j), s1 = __ldg(sec.starts + j + 1);
+        const uint64_t u0 = ((uint64_t)s0 * b) >> 7, u1 = ((uint64_t)s1 * b) >> 7;
+        ulonglong2* rec = acc + acc_unit(j, s0, b);
+        if (lane == 0) rec[0] = __ldg(sec.params + j);
+        for (uint64_t u = u0 + lane; u <= u1; u += 32)
+            rec[1 + (u - u0)] = __ldg(W16 + LC_BOUND(true, u, (sec.W + 3) / 4));
+    }
+}
+
 // Dec(K^c)[i] per query (Table I): hint bracket, binary search
 // over starts, one params gather, one residual field.  Each thread serves access_per_thread()
 // queries whose dependent load chains are interleaved; the residual words do not depend on
 // the segment and are fetched before the search.  Quantiles use the same
 // path with i = min(floor(N k / q), N - 1): exact = f(i) + Delta[i]; approximate = floor(f(i))
 // from the segment alone, no residual read, error <= eps, saturated at the key width (L24).
-template <bool K64, int MODE>
+// ACC (access layout attached): after the search, params and the residual field come from
+// the segment's record (one DRAM line in most lookups) instead of the params and words
+// sections (two independent gathers).
+template <bool K64, int MODE, bool ACC = false>
 __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
     constexpr bool kResidual = MODE != kQuantileApprox;
     constexpr uint32_t kAccessPerThread = access_per_thread(MODE);
@@ -371,7 +398,7 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         if (live[k]) {
             lo[k] = ldh(sec.hint + (i[k] >> 10), keep);
             hi[k] = ldh(sec.hint + (i[k] >> 10) + 1, keep);
-            if (kResidual && a.b) w[k] = field_words(sec, i[k], a.b, once);
+            if (!ACC && kResidual && a.b) w[k] = field_words(sec, i[k], a.b, once);
         }
     }
     for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
@@ -395,22 +422,38 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
             }
         }
     }
+    uint32_t s[kAccessPerThread];
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) s[k] = live[k] ? ldh(sec.starts + lo[k], keep) : 0;
+    ulonglong2 pr[kAccessPerThread];
+#pragma unroll
+    for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        pr[k] = make_ulonglong2(0, 0);
+        if (!live[k]) continue;
+        if (ACC) {  // the record: params, then the residual units from floor(s b / 128)
+            const ulonglong2* rec = sec.acc + acc_unit(lo[k], s[k], a.b);
+            pr[k] = ldh(rec, once);
+            if (kResidual && a.b) {
+                const uint32_t p = (uint32_t)((uint64_t)i[k] * a.b - ((((uint64_t)s[k] * a.b) >> 7) << 7));
+                const uint32_t* wp = (const uint32_t*)(rec + 1) + (p >> 5);
+                w[k] = make_uint2(ldh(wp, once), ldh(wp + 1, once));
+            }
+        } else {
+            pr[k] = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
+        }
+    }
 #pragma unroll
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {
         if (!live[k]) continue;
-        const uint32_t s = ldh(sec.starts + lo[k], keep);
-        const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
         uint8_t* o = (uint8_t*)a.out + (t0 + 256 * k) * (K64 ? 8 : 4);
         if (kResidual) {
             const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
-            put<K64>(o, pr.x, pred_plus(pr.y, i[k] - s, u - a.bias));
+            put<K64>(o, pr[k].x, pred_plus(pr[k].y, i[k] - s[k], u - a.bias));
         } else {  // floor(f(i)) can exceed the key width by up to eps: saturate (L24)
             // floor(f(i)) = base + floor(slope d / 2^32) + (eps - bias): F7 bases sit eps below
-            const uint64_t f = pr.x + pred_plus(pr.y, i[k] - s, a.center);
-            if (K64) __stcs((unsigned long long*)o, f < pr.x ? ~0ull : (unsigned long long)f);
+            const uint64_t f = pr[k].x + pred_plus(pr[k].y, i[k] - s[k], a.center);
+            if (K64) __stcs((unsigned long long*)o, f < pr[k].x ? ~0ull : (unsigned long long)f);
             else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
         }
     }
 }
-
-

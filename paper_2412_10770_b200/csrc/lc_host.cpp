@@ -650,6 +650,7 @@ int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
     v->h = h;
     v->d_blob = d_blob;
     v->d_first = nullptr;
+    v->d_acc = nullptr;
     v->span_lo = v->span_hi = 0;
     std::memset(v->sec_base, 0, sizeof v->sec_base);
     return LC_OK;

@@ -258,14 +258,19 @@ int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const unsigned g = (unsigned)grid;
     const bool k64 = v->h.key_bits == 64;
+    const bool acc = v->d_acc != nullptr;  // access layout attached (approximate mode: params only)
     switch (mode) {
         case kAccess:
-            if (k64) lc_access_kernel<true, kAccess><<<g, 256, 0, st>>>(a);
-            else lc_access_kernel<false, kAccess><<<g, 256, 0, st>>>(a);
+            if (k64) acc ? lc_access_kernel<true, kAccess, true><<<g, 256, 0, st>>>(a)
+                         : lc_access_kernel<true, kAccess><<<g, 256, 0, st>>>(a);
+            else acc ? lc_access_kernel<false, kAccess, true><<<g, 256, 0, st>>>(a)
+                     : lc_access_kernel<false, kAccess><<<g, 256, 0, st>>>(a);
             break;
         case kQuantileExact:
-            if (k64) lc_access_kernel<true, kQuantileExact><<<g, 256, 0, st>>>(a);
-            else lc_access_kernel<false, kQuantileExact><<<g, 256, 0, st>>>(a);
+            if (k64) acc ? lc_access_kernel<true, kQuantileExact, true><<<g, 256, 0, st>>>(a)
+                         : lc_access_kernel<true, kQuantileExact><<<g, 256, 0, st>>>(a);
+            else acc ? lc_access_kernel<false, kQuantileExact, true><<<g, 256, 0, st>>>(a)
+                     : lc_access_kernel<false, kQuantileExact><<<g, 256, 0, st>>>(a);
             break;
         default:
             if (k64) lc_access_kernel<true, kQuantileApprox><<<g, 256, 0, st>>>(a);
@@ -412,6 +417,27 @@ int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream) {
     lc_detail::count_launch(1);
     const int32_t rc = cuda_status();
     if (!rc) v->d_first = (const uint64_t*)d_index;
+    return rc;
+}
+
+uint64_t lc_access_layout_bytes(const lc_view* v) {
+    if (!v) return 0;
+    return 16 * (2 * v->h.n_seg + ((v->h.n * v->h.res_bits) >> 7));
+}
+
+int32_t lc_access_layout_build(lc_view* v, void* d_layout, lc_stream stream) {
+    if (!v || !v->d_blob || is_shard(v) || !d_layout || ((uintptr_t)d_layout & 127)) return LC_ERR_ARG;
+    const Sections sec = sections_of(v);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (v->h.n_seg + 7) / 8;  // one warp per segment, 8 warps per CTA
+    const unsigned grid = (unsigned)(want < (uint64_t)sms * 16 ? want : (uint64_t)sms * 16);
+    lc_acc_build_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(sec, (ulonglong2*)d_layout,
+                                                                v->h.res_bits);
+    lc_detail::count_launch(1);
+    const int32_t rc = cuda_status();
+    if (!rc) v->d_acc = d_layout;
     return rc;
 }
 

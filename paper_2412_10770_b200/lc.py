@@ -42,7 +42,7 @@ assert C.sizeof(lc_header) == 128
 
 class lc_view(C.Structure):
     _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p),
-                ("span_lo", C.c_uint64), ("span_hi", C.c_uint64), ("sec_base", C.c_uint64 * 4)]
+                ("d_acc", C.c_void_p), ("span_lo", C.c_uint64), ("span_hi", C.c_uint64), ("sec_base", C.c_uint64 * 4)]
 
 
 _p, _u64, _u32, _i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32
@@ -63,6 +63,8 @@ _sig = {
     "lc_union_scratch_bytes": ([C.POINTER(lc_view), C.POINTER(lc_view)], _u64),
     "lc_search_index_bytes": ([C.POINTER(lc_view)], _u64),
     "lc_search_index_build": ([C.POINTER(lc_view), _p, _p], _i32),
+    "lc_access_layout_bytes": ([C.POINTER(lc_view)], _u64),
+    "lc_access_layout_build": ([C.POINTER(lc_view), _p, _p], _i32),
     "lc_union": ([C.POINTER(lc_view), C.POINTER(lc_view), _p, _u64, _p, _p, _p], _i32),
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_shard_bytes": ([_p, _u64, _u64, _u64, C.POINTER(_u64)], _i32),
@@ -202,6 +204,7 @@ class View:
             d_blob = torch.from_numpy(host.copy()).to(device)
         self.d_blob = d_blob
         self.d_first = None
+        self.d_acc = None
         self.v = lc_view()
         nbytes = host.nbytes if blob_bytes is None else int(blob_bytes)
         _check(_lib.lc_view_init(C.byref(self.v), host.ctypes.data, d_blob.data_ptr(), nbytes),
@@ -218,6 +221,7 @@ class View:
         _check(_lib.lc_shard_bytes(hp, hn, i0, i1, C.byref(nb)), "lc_shard_bytes")
         self = cls.__new__(cls)
         self.d_first = None
+        self.d_acc = None
         self._host_keep = keep
         with _On(stream) as on:
             if out is None:
@@ -277,9 +281,29 @@ class View:
                    "lc_search_index_build")
         return self.d_first
 
+    def access_layout_bytes(self) -> int:
+        return int(_lib.lc_access_layout_bytes(C.byref(self.v)))
+
+    def build_access_layout(self, stream=None, out=None):
+        """lc_access_layout_build: allocate the access layout (segment-major records: params
+        followed by the segment's residual units, 16 (2 L + N b / 128) bytes) on the blob's
+        device, build it on `stream` and attach it (access / exact quantiles then use it)."""
+        import torch
+        nbytes = self.access_layout_bytes()
+        with _On(stream, self.d_blob) as on:
+            if out is None:
+                out = torch.empty(max(nbytes // 8, 2), dtype=torch.int64,
+                                  device=self.d_blob.device)
+            if out.numel() * out.element_size() < nbytes:
+                raise ValueError("access layout buffer too small")
+            self.d_acc = on.use(out)
+            _check(_lib.lc_access_layout_build(C.byref(self.v), self.d_acc.data_ptr(),
+                                               on.handle), "lc_access_layout_build")
+        return self.d_acc
+
     def tensors(self):
         """Device tensors the view's calls read (for stream bookkeeping)."""
-        return (self.d_blob, self.d_first)
+        return (self.d_blob, self.d_first, getattr(self, "d_acc", None))
 
     def out_tensor(self, count: int):
         import torch
