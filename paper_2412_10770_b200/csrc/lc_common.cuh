@@ -15,7 +15,12 @@ struct Sections {
     const uint32_t* hint;
     const uint32_t* words;
     const uint64_t* first;  // optional successor-search index (lc_view.d_first), may be null
-    const ulonglong2* acc;  // optional access layout (lc_view.d_acc), may be null
+    // optional access layout (lc_view.d_acc, lc_access_layout_build), null when absent:
+    // per 1024-key block a bitmap of segment starts and per-word (rank, distance) entries,
+    // then the segment-major records
+    const uint32_t* dbits;
+    const uint32_t* dent;
+    const ulonglong2* acc;
     uint32_t L;  // segments (bound of params)
     uint64_t W;  // residual words (bound of words; up to 2^32 + 4 at N = 2^32 - 1, b = 32)
 };
@@ -37,7 +42,11 @@ Sections sections_of(const lc_view* v) {
         s.words = (const uint32_t*)(B + v->h.off_words);
     }
     s.first = v->d_first;
-    s.acc = (const ulonglong2*)v->d_acc;
+    const uint64_t H = v->h.n_hint - 1;
+    const uint8_t* A = (const uint8_t*)v->d_acc;
+    s.dbits = A ? (const uint32_t*)A : nullptr;
+    s.dent = A ? (const uint32_t*)(A + 128 * H) : nullptr;
+    s.acc = A ? (const ulonglong2*)(A + 256 * H) : nullptr;
     s.L = (uint32_t)v->h.n_seg;
     s.W = v->h.n_words;
     return s;

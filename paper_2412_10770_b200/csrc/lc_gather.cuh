@@ -329,15 +329,58 @@ __host__ __device__ constexpr uint32_t access_per_thread(int mode) {
     return mode == kQuantileApprox ? 1 : 2;
 }
 
-// Access layout (lc_access_layout_build): record j starts at 16-byte unit 2 j + floor(s_j b / 128)
-// and holds {base_j, slope_j} followed by the residual units floor(s_j b / 128) ..
-// floor(s_{j+1} b / 128) (every unit of the words section that holds a bit of the segment's
-// keys).  The offset needs only j and s_j, both known after the search: no offset array.
+// Access layout (lc_access_layout_build), three parts in one buffer:
+//  * dbits[32 h + w]: bit t set iff key 1024 h + 32 w + t starts a segment (block position 0
+//    excluded: the hint already names the segment holding key 1024 h);
+//  * dent[32 h + w] = rank | dist << 11: rank = set bits of dbits in words < w of block h, dist
+//    = 32 w - (start of the segment holding key 1024 h + 32 w), kDistNone when >= 2^21 - 1;
+//  * records: record j at 16-byte unit 2 j + floor(s_j b / 128) holds {base_j, slope_j} then
+//    the residual units floor(s_j b / 128) .. floor(s_{j+1} b / 128) (every unit of the words
+//    section holding a bit of the segment's keys); the offset needs only j and s_j.
+// A lookup of key i: j = hint[h] + rank + popc(bits at or below i in its word), d = i - s_j
+// from the highest such bit (or dist), then params and residual from record j: one L2 round
+// trip (hint, bits, entry: independent loads) and one DRAM line instead of a binary search.
+constexpr uint32_t kDistNone = 0x1FFFFF;
 __host__ __device__ __forceinline__ uint64_t acc_unit(uint32_t j, uint32_t s, uint32_t b) {
     return 2 * (uint64_t)j + (((uint64_t)s * b) >> 7);
 }
 
-// One warp per segment (grid-stride): copy params[j] and the segment's residual units.
+// segment starts -> block bitmaps (dbits zeroed before)
+__global__ void __launch_bounds__(256) lc_acc_bits_kernel(const Sections sec, uint32_t* dbits) {
+    const uint32_t j = blockIdx.x * 256 + threadIdx.x + 1;  // segment 0 starts at key 0
+    if (j >= sec.L) return;
+    const uint32_t s = __ldg(sec.starts + j);
+    if (s & 1023) atomicOr(dbits + (s >> 5), 1u << (s & 31));  // word (s >> 10) * 32 + ((s >> 5) & 31)
+}
+
+// one warp per block: rank (exclusive warp scan of the word popcounts) and dist per word
+__global__ void __launch_bounds__(256) lc_acc_dir_kernel(const Sections sec, const uint32_t* dbits,
+                                                         uint32_t* dent, uint32_t H) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t h = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (h >= H) return;
+    const uint32_t bw = dbits[32 * h + lane];
+    uint32_t inc = __popc(bw);  // inclusive scan of popcounts
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += x;
+    }
+    const uint32_t rank = inc - __popc(bw);
+    const uint32_t nz = __ballot_sync(kFull, bw != 0) & ((1u << lane) - 1);  // nonzero words < w
+    const uint32_t wl = nz ? 31 - __clz(nz) : 0;
+    const uint32_t bl = __shfl_sync(kFull, bw, wl);
+    uint64_t dist;
+    if (nz) {
+        dist = 32 * lane - (32 * wl + (31 - __clz(bl)));
+    } else {
+        const uint32_t s0 = __ldg(sec.starts + __ldg(sec.hint + h));
+        dist = ((uint64_t)h << 10) + 32 * lane - s0;
+    }
+    dent[32 * h + lane] = rank | ((uint32_t)min(dist, (uint64_t)kDistNone) << 11);
+}
+
+// records: one warp per segment (grid-stride) copies params[j] and the segment's residual units
 __global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, ulonglong2* acc,
                                                            uint32_t b) {
     const uint32_t lane = threadIdx.x & 31;
@@ -353,16 +396,94 @@ __global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, u
     }
 }
 
+// Q queries per thread through the access layout: all loads of one step are issued for the Q
+// queries before any is consumed.
+template <bool K64, int MODE, int Q>
+__global__ void __launch_bounds__(256) lc_access_dir_kernel(const AccessArgs a) {
+    constexpr bool kResidual = MODE != kQuantileApprox;
+    const uint64_t t0 = (uint64_t)blockIdx.x * (256 * Q) + threadIdx.x;
+    const Sections sec = a.sec;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+    uint32_t i[Q], j[Q], bw[Q], e[Q], s[Q];
+    bool live[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        const uint64_t t = t0 + 256 * k;
+        live[k] = false;
+        i[k] = 0;
+        if (t < a.q) {
+            const uint64_t v = __ldcs(a.idx + t);
+            const bool ok = MODE == kAccess ? v < a.n : v <= a.qdiv;
+            if (ok) {
+                live[k] = true;
+                i[k] = MODE == kAccess ? (uint32_t)v
+                                       : (uint32_t)min((uint64_t)a.n * v / a.qdiv, (uint64_t)a.n - 1);
+            } else {
+                if (a.err) atomicOr(a.err, 1u);
+                if (K64) __stcs((unsigned long long*)a.out + t, 0ull);
+                else __stcs((unsigned int*)a.out + t, 0u);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {  // one L2 round trip: hint, bitmap word, entry
+        j[k] = bw[k] = e[k] = 0;
+        if (live[k]) {
+            const uint32_t wi = i[k] >> 5;  // = 32 h + w
+            j[k] = ldh(sec.hint + (i[k] >> 10), keep);
+            bw[k] = ldh(sec.dbits + wi, keep);
+            e[k] = ldh(sec.dent + wi, keep);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        s[k] = 0;
+        if (!live[k]) continue;
+        const uint32_t t = i[k] & 31;
+        const uint32_t m = bw[k] & ((2u << t) - 1);  // starts in the word at or below the key
+        j[k] += (e[k] & 2047) + __popc(m);
+        const uint32_t dist = e[k] >> 11;
+        if (m) s[k] = (i[k] & ~31u) + (31 - __clz(m));
+        else if (dist != kDistNone) s[k] = (i[k] & ~31u) - dist;
+        else s[k] = ldh(sec.starts + j[k], keep);  // segment longer than 2^21 keys
+    }
+    ulonglong2 pr[Q];
+    uint2 w[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {  // one DRAM line (usually): the record's params and field
+        pr[k] = make_ulonglong2(0, 0);
+        w[k] = make_uint2(0, 0);
+        if (!live[k]) continue;
+        const ulonglong2* rec = sec.acc + acc_unit(j[k], s[k], a.b);
+        pr[k] = ldh(rec, once);
+        if (kResidual && a.b) {
+            const uint32_t p = (uint32_t)((uint64_t)i[k] * a.b - ((((uint64_t)s[k] * a.b) >> 7) << 7));
+            const uint32_t* wp = (const uint32_t*)(rec + 1) + (p >> 5);
+            w[k] = make_uint2(ldh(wp, once), ldh(wp + 1, once));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        if (!live[k]) continue;
+        uint8_t* o = (uint8_t*)a.out + (t0 + 256 * k) * (K64 ? 8 : 4);
+        if (kResidual) {
+            const uint32_t u = a.b ? field_of(w[k], i[k], a.b, a.mask) : 0;
+            put<K64>(o, pr[k].x, pred_plus(pr[k].y, i[k] - s[k], u - a.bias));
+        } else {
+            const uint64_t f = pr[k].x + pred_plus(pr[k].y, i[k] - s[k], a.center);
+            if (K64) __stcs((unsigned long long*)o, f < pr[k].x ? ~0ull : (unsigned long long)f);
+            else __stcs((unsigned int*)o, f > 0xffffffffull ? 0xffffffffu : (unsigned int)f);
+        }
+    }
+}
+
 // Dec(K^c)[i] per query (Table I): hint bracket, binary search
 // over starts, one params gather, one residual field.  Each thread serves access_per_thread()
 // queries whose dependent load chains are interleaved; the residual words do not depend on
 // the segment and are fetched before the search.  Quantiles use the same
 // path with i = min(floor(N k / q), N - 1): exact = f(i) + Delta[i]; approximate = floor(f(i))
 // from the segment alone, no residual read, error <= eps, saturated at the key width (L24).
-// ACC (access layout attached): after the search, params and the residual field come from
-// the segment's record (one DRAM line in most lookups) instead of the params and words
-// sections (two independent gathers).
-template <bool K64, int MODE, bool ACC = false>
+template <bool K64, int MODE>
 __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
     constexpr bool kResidual = MODE != kQuantileApprox;
     constexpr uint32_t kAccessPerThread = access_per_thread(MODE);
@@ -398,7 +519,7 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         if (live[k]) {
             lo[k] = ldh(sec.hint + (i[k] >> 10), keep);
             hi[k] = ldh(sec.hint + (i[k] >> 10) + 1, keep);
-            if (!ACC && kResidual && a.b) w[k] = field_words(sec, i[k], a.b, once);
+            if (kResidual && a.b) w[k] = field_words(sec, i[k], a.b, once);
         }
     }
     for (;;) {  // interleaved binary searches: j = max{t in [lo, hi] : starts[t] <= i}
@@ -423,24 +544,14 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         }
     }
     uint32_t s[kAccessPerThread];
-#pragma unroll
-    for (uint32_t k = 0; k < kAccessPerThread; ++k) s[k] = live[k] ? ldh(sec.starts + lo[k], keep) : 0;
     ulonglong2 pr[kAccessPerThread];
 #pragma unroll
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {
+        s[k] = 0;
         pr[k] = make_ulonglong2(0, 0);
         if (!live[k]) continue;
-        if (ACC) {  // the record: params, then the residual units from floor(s b / 128)
-            const ulonglong2* rec = sec.acc + acc_unit(lo[k], s[k], a.b);
-            pr[k] = ldh(rec, once);
-            if (kResidual && a.b) {
-                const uint32_t p = (uint32_t)((uint64_t)i[k] * a.b - ((((uint64_t)s[k] * a.b) >> 7) << 7));
-                const uint32_t* wp = (const uint32_t*)(rec + 1) + (p >> 5);
-                w[k] = make_uint2(ldh(wp, once), ldh(wp + 1, once));
-            }
-        } else {
-            pr[k] = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
-        }
+        s[k] = ldh(sec.starts + lo[k], keep);
+        pr[k] = ldh(sec.params + LC_BOUND(true, lo[k], sec.L), once);
     }
 #pragma unroll
     for (uint32_t k = 0; k < kAccessPerThread; ++k) {

@@ -26,6 +26,7 @@
 
 #include <array>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -239,6 +240,33 @@ int32_t shard_plan(const void* h_blob, uint64_t blob_bytes, uint64_t i0, uint64_
     return span_slices(*h, (const uint8_t*)h_blob, i0, i1, sl);
 }
 
+// queries per thread of the access-layout kernel (LC_ACC_Q = 1 | 2 | 4 overrides, for A/B)
+int acc_queries_per_thread() {
+    static const int q = [] {
+        const char* e = std::getenv("LC_ACC_Q");
+        const int x = e ? std::atoi(e) : 0;
+        return x == 1 || x == 2 || x == 4 ? x : 2;
+    }();
+    return q;
+}
+
+// f(K64, MODE, Q) with compile-time constants
+template <typename F>
+void dispatch_acc(bool k64, int mode, int qp, F&& f) {
+    auto with_k = [&](auto K) {
+        auto with_m = [&](auto M) {
+            if (qp == 1) f(K, M, std::integral_constant<int, 1>{});
+            else if (qp == 4) f(K, M, std::integral_constant<int, 4>{});
+            else f(K, M, std::integral_constant<int, 2>{});
+        };
+        if (mode == kAccess) with_m(std::integral_constant<int, kAccess>{});
+        else if (mode == kQuantileExact) with_m(std::integral_constant<int, kQuantileExact>{});
+        else with_m(std::integral_constant<int, kQuantileApprox>{});
+    };
+    if (k64) with_k(std::true_type{});
+    else with_k(std::false_type{});
+}
+
 int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64_t qdiv, int mode,
                       void* d_out, uint32_t* d_err, cudaStream_t st) {
     AccessArgs a;
@@ -258,19 +286,26 @@ int32_t launch_access(const lc_view* v, const uint64_t* d_in, uint64_t q, uint64
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const unsigned g = (unsigned)grid;
     const bool k64 = v->h.key_bits == 64;
-    const bool acc = v->d_acc != nullptr;  // access layout attached (approximate mode: params only)
+    if (v->d_acc) {  // access layout attached: no binary search, one record per query
+        const int q_per = acc_queries_per_thread();
+        const uint64_t per2 = 256ull * q_per;
+        const uint64_t grid2 = (q + per2 - 1) / per2;
+        if (grid2 > 0x7fffffffULL) return LC_ERR_ARG;
+        dispatch_acc(k64, mode, q_per, [&](auto K, auto M, auto Q) {
+            lc_access_dir_kernel<decltype(K)::value, decltype(M)::value, decltype(Q)::value>
+                <<<(unsigned)grid2, 256, 0, st>>>(a);
+        });
+        lc_detail::count_launch(1);
+        return cuda_status();
+    }
     switch (mode) {
         case kAccess:
-            if (k64) acc ? lc_access_kernel<true, kAccess, true><<<g, 256, 0, st>>>(a)
-                         : lc_access_kernel<true, kAccess><<<g, 256, 0, st>>>(a);
-            else acc ? lc_access_kernel<false, kAccess, true><<<g, 256, 0, st>>>(a)
-                     : lc_access_kernel<false, kAccess><<<g, 256, 0, st>>>(a);
+            if (k64) lc_access_kernel<true, kAccess><<<g, 256, 0, st>>>(a);
+            else lc_access_kernel<false, kAccess><<<g, 256, 0, st>>>(a);
             break;
         case kQuantileExact:
-            if (k64) acc ? lc_access_kernel<true, kQuantileExact, true><<<g, 256, 0, st>>>(a)
-                         : lc_access_kernel<true, kQuantileExact><<<g, 256, 0, st>>>(a);
-            else acc ? lc_access_kernel<false, kQuantileExact, true><<<g, 256, 0, st>>>(a)
-                     : lc_access_kernel<false, kQuantileExact><<<g, 256, 0, st>>>(a);
+            if (k64) lc_access_kernel<true, kQuantileExact><<<g, 256, 0, st>>>(a);
+            else lc_access_kernel<false, kQuantileExact><<<g, 256, 0, st>>>(a);
             break;
         default:
             if (k64) lc_access_kernel<true, kQuantileApprox><<<g, 256, 0, st>>>(a);
@@ -422,20 +457,28 @@ int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream) {
 
 uint64_t lc_access_layout_bytes(const lc_view* v) {
     if (!v) return 0;
-    return 16 * (2 * v->h.n_seg + ((v->h.n * v->h.res_bits) >> 7));
+    const uint64_t H = v->h.n_hint - 1;
+    return 256 * H + 16 * (2 * v->h.n_seg + ((v->h.n * v->h.res_bits) >> 7));
 }
 
 int32_t lc_access_layout_build(lc_view* v, void* d_layout, lc_stream stream) {
     if (!v || !v->d_blob || is_shard(v) || !d_layout || ((uintptr_t)d_layout & 127)) return LC_ERR_ARG;
-    const Sections sec = sections_of(v);
+    cudaStream_t st = (cudaStream_t)stream;
+    lc_view t = *v;
+    t.d_acc = d_layout;
+    const Sections sec = sections_of(&t);
+    const uint64_t H = v->h.n_hint - 1, L = v->h.n_seg;
+    if (cudaMemsetAsync(d_layout, 0, 128 * H, st) != cudaSuccess) return LC_ERR_CUDA;
+    if (L > 1) lc_acc_bits_kernel<<<(unsigned)((L - 1 + 255) / 256), 256, 0, st>>>(sec, (uint32_t*)sec.dbits);
+    lc_acc_dir_kernel<<<(unsigned)((H + 7) / 8), 256, 0, st>>>(sec, sec.dbits, (uint32_t*)sec.dent,
+                                                               (uint32_t)H);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t want = (v->h.n_seg + 7) / 8;  // one warp per segment, 8 warps per CTA
+    const uint64_t want = (L + 7) / 8;  // one warp per segment, 8 warps per CTA
     const unsigned grid = (unsigned)(want < (uint64_t)sms * 16 ? want : (uint64_t)sms * 16);
-    lc_acc_build_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(sec, (ulonglong2*)d_layout,
-                                                                v->h.res_bits);
-    lc_detail::count_launch(1);
+    lc_acc_build_kernel<<<grid, 256, 0, st>>>(sec, (ulonglong2*)sec.acc, v->h.res_bits);
+    lc_detail::count_launch(L > 1 ? 3 : 2);
     const int32_t rc = cuda_status();
     if (!rc) v->d_acc = d_layout;
     return rc;

@@ -26,19 +26,38 @@ def lc():
 
 
 def _records(blob: bytes) -> np.ndarray:
-    """The layout by its definition: record j at 16-byte unit 2 j + floor(s_j b / 128) holds
-    {base_j, slope_j} then the words' 16-byte units floor(s_j b/128) .. floor(s_{j+1} b/128)."""
+    """The layout by its definition (include/lc.h): per 1024-key block h, 32 bitmap words
+    (bit t of word w: key 1024 h + 32 w + t starts a segment, block position 0 excluded), then
+    per block 32 entries rank | dist << 11 (rank = bitmap bits in words < w; dist = 32 w minus
+    the start of the segment holding key 1024 h + 32 w, capped at 2^21 - 1), then record j at
+    16-byte unit 2 j + floor(s_j b / 128): {base_j, slope_j} and the words' 16-byte units
+    floor(s_j b/128) .. floor(s_{j+1} b/128)."""
     bl = parse(blob)
-    units = 2 * bl.L + (bl.n * bl.b) // 128
-    out = np.zeros(units * 4, np.uint32)
+    n, L, b = bl.n, bl.L, bl.b
+    H = (n + 1023) // 1024
+    starts = bl.starts.astype(np.int64)
+    bits = np.zeros(32 * H, np.uint32)
+    for s in starts[1:L]:
+        if s % 1024:
+            bits[s >> 5] |= np.uint32(1 << (s & 31))
+    ent = np.zeros(32 * H, np.uint32)
+    for h in range(H):
+        for w in range(32):
+            rank = sum(bin(int(x)).count("1") for x in bits[32 * h:32 * h + w])
+            key = 1024 * h + 32 * w
+            j = int(np.searchsorted(starts[:L], key, side="right")) - 1  # segment holding key
+            dist = min(key - int(starts[j]), (1 << 21) - 1)
+            ent[32 * h + w] = rank | (dist << 11)
+    units = 2 * L + (n * b) // 128
+    rec = np.zeros(units * 4, np.uint32)
     w = bl.words
-    for j in range(bl.L):
-        s0, s1 = int(bl.starts[j]), int(bl.starts[j + 1])
-        u0, u1 = (s0 * bl.b) // 128, (s1 * bl.b) // 128
+    for j in range(L):
+        s0, s1 = int(starts[j]), int(starts[j + 1])
+        u0, u1 = (s0 * b) // 128, (s1 * b) // 128
         r = 2 * j + u0
-        out[4 * r:4 * r + 4] = np.array([int(bl.base[j]), int(bl.slope[j])], np.uint64).view(np.uint32)
-        out[4 * (r + 1):4 * (r + 2 + u1 - u0)] = w[4 * u0:4 * (u1 + 1)]
-    return out
+        rec[4 * r:4 * r + 4] = np.array([int(bl.base[j]), int(bl.slope[j])], np.uint64).view(np.uint32)
+        rec[4 * (r + 1):4 * (r + 2 + u1 - u0)] = w[4 * u0:4 * (u1 + 1)]
+    return np.concatenate([bits, ent, rec])
 
 
 @pytest.mark.parametrize("seed", range(7300, 7310))
@@ -47,13 +66,12 @@ def test_layout_bytes_formula(lc, seed):
     blob = lc.encode(keys, eps, key_bits=kb)
     bl = parse(blob)
 
-    class _V:  # lc_access_layout_bytes reads only the header of the view
-        pass
-    v = lc.lc_view()
+    v = lc.lc_view()  # lc_access_layout_bytes reads only the header of the view
     import ctypes as C
     C.memmove(C.addressof(v.h), blob, 128)
     assert lc._lib.lc_access_layout_bytes(C.byref(v)) == _records(blob).nbytes
-    assert _records(blob).nbytes == 16 * (2 * bl.L + bl.n * bl.b // 128)
+    H = (bl.n + 1023) // 1024
+    assert _records(blob).nbytes == 256 * H + 16 * (2 * bl.L + bl.n * bl.b // 128)
 
 
 def _dev(a):
@@ -69,7 +87,7 @@ def _check_blob(lc, blob, keys, rng, m=20_000, layout_bytes=True):
     v = lc.View(blob, device=DEV)
     lay = v.build_access_layout()
     torch.cuda.synchronize()
-    if layout_bytes:
+    if layout_bytes and keys.size <= 200_000:
         got = lay.cpu().numpy().view(np.uint32)[: v.access_layout_bytes() // 4]
         assert np.array_equal(got, _records(blob))
     n = keys.size
@@ -79,11 +97,13 @@ def _check_blob(lc, blob, keys, rng, m=20_000, layout_bytes=True):
     ranks = rng.integers(0, 1000, 2000, endpoint=True).astype(np.uint64)
     qi = np.array([orc.quantile_index(n, int(k), 1000) for k in ranks], np.int64)
     q = lc.quantile(v, _dev(ranks), 1000, err=err)
+    qa = lc.quantile(v, _dev(ranks), 1000, exact=False)
     bad = np.array([n, n + 5, 1 << 40], np.uint64)  # out of range: 0 and the error bit
     ab = lc.access(v, _dev(bad), err=err)
     torch.cuda.synchronize()
     assert np.array_equal(_host(a, keys.dtype), keys[idx.astype(np.int64)])
     assert np.array_equal(_host(q, keys.dtype), keys[qi])
+    assert np.array_equal(_host(qa, keys.dtype), orc.predict(blob, qi.astype(np.uint64))[0])
     assert not _host(ab, keys.dtype).any() and int(err.item()) == 1
 
 
