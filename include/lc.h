@@ -67,9 +67,10 @@ typedef struct lc_view {
      * key of segment j, as uint64, in caller-owned device memory.  NULL (lc_view_init's
      * default): lc_next_geq / lc_intersect / lc_union search the params section directly. */
     const uint64_t* d_first;
-    /* Optional access layout (lc_access_layout_build): segment-major records, NULL by default
-     * (lc_view_init).  When attached, lc_access and exact lc_quantile read a key's segment
-     * parameters and its residual field from one record instead of two sections. */
+    /* Optional access layout (lc_access_layout_build), NULL by default (lc_view_init).  When
+     * attached, lc_access and lc_quantile locate a key's segment through its directory (no
+     * binary search) and read the segment parameters and the residual field from one record
+     * instead of two sections. */
     const void* d_acc;
     /* Shard views only (lc_shard_upload; both 0 for a whole-blob view): the view holds the
      * slices of keys [span_lo, span_hi) and nothing else.  Only lc_decode (which then decodes
@@ -205,21 +206,29 @@ uint64_t lc_search_index_bytes(const lc_view* v);
  * with and without it.  Errors: LC_ERR_ARG (null or misaligned d_index). */
 int32_t lc_search_index_build(lc_view* v, void* d_index, lc_stream stream);
 
-/* Device bytes of v's access layout: 16 (2 L + floor(N b / 128)) bytes. */
+/* Device bytes of v's access layout: 256 H + 16 (2 L + floor(N b / 128)) bytes,
+ * H = ceil(N / 1024). */
 uint64_t lc_access_layout_bytes(const lc_view* v);
 
 /* Build v's access layout into d_layout (>= lc_access_layout_bytes(v) bytes, 128-byte aligned,
  * caller-owned, kept alive while v is used) asynchronously on `stream`, and attach it
- * (v->d_acc = d_layout).  The layout is an auxiliary structure aligned with the memory
- * hierarchy (§IV-E ②) for random access f(j) + Delta[j]:
- * record j, at 16-byte unit 2 j + floor(s_j b / 128), holds segment j's {base, slope_fx} (16 B)
- * followed by the 16-byte units floor(s_j b / 128) .. floor(s_{j+1} b / 128) of the residual
- * words (a copy, so the unit shared with the next segment appears in both records).  A lookup
- * still finds j with the hint bracket and the L2-resident binary search over starts, then
- * reads params and its residual field from the same record (usually one DRAM line) instead of
- * two sections.  The blob (FORMAT F1-F7) is unchanged; results of lc_access / lc_quantile are
- * identical with and without the layout.  Errors: LC_ERR_ARG (null or misaligned d_layout,
- * shard view). */
+ * (v->d_acc = d_layout).  An auxiliary structure aligned with the memory hierarchy
+ * (§IV-E ②) for random access f(j) + Delta[j] and quantiles
+ * (PAPER.md:296-315), in two parts:
+ *   directory: for every 32 keys (word w of 1024-key block h) 8 bytes {bits, entry}: bit t of
+ *     bits is set iff key 1024 h + 32 w + t starts a segment (block position 0 excluded: hint[h]
+ *     names the segment holding key 1024 h), entry = rank | dist << 11 with rank = the bits set
+ *     in words < w of the block and dist = 32 w - (start of the segment holding key
+ *     1024 h + 32 w), 2^21 - 1 when larger.  Key i's segment is then
+ *     j = hint[h] + rank + popc(bits at or below i) and its start follows from the highest such
+ *     bit or from dist, with no binary search (Table I's O(log) search, becomes
+ *     one L2 round trip);
+ *   records (from byte 256 H): record j, at 16-byte unit 2 j + floor(s_j b / 128), holds segment
+ *     j's {base, slope_fx} (16 B) followed by the 16-byte units floor(s_j b / 128) ..
+ *     floor(s_{j+1} b / 128) of the residual words (a copy), so params and the residual field
+ *     come from one record (usually one DRAM line) instead of two sections.
+ * The blob (FORMAT F1-F7) is unchanged; results of lc_access / lc_quantile are identical with
+ * and without the layout.  Errors: LC_ERR_ARG (null or misaligned d_layout, shard view). */
 int32_t lc_access_layout_build(lc_view* v, void* d_layout, lc_stream stream);
 
 /* Device scratch bytes lc_intersect needs for list a (its decoded keys, a match bitmap and

@@ -15,11 +15,9 @@ struct Sections {
     const uint32_t* hint;
     const uint32_t* words;
     const uint64_t* first;  // optional successor-search index (lc_view.d_first), may be null
-    // optional access layout (lc_view.d_acc, lc_access_layout_build), null when absent:
-    // per 1024-key block a bitmap of segment starts and per-word (rank, distance) entries,
-    // then the segment-major records
-    const uint32_t* dbits;
-    const uint32_t* dent;
+    // optional access layout (lc_view.d_acc, lc_access_layout_build), null when absent: per
+    // 32 keys {start bitmap, rank | dist << 11}, then the segment-major records
+    const uint2* dir;
     const ulonglong2* acc;
     uint32_t L;  // segments (bound of params)
     uint64_t W;  // residual words (bound of words; up to 2^32 + 4 at N = 2^32 - 1, b = 32)
@@ -44,8 +42,7 @@ Sections sections_of(const lc_view* v) {
     s.first = v->d_first;
     const uint64_t H = v->h.n_hint - 1;
     const uint8_t* A = (const uint8_t*)v->d_acc;
-    s.dbits = A ? (const uint32_t*)A : nullptr;
-    s.dent = A ? (const uint32_t*)(A + 128 * H) : nullptr;
+    s.dir = A ? (const uint2*)A : nullptr;
     s.acc = A ? (const ulonglong2*)(A + 256 * H) : nullptr;
     s.L = (uint32_t)v->h.n_seg;
     s.W = v->h.n_words;
@@ -138,6 +135,11 @@ __device__ __forceinline__ uint32_t ldh(const uint32_t* p, uint64_t pol) {
 __device__ __forceinline__ uint64_t ldh(const uint64_t* p, uint64_t pol) {
     uint64_t v;
     asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ldh(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ ulonglong2 ldh(const ulonglong2* p, uint64_t pol) {

@@ -329,11 +329,12 @@ __host__ __device__ constexpr uint32_t access_per_thread(int mode) {
     return mode == kQuantileApprox ? 1 : 2;
 }
 
-// Access layout (lc_access_layout_build), three parts in one buffer:
-//  * dbits[32 h + w]: bit t set iff key 1024 h + 32 w + t starts a segment (block position 0
-//    excluded: the hint already names the segment holding key 1024 h);
-//  * dent[32 h + w] = rank | dist << 11: rank = set bits of dbits in words < w of block h, dist
-//    = 32 w - (start of the segment holding key 1024 h + 32 w), kDistNone when >= 2^21 - 1;
+// Access layout (lc_access_layout_build), two parts in one buffer:
+//  * dir[32 h + w] = {bits, entry} (8 bytes per 32 keys): bit t of `bits` set iff key
+//    1024 h + 32 w + t starts a segment (block position 0 excluded: the hint already names the
+//    segment holding key 1024 h); entry = rank | dist << 11, rank = set bits in words < w of
+//    block h, dist = 32 w - (start of the segment holding key 1024 h + 32 w), kDistNone when
+//    >= 2^21 - 1;
 //  * records: record j at 16-byte unit 2 j + floor(s_j b / 128) holds {base_j, slope_j} then
 //    the residual units floor(s_j b / 128) .. floor(s_{j+1} b / 128) (every unit of the words
 //    section holding a bit of the segment's keys); the offset needs only j and s_j.
@@ -345,21 +346,21 @@ __host__ __device__ __forceinline__ uint64_t acc_unit(uint32_t j, uint32_t s, ui
     return 2 * (uint64_t)j + (((uint64_t)s * b) >> 7);
 }
 
-// segment starts -> block bitmaps (dbits zeroed before)
-__global__ void __launch_bounds__(256) lc_acc_bits_kernel(const Sections sec, uint32_t* dbits) {
+// segment starts -> block bitmaps (dir zeroed before)
+__global__ void __launch_bounds__(256) lc_acc_bits_kernel(const Sections sec, uint2* dir) {
     const uint32_t j = blockIdx.x * 256 + threadIdx.x + 1;  // segment 0 starts at key 0
     if (j >= sec.L) return;
     const uint32_t s = __ldg(sec.starts + j);
-    if (s & 1023) atomicOr(dbits + (s >> 5), 1u << (s & 31));  // word (s >> 10) * 32 + ((s >> 5) & 31)
+    // word (s >> 10) * 32 + ((s >> 5) & 31) = s >> 5
+    if (s & 1023) atomicOr(&dir[s >> 5].x, 1u << (s & 31));
 }
 
 // one warp per block: rank (exclusive warp scan of the word popcounts) and dist per word
-__global__ void __launch_bounds__(256) lc_acc_dir_kernel(const Sections sec, const uint32_t* dbits,
-                                                         uint32_t* dent, uint32_t H) {
+__global__ void __launch_bounds__(256) lc_acc_dir_kernel(const Sections sec, uint2* dir, uint32_t H) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t h = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (h >= H) return;
-    const uint32_t bw = dbits[32 * h + lane];
+    const uint32_t bw = dir[32 * h + lane].x;
     uint32_t inc = __popc(bw);  // inclusive scan of popcounts
 #pragma unroll
     for (uint32_t o = 1; o < 32; o <<= 1) {
@@ -371,13 +372,15 @@ __global__ void __launch_bounds__(256) lc_acc_dir_kernel(const Sections sec, con
     const uint32_t wl = nz ? 31 - __clz(nz) : 0;
     const uint32_t bl = __shfl_sync(kFull, bw, wl);
     uint64_t dist;
-    if (nz) {
+    if (bw & 1) {  // a segment starts at the word's first key
+        dist = 0;
+    } else if (nz) {
         dist = 32 * lane - (32 * wl + (31 - __clz(bl)));
     } else {
         const uint32_t s0 = __ldg(sec.starts + __ldg(sec.hint + h));
         dist = ((uint64_t)h << 10) + 32 * lane - s0;
     }
-    dent[32 * h + lane] = rank | ((uint32_t)min(dist, (uint64_t)kDistNone) << 11);
+    dir[32 * h + lane].y = rank | ((uint32_t)min(dist, (uint64_t)kDistNone) << 11);
 }
 
 // records: one warp per segment (grid-stride) copies params[j] and the segment's residual units
@@ -404,7 +407,8 @@ __global__ void __launch_bounds__(256) lc_access_dir_kernel(const AccessArgs a) 
     const uint64_t t0 = (uint64_t)blockIdx.x * (256 * Q) + threadIdx.x;
     const Sections sec = a.sec;
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    uint32_t i[Q], j[Q], bw[Q], e[Q], s[Q];
+    uint32_t i[Q], j[Q], s[Q];
+    uint2 de[Q];
     bool live[Q];
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
@@ -426,13 +430,12 @@ __global__ void __launch_bounds__(256) lc_access_dir_kernel(const AccessArgs a) 
         }
     }
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {  // one L2 round trip: hint, bitmap word, entry
-        j[k] = bw[k] = e[k] = 0;
+    for (int k = 0; k < Q; ++k) {  // one L2 round trip: hint and the word's {bits, entry}
+        j[k] = 0;
+        de[k] = make_uint2(0, 0);
         if (live[k]) {
-            const uint32_t wi = i[k] >> 5;  // = 32 h + w
             j[k] = ldh(sec.hint + (i[k] >> 10), keep);
-            bw[k] = ldh(sec.dbits + wi, keep);
-            e[k] = ldh(sec.dent + wi, keep);
+            de[k] = ldh(sec.dir + (i[k] >> 5), keep);  // index 32 h + w
         }
     }
 #pragma unroll
@@ -440,9 +443,9 @@ __global__ void __launch_bounds__(256) lc_access_dir_kernel(const AccessArgs a) 
         s[k] = 0;
         if (!live[k]) continue;
         const uint32_t t = i[k] & 31;
-        const uint32_t m = bw[k] & ((2u << t) - 1);  // starts in the word at or below the key
-        j[k] += (e[k] & 2047) + __popc(m);
-        const uint32_t dist = e[k] >> 11;
+        const uint32_t m = de[k].x & ((2u << t) - 1);  // starts in the word at or below the key
+        j[k] += (de[k].y & 2047) + __popc(m);
+        const uint32_t dist = de[k].y >> 11;
         if (m) s[k] = (i[k] & ~31u) + (31 - __clz(m));
         else if (dist != kDistNone) s[k] = (i[k] & ~31u) - dist;
         else s[k] = ldh(sec.starts + j[k], keep);  // segment longer than 2^21 keys

@@ -468,10 +468,9 @@ int32_t lc_access_layout_build(lc_view* v, void* d_layout, lc_stream stream) {
     t.d_acc = d_layout;
     const Sections sec = sections_of(&t);
     const uint64_t H = v->h.n_hint - 1, L = v->h.n_seg;
-    if (cudaMemsetAsync(d_layout, 0, 128 * H, st) != cudaSuccess) return LC_ERR_CUDA;
-    if (L > 1) lc_acc_bits_kernel<<<(unsigned)((L - 1 + 255) / 256), 256, 0, st>>>(sec, (uint32_t*)sec.dbits);
-    lc_acc_dir_kernel<<<(unsigned)((H + 7) / 8), 256, 0, st>>>(sec, sec.dbits, (uint32_t*)sec.dent,
-                                                               (uint32_t)H);
+    if (cudaMemsetAsync(d_layout, 0, 256 * H, st) != cudaSuccess) return LC_ERR_CUDA;
+    if (L > 1) lc_acc_bits_kernel<<<(unsigned)((L - 1 + 255) / 256), 256, 0, st>>>(sec, (uint2*)sec.dir);
+    lc_acc_dir_kernel<<<(unsigned)((H + 7) / 8), 256, 0, st>>>(sec, (uint2*)sec.dir, (uint32_t)H);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

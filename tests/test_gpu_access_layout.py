@@ -26,11 +26,11 @@ def lc():
 
 
 def _records(blob: bytes) -> np.ndarray:
-    """The layout by its definition (include/lc.h): per 1024-key block h, 32 bitmap words
-    (bit t of word w: key 1024 h + 32 w + t starts a segment, block position 0 excluded), then
-    per block 32 entries rank | dist << 11 (rank = bitmap bits in words < w; dist = 32 w minus
-    the start of the segment holding key 1024 h + 32 w, capped at 2^21 - 1), then record j at
-    16-byte unit 2 j + floor(s_j b / 128): {base_j, slope_j} and the words' 16-byte units
+    """The layout by its definition (include/lc.h): per 32 keys (word w of 1024-key block h)
+    a pair {bits, rank | dist << 11}: bit t of `bits` set iff key 1024 h + 32 w + t starts a
+    segment (block position 0 excluded), rank = bits set in words < w of the block, dist = 32 w
+    minus the start of the segment holding key 1024 h + 32 w (capped at 2^21 - 1); then record
+    j at 16-byte unit 2 j + floor(s_j b / 128): {base_j, slope_j} and the words' 16-byte units
     floor(s_j b/128) .. floor(s_{j+1} b/128)."""
     bl = parse(blob)
     n, L, b = bl.n, bl.L, bl.b
@@ -57,7 +57,7 @@ def _records(blob: bytes) -> np.ndarray:
         r = 2 * j + u0
         rec[4 * r:4 * r + 4] = np.array([int(bl.base[j]), int(bl.slope[j])], np.uint64).view(np.uint32)
         rec[4 * (r + 1):4 * (r + 2 + u1 - u0)] = w[4 * u0:4 * (u1 + 1)]
-    return np.concatenate([bits, ent, rec])
+    return np.concatenate([np.stack([bits, ent], axis=1).reshape(-1), rec])
 
 
 @pytest.mark.parametrize("seed", range(7300, 7310))
