@@ -260,6 +260,47 @@ uint64_t lc_union_scratch_bytes(const lc_view* a, const lc_view* b);
 int32_t lc_union(const lc_view* a, const lc_view* b, void* d_scratch, uint64_t scratch_bytes,
                  void* d_out, uint64_t* d_count, lc_stream stream);
 
+/* ------------------------------------------------------------- batches (many short lists)
+ * An inverted index is many posting lists (§III-A); decoding them one call
+ * each is launch-bound (a 1e6-key list decodes in ~10 us).  A batch groups m blobs that live in
+ * one device buffer (each 256-byte aligned) and decodes all of them in ONE launch: the work
+ * units are the 1024-key chunks of all lists (a short list is one partial chunk), described by
+ * a host-built directory in device memory.  All lists of a batch share key_bits; eps, and so
+ * the residual width b, may differ per list. */
+typedef struct lc_batch {
+    uint32_t m;             /* lists */
+    uint32_t key_bits;      /* common key width (32 | 64) */
+    uint32_t max_res_bits;  /* widest residual field of the batch */
+    uint32_t sparse;        /* fewer than one segment per 64 keys overall (decode variant) */
+    uint64_t n_total;       /* keys over all lists */
+    uint64_t n_chunks;      /* 1024-key chunks over all lists */
+    uint64_t payload_bytes; /* bytes of the lists' headers and sections, without the 256-byte
+                               alignment padding: what a decode reads */
+    const void* d_lists;    /* device directory: m list records (64 B each) ... */
+    const void* d_chunks;   /* ... then n_chunks chunk records (48 B each) */
+} lc_batch;
+
+/* Directory bytes of the batch of m blobs at host byte offsets blob_off[k] of h_blobs (each a
+ * full LCG1 blob; headers checked).  LC_ERR_FORMAT for a bad header, LC_ERR_ARG for m == 0,
+ * mixed key widths or an unaligned offset. */
+int32_t lc_batch_dir_bytes(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off,
+                           uint32_t m, uint64_t* dir_bytes);
+
+/* Fill *b and write the batch directory into d_dir (>= lc_batch_dir_bytes, 16-byte aligned)
+ * asynchronously on `stream` (from a library-internal host staging copy: h_* may be released on
+ * return).  h_blobs holds the m blobs at blob_off[k]; d_blobs is the device copy of the same
+ * bytes (same offsets, 256-byte aligned base).  out_off[k] is the element offset of list k's
+ * keys in the batch output, or NULL for packed lists in order (prefix sums of n).  Every
+ * list's hint section is checked (non-decreasing, within [0, L - 1]) since chunk records copy
+ * it: LC_ERR_FORMAT otherwise. */
+int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off,
+                      uint32_t m, const void* d_blobs, const uint64_t* out_off, void* d_dir,
+                      uint64_t dir_bytes, lc_stream stream);
+
+/* Decode every list of the batch in one launch: list k's keys to d_out[out_off[k] ..
+ * out_off[k] + n_k) (elements of key_bits / 8 bytes).  Dec(K^c) per list (Def. 1). */
+int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream);
+
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
  * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out

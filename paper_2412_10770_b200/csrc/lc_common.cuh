@@ -52,6 +52,7 @@ Sections sections_of(const lc_view* v) {
 // FORMAT F3 decode bias c: eps for anchored blobs, 0 for free-intercept blobs (F7)
 bool is_free(const lc_view* v) { return v->h.flags & LC_FLAG_FREE_INTERCEPT; }
 uint32_t bias_of(const lc_view* v) { return is_free(v) ? 0u : v->h.eps; }
+uint32_t bias_of_header(const lc_header& h) { return (h.flags & LC_FLAG_FREE_INTERCEPT) ? 0u : h.eps; }
 
 // Bounds-checked build (-DLC_DEBUG_BOUNDS, tests/test_gpu_bounds.py): every shared-memory page
 // / ring-slot index and every section index is checked; a violation is counted in

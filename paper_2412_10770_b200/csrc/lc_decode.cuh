@@ -97,10 +97,26 @@ struct Page {
     uint32_t* sW;         // the chunk's residual words
     uint32_t pj, cp;
     uint32_t phase;
+    uint32_t rb, rmask;   // runtime residual width and mask (B == kRtB: batch kernels)
 #ifdef LC_DEBUG_BOUNDS
     uint32_t cs, nw;  // staged starts / words entries
 #endif
 };
+
+// B == kRtB: the residual width is a runtime value (pg.rb), for the batch kernels whose lists
+// have different widths; every other B is a compile-time width (lc_decode_kernel).
+constexpr uint32_t kRtB = 64;
+template <uint32_t B>
+__device__ __forceinline__ uint32_t bits_of(const Page& pg) { return B == kRtB ? pg.rb : B; }
+template <uint32_t B>
+__device__ __forceinline__ uint32_t fld(const Page& pg, uint32_t w, uint32_t lw, uint32_t ls) {
+    if (B == kRtB) {
+        if (!pg.rb) return 0;
+        const uint32_t* wp = pg.sW + w * pg.rb + lw;
+        return __funnelshift_r(wp[0], wp[1], ls) & pg.rmask;
+    }
+    return field<B == kRtB ? 0 : B>(pg.sW, w, lw, ls);
+}
 
 // Stage starts[pj, pj + cs) and params[pj, pj + cp) (plus, when wbytes != 0, the chunk's words)
 // with TMA bulk copies; cs covers one start past the params so every window candidate
@@ -148,8 +164,8 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
     const uint32_t seg = jb + __popc(m);
     const uint32_t d = m ? lane - (31 - __clz(m)) : (wb - sb) + lane;
     const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
-    LC_CHECK(B && (FULL || lane < valid), w * B + lw + 1, pg.nw);
-    const uint32_t t = pred_plus(pr.y, d, field<B>(pg.sW, w, lw, ls) - bias);
+    LC_CHECK(bits_of<B>(pg) && (FULL || lane < valid), w * bits_of<B>(pg) + lw + 1, pg.nw);
+    const uint32_t t = pred_plus(pr.y, d, fld<B>(pg, w, lw, ls) - bias);
     outw = shifted<K64, UNI>(outw, ins, wb, lane);
     if (FULL || lane < valid) put<K64>(outw, pr.x, t);
     // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
@@ -193,9 +209,9 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t mB = PB & lmask;
     const uint32_t dB = mB ? lane - (31 - __clz(mB)) : offB + lane;
     const ulonglong2 pB = pg.sP[LC_BOUND(true, jB + __popc(mB) - pg.pj, pg.cp)];
-    LC_CHECK(B, (2 * w2 + 1) * B + lw + 1, pg.nw);
-    const uint32_t tA = pred_plus(pA.y, dA, field<B>(pg.sW, 2 * w2, lw, ls) - bias);
-    const uint32_t tB = pred_plus(pB.y, dB, field<B>(pg.sW, 2 * w2 + 1, lw, ls) - bias);
+    LC_CHECK(bits_of<B>(pg), (2 * w2 + 1) * bits_of<B>(pg) + lw + 1, pg.nw);
+    const uint32_t tA = pred_plus(pA.y, dA, fld<B>(pg, 2 * w2, lw, ls) - bias);
+    const uint32_t tB = pred_plus(pB.y, dB, fld<B>(pg, 2 * w2 + 1, lw, ls) - bias);
     put<K64>(shifted<K64, UNI>(outw, ins, wb, lane), pA.x, tA);
     put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw, ins, wb + 32, lane), pB.x, tB);
     jb = min(jb + adv, jlast + 1);  // see decode_window
@@ -222,9 +238,9 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         const uint32_t d0 = (wb - sb) + lane;
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
-            LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
+            LC_CHECK(bits_of<B>(pg), (4 * w4 + q) * bits_of<B>(pg) + lw + 1, pg.nw);
             put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
-                     pred_plus(pr.y, d0 + 32 * q, field<B>(pg.sW, 4 * w4 + q, lw, ls) - bias));
+                     pred_plus(pr.y, d0 + 32 * q, fld<B>(pg, 4 * w4 + q, lw, ls) - bias));
         }
         jb = min(jb + __popc(__ballot_sync(kFull, x == 128)), jlast + 1);  // a start at wb + 128
         sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
@@ -245,9 +261,9 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         const uint32_t m = P & lmask;
         const uint32_t d = m ? lane - (31 - __clz(m)) : off + lane;
         const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
-        LC_CHECK(B, (4 * w4 + q) * B + lw + 1, pg.nw);
+        LC_CHECK(bits_of<B>(pg), (4 * w4 + q) * bits_of<B>(pg) + lw + 1, pg.nw);
         put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
-                 pred_plus(pr.y, d, field<B>(pg.sW, 4 * w4 + q, lw, ls) - bias));
+                 pred_plus(pr.y, d, fld<B>(pg, 4 * w4 + q, lw, ls) - bias));
         off = P ? __clz(P) + 1 : off + 32;
         jq += __popc(P);
     }
@@ -358,3 +374,145 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
 }
 
+
+// ------------------------------------------------------------------------ batch decode
+// A batch of many lists (lc_batch_init: an inverted index's posting lists)
+// decoded in ONE launch: every 1024-key chunk of every list is a work unit, described by a
+// host-built 48-byte record, so the persistent warps stream through all lists the same way
+// lc_decode_kernel streams through one (short lists are single partial chunks).  The lists'
+// residual widths differ (each list has its own eps), so the width is a runtime value
+// (B = kRtB).
+struct BatchChunk {
+    uint64_t blob;        // device address of the list's blob (FORMAT F1: starts at byte 256)
+    uint64_t out;         // output element offset of the chunk's first key
+    uint32_t off_params, off_words;
+    uint32_t j0, jlast;   // hint pair of the chunk (hint[h], hint[h + 1])
+    uint32_t key0;        // first key of the chunk in its list (a multiple of 1024)
+    uint32_t nk_b;        // keys in the chunk (1..1024) | residual width b << 16
+    uint32_t bias;        // FORMAT F3 decode bias
+    uint32_t list;        // list index in the batch
+};
+static_assert(sizeof(BatchChunk) == 48, "BatchChunk is three 16-byte loads");
+
+// One list of a batch (64 bytes): what the set operations need to search it.
+struct BatchList {
+    uint64_t blob;        // device address of the list's blob
+    uint64_t out;         // output element offset of the list's first key
+    uint32_t n, L;
+    uint32_t off_params, off_hint, off_words;
+    uint32_t chunk0;      // the list's first chunk record
+    uint32_t b, bias, eps, flags;
+    uint32_t pad[2];
+};
+static_assert(sizeof(BatchList) == 64, "BatchList is four 16-byte loads");
+
+struct BatchArgs {
+    const BatchChunk* chunks;  // the batch's chunk records
+    const uint32_t* sel;       // optional selection: unit c decodes chunk sel[c] ...
+    const uint64_t* sel_out;   // ... to output element offset sel_out[c] (both or neither)
+    void* out;
+    const uint32_t* nunits;    // optional device count of units (overrides `units` when set)
+    uint32_t units;            // chunks to decode (the batch's, or the selection's)
+    uint32_t warp_bytes;       // shared memory per warp (widest b of the batch)
+};
+
+__device__ __forceinline__ BatchChunk load_chunk(const BatchChunk* p) {
+    BatchChunk r;
+    const uint4* q = (const uint4*)p;
+    const uint4 x = __ldg(q), y = __ldg(q + 1), z = __ldg(q + 2);
+    r.blob = ((uint64_t)x.y << 32) | x.x;
+    r.out = ((uint64_t)x.w << 32) | x.z;
+    r.off_params = y.x;
+    r.off_words = y.y;
+    r.j0 = y.z;
+    r.jlast = y.w;
+    r.key0 = z.x;
+    r.nk_b = z.y;
+    r.bias = z.z;
+    r.list = z.w;
+    return r;
+}
+
+template <bool K64, bool SPARSE>
+__global__ void __launch_bounds__(kThreads, 4)
+    lc_decode_batch_kernel(const BatchArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* base = smem + warp * a.warp_bytes;
+    Page pg;
+    pg.bar = (uint64_t*)base;
+    pg.sS = (uint32_t*)(base + page_starts_off());
+    pg.sP = (ulonglong2*)(base + page_params_off());
+    pg.sW = (uint32_t*)(base + page_words_off());
+    pg.phase = 0;
+    if (lane == 0) mbar_init(pg.bar);
+    __syncwarp();
+
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lmask = lanemask_le();
+    const uint32_t nwarps = gridDim.x * kWarpsPerCta;
+    const uint32_t units = a.nunits ? *a.nunits : a.units;
+    Ins ins;  // unused (no insertions)
+    ins.rho = nullptr;
+
+    uint32_t c = blockIdx.x * kWarpsPerCta + warp;
+    BatchChunk nr;  // the warp's next chunk record, loaded one chunk ahead
+    uint64_t nout = 0;
+    if (c < units) {
+        nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c) : c));
+        nout = a.sel ? __ldg(a.sel_out + c) : nr.out;
+    }
+    for (; c < units; c += nwarps) {
+        const BatchChunk r = nr;
+        const uint64_t out0 = nout;
+        if (c + nwarps < units) {
+            nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c + nwarps) : c + nwarps));
+            nout = a.sel ? __ldg(a.sel_out + c + nwarps) : nr.out;
+        }
+        const uint8_t* blob = (const uint8_t*)r.blob;
+        Sections sec;
+        sec.starts = (const uint32_t*)(blob + 256);
+        sec.params = (const ulonglong2*)(blob + r.off_params);
+        sec.words = (const uint32_t*)(blob + r.off_words);
+        sec.hint = nullptr;
+        sec.first = nullptr;
+        sec.dir = nullptr;
+        sec.acc = nullptr;
+        sec.L = r.jlast + 1;
+        sec.W = 0;
+        const uint32_t nk = r.nk_b & 0xffff, b = r.nk_b >> 16;
+        pg.rb = b;
+        pg.rmask = b >= 32 ? kFull : (1u << b) - 1;
+        const uint32_t lw = (lane * b) >> 5, ls = (lane * b) & 31;
+        const uint32_t wbytes = b ? ((((nk * b + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
+        stage(pg, sec, r.j0, r.jlast, sec.words + (size_t)(r.key0 >> 10) * 32 * b, wbytes, lane);
+        uint32_t jb = r.j0, sb = pg.sS[LC_BOUND(true, r.j0 - pg.pj, pg.cs)];
+        uint8_t* outl = (uint8_t*)a.out + (out0 + lane) * kw;
+        const uint32_t key0 = r.key0, jlast = r.jlast;
+        if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged
+#pragma unroll 1
+            for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
+#pragma unroll
+                for (uint32_t k = 0; k < 2; ++k)
+                    decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast,
+                                                                 key0 + 128 * (g + k), g + k, lane,
+                                                                 lmask, lw, ls, r.bias,
+                                                                 outl + 128 * kw * k, ins);
+            }
+        } else if (nk == 1024) {  // dense chunk: paged
+#pragma unroll 1
+            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    decode_pair<K64, kRtB, true, false>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k),
+                                                        g + k, lane, lmask, lw, ls, r.bias,
+                                                        outl + 64 * kw * k, ins);
+            }
+        } else {  // a list's last (partial) chunk: short lists are only this
+            for (uint32_t w = 0; 32 * w < nk; ++w)
+                decode_window<K64, kRtB, true, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
+                                                             w, lane, lmask, lw, ls, r.bias,
+                                                             outl + 32 * kw * w, nk - 32 * w, ins);
+        }
+    }
+}

@@ -123,6 +123,44 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     return cuda_status();
 }
 
+// batch decode: units [0, units) of the batch's chunk records (or of a selection sel/sel_out;
+// nunits: optional device count)
+const void* batch_kernel(bool k64, bool sparse) {
+    if (k64) return sparse ? (const void*)lc_decode_batch_kernel<true, true>
+                           : (const void*)lc_decode_batch_kernel<true, false>;
+    return sparse ? (const void*)lc_decode_batch_kernel<false, true>
+                  : (const void*)lc_decode_batch_kernel<false, false>;
+}
+
+int32_t launch_batch_decode(const lc_batch* b, const uint32_t* sel, const uint64_t* sel_out,
+                            const uint32_t* nunits, uint32_t units, void* d_out, cudaStream_t st) {
+    BatchArgs a;
+    a.chunks = (const BatchChunk*)b->d_chunks;
+    a.sel = sel;
+    a.sel_out = sel_out;
+    a.out = d_out;
+    a.nunits = nunits;
+    a.units = units;
+    a.warp_bytes = warp_bytes_for(b->max_res_bits);
+    const uint32_t smem = a.warp_bytes * kWarpsPerCta;
+    const bool k64 = b->key_bits == 64;
+    const void* fn = batch_kernel(k64, b->sparse);
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
+    const uint32_t full = (uint32_t)(sms * (occ > 0 ? occ : 1));
+    const uint32_t need = (units + kWarpsPerCta - 1) / kWarpsPerCta;
+    const uint32_t grid = nunits ? full : (need < full ? need : full);
+    if (!grid) return LC_OK;
+    void* args[] = {&a};
+    if (cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st) != cudaSuccess)
+        return LC_ERR_CUDA;
+    lc_detail::count_launch(1);
+    return cuda_status();
+}
+
 // lc_decode_host pipeline resources: an H2D and a D2H copy stream plus one event per span and
 // stage.  Pipes are pooled per device: a call takes a free pipe of its device (creating one
 // when every pipe is busy enqueueing), so concurrent callers never share events and never hold
@@ -245,7 +283,7 @@ int acc_queries_per_thread() {
     static const int q = [] {
         const char* e = std::getenv("LC_ACC_Q");
         const int x = e ? std::atoi(e) : 0;
-        return x == 1 || x == 2 || x == 4 ? x : 2;
+        return x == 1 || x == 2 || x == 4 ? x : 1;
     }();
     return q;
 }
@@ -636,6 +674,123 @@ int32_t lc_shard_upload(const void* h_blob, uint64_t blob_bytes, uint64_t i0, ui
     v->sec_base[2] = d + y.o_hint - 4 * sl.c0;
     v->sec_base[3] = d + y.o_words - 4 * sl.w_lo;
     return cuda_status();
+}
+
+// ---------------------------------------------------------------------------- batches
+namespace {
+int32_t batch_scan(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off, uint32_t m,
+                   uint64_t* n_chunks, uint32_t* key_bits) {
+    if (!h_blobs || !blob_off || !m || !n_chunks) return LC_ERR_ARG;
+    uint64_t c = 0;
+    for (uint32_t k = 0; k < m; ++k) {
+        if ((blob_off[k] & 255) || blob_off[k] + sizeof(lc_header) > h_bytes) return LC_ERR_ARG;
+        lc_header h;
+        std::memcpy(&h, (const uint8_t*)h_blobs + blob_off[k], sizeof h);
+        const int32_t st = lc_detail::check_header(&h, h_bytes - blob_off[k]);
+        if (st) return st;
+        if (k == 0) *key_bits = h.key_bits;
+        else if (h.key_bits != *key_bits) return LC_ERR_ARG;
+        c += h.n_hint - 1;
+    }
+    *n_chunks = c;
+    return LC_OK;
+}
+}  // namespace
+
+int32_t lc_batch_dir_bytes(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off,
+                           uint32_t m, uint64_t* dir_bytes) {
+    if (!dir_bytes) return LC_ERR_ARG;
+    uint64_t nc = 0;
+    uint32_t kb = 0;
+    const int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb);
+    if (st) return st;
+    *dir_bytes = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc;
+    return LC_OK;
+}
+
+int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off,
+                      uint32_t m, const void* d_blobs, const uint64_t* out_off, void* d_dir,
+                      uint64_t dir_bytes, lc_stream stream) {
+    if (!b || !d_blobs || ((uintptr_t)d_blobs & 255) || !d_dir || ((uintptr_t)d_dir & 15))
+        return LC_ERR_ARG;
+    uint64_t nc = 0;
+    uint32_t kb = 0;
+    int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb);
+    if (st) return st;
+    if (nc >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
+    const uint64_t need = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc;
+    if (dir_bytes < need) return LC_ERR_ARG;
+    std::vector<uint8_t> host(need);
+    BatchList* lists = (BatchList*)host.data();
+    BatchChunk* chunks = (BatchChunk*)(host.data() + sizeof(BatchList) * (uint64_t)m);
+    uint64_t c = 0, pos = 0, segs = 0, payload = 0;
+    uint32_t maxb = 0;
+    for (uint32_t k = 0; k < m; ++k) {
+        const uint8_t* B = (const uint8_t*)h_blobs + blob_off[k];
+        lc_header h;
+        std::memcpy(&h, B, sizeof h);
+        const uint64_t H = h.n_hint - 1, L = h.n_seg;
+        const uint32_t* hint = (const uint32_t*)(B + h.off_hint);
+        for (uint64_t q = 0; q <= H; ++q)  // chunk records copy the hint pairs: check them
+            if (hint[q] >= L || (q && hint[q] < hint[q - 1])) return LC_ERR_FORMAT;
+        const uint64_t out = out_off ? out_off[k] : pos;
+        const uint32_t bias = bias_of_header(h);
+        BatchList& e = lists[k];
+        e.blob = (uint64_t)(uintptr_t)d_blobs + blob_off[k];
+        e.out = out;
+        e.n = (uint32_t)h.n;
+        e.L = (uint32_t)L;
+        e.off_params = (uint32_t)h.off_params;
+        e.off_hint = (uint32_t)h.off_hint;
+        e.off_words = (uint32_t)h.off_words;
+        e.chunk0 = (uint32_t)c;
+        e.b = h.res_bits;
+        e.bias = bias;
+        e.eps = h.eps;
+        e.flags = h.flags;
+        e.pad[0] = e.pad[1] = 0;
+        if (h.off_words >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
+        for (uint64_t q = 0; q < H; ++q, ++c) {
+            BatchChunk& r = chunks[c];
+            r.blob = e.blob;
+            r.out = out + (q << 10);
+            r.off_params = e.off_params;
+            r.off_words = e.off_words;
+            r.j0 = hint[q];
+            r.jlast = hint[q + 1];
+            r.key0 = (uint32_t)(q << 10);
+            const uint64_t nk = h.n - (q << 10) < 1024 ? h.n - (q << 10) : 1024;
+            r.nk_b = (uint32_t)nk | ((uint32_t)h.res_bits << 16);
+            r.bias = bias;
+            r.list = k;
+        }
+        pos += h.n;
+        segs += L;
+        maxb = h.res_bits > maxb ? h.res_bits : maxb;
+        // what a decode reads: header, starts, params, hint, words (no alignment padding)
+        payload += sizeof(lc_header) + 4 * (L + 1) + 16 * L + 4 * h.n_hint +
+                   4 * ((h.n * h.res_bits + 31) / 32);
+    }
+    if (cudaMemcpyAsync(d_dir, host.data(), need, cudaMemcpyHostToDevice, (cudaStream_t)stream) !=
+        cudaSuccess)
+        return LC_ERR_CUDA;
+    b->m = m;
+    b->key_bits = kb;
+    b->max_res_bits = maxb;
+    b->sparse = segs * 64 < pos;
+    b->n_total = pos;
+    b->n_chunks = nc;
+    b->payload_bytes = payload;
+    b->d_lists = d_dir;
+    b->d_chunks = (const uint8_t*)d_dir + sizeof(BatchList) * (uint64_t)m;
+    return LC_OK;
+}
+
+int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream) {
+    if (!b || !b->d_chunks || !d_out || ((uintptr_t)d_out % (b->key_bits / 8))) return LC_ERR_ARG;
+    if (!b->n_chunks) return LC_OK;
+    return launch_batch_decode(b, nullptr, nullptr, nullptr, (uint32_t)b->n_chunks, d_out,
+                               (cudaStream_t)stream);
 }
 
 int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, void* d_out,

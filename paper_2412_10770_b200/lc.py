@@ -40,6 +40,12 @@ class lc_header(C.Structure):
 assert C.sizeof(lc_header) == 128
 
 
+class lc_batch(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("key_bits", C.c_uint32), ("max_res_bits", C.c_uint32),
+                ("sparse", C.c_uint32), ("n_total", C.c_uint64), ("n_chunks", C.c_uint64),
+                ("payload_bytes", C.c_uint64), ("d_lists", C.c_void_p), ("d_chunks", C.c_void_p)]
+
+
 class lc_view(C.Structure):
     _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p),
                 ("d_acc", C.c_void_p), ("span_lo", C.c_uint64), ("span_hi", C.c_uint64), ("sec_base", C.c_uint64 * 4)]
@@ -69,6 +75,9 @@ _sig = {
     "lc_decode_host": ([_p, _u64, _p, _p, _p, _p], _i32),
     "lc_shard_bytes": ([_p, _u64, _u64, _u64, C.POINTER(_u64)], _i32),
     "lc_shard_upload": ([_p, _u64, _u64, _u64, _p, _u64, C.POINTER(lc_view), _p], _i32),
+    "lc_batch_dir_bytes": ([_p, _u64, _p, _u32, C.POINTER(_u64)], _i32),
+    "lc_batch_init": ([C.POINTER(lc_batch), _p, _u64, _p, _u32, _p, _p, _p, _u64, _p], _i32),
+    "lc_decode_batch": ([C.POINTER(lc_batch), _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
 }
@@ -449,3 +458,65 @@ def decode_host(h_blob, d_blob, d_out, h_out, stream=None) -> None:
         _check(_lib.lc_decode_host(h_blob.data_ptr(), h_blob.numel(), d_blob.data_ptr(),
                                    d_out.data_ptr(), h_out.data_ptr(), on.handle),
                "lc_decode_host")
+
+
+# ------------------------------------------------------------------------------- batches
+class Batch:
+    """Many lists in one device buffer (lc_batch_init): their blobs packed at 256-byte aligned
+    offsets, uploaded once, plus the device directory of the batch (list and chunk records)."""
+
+    def __init__(self, blobs, device="cuda", stream=None, out_off=None):
+        import torch
+        offs, pos = [], 0
+        for bl in blobs:
+            offs.append(pos)
+            pos += (len(bl) + 255) // 256 * 256
+        host = np.zeros(max(pos, 256), np.uint8)
+        for o, bl in zip(offs, blobs):
+            host[o:o + len(bl)] = np.frombuffer(bl, np.uint8)
+        self.blob_off = np.asarray(offs, np.uint64)
+        self.m = len(blobs)
+        self.host = host
+        nb = C.c_uint64()
+        _check(_lib.lc_batch_dir_bytes(host.ctypes.data, host.nbytes, self.blob_off.ctypes.data,
+                                       self.m, C.byref(nb)), "lc_batch_dir_bytes")
+        oo = None if out_off is None else np.ascontiguousarray(out_off, np.uint64)
+        with _On(stream) as on:
+            self.d_blobs = on.use(torch.from_numpy(host).to(device, non_blocking=False))
+            self.d_dir = on.use(torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device))
+            self.b = lc_batch()
+            _check(_lib.lc_batch_init(C.byref(self.b), host.ctypes.data, host.nbytes,
+                                      self.blob_off.ctypes.data, self.m, self.d_blobs.data_ptr(),
+                                      None if oo is None else oo.ctypes.data,
+                                      self.d_dir.data_ptr(), self.d_dir.numel(), on.handle),
+                   "lc_batch_init")
+        headers = [lc_header.from_buffer_copy(bl[:128]) for bl in blobs]
+        self.n = np.array([h.n for h in headers], np.int64)
+        self.out_off = (np.concatenate([[0], np.cumsum(self.n)[:-1]]).astype(np.int64)
+                        if oo is None else oo.astype(np.int64))
+
+    @property
+    def n_total(self) -> int:
+        return int(self.b.n_total)
+
+    @property
+    def torch_dtype(self):
+        import torch
+        return torch.int64 if self.b.key_bits == 64 else torch.int32
+
+    def tensors(self):
+        return (self.d_blobs, self.d_dir)
+
+
+def decode_batch(batch: Batch, out=None, stream=None):
+    """lc_decode_batch: every list of the batch in one launch; list k's keys at
+    out[batch.out_off[k] : batch.out_off[k] + batch.n[k]]."""
+    import torch
+    with _On(stream, *batch.tensors()) as on:
+        if out is None:
+            size = int((batch.out_off + batch.n).max()) if batch.m else 0
+            out = torch.empty(max(size, 1), dtype=batch.torch_dtype, device=batch.d_blobs.device)
+        on.use(out)
+        _check(_lib.lc_decode_batch(C.byref(batch.b), out.data_ptr(), on.handle),
+               "lc_decode_batch")
+    return out

@@ -11,3 +11,4 @@ from .configs import (  # noqa: F401
     make_queries,
     fuzz_case,
 )
+from .corpus import list_eps, make_corpus  # noqa: F401,E402
