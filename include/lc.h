@@ -273,7 +273,8 @@ typedef struct lc_batch {
     uint32_t max_res_bits;  /* widest residual field of the batch */
     uint32_t sparse;        /* fewer than one segment per 64 keys overall (decode variant) */
     uint64_t n_total;       /* keys over all lists */
-    uint64_t n_chunks;      /* 1024-key chunks over all lists */
+    uint64_t n_chunks;      /* 1024-key chunks over all lists (a list's last one may be partial) */
+    uint64_t n_small;       /* of which partial chunks of <= 64 keys (records stored last) */
     uint64_t payload_bytes; /* bytes of the lists' headers and sections, without the 256-byte
                                alignment padding: what a decode reads */
     const void* d_lists;    /* device directory: m list records (64 B each) ... */

@@ -400,9 +400,9 @@ struct BatchList {
     uint64_t out;         // output element offset of the list's first key
     uint32_t n, L;
     uint32_t off_params, off_hint, off_words;
-    uint32_t chunk0;      // the list's first chunk record
+    uint32_t chunk0;      // the list's first chunk record of more than kSmallUnit keys ...
     uint32_t b, bias, eps, flags;
-    uint32_t pad[2];
+    uint32_t pad[2];      // [0]: ... and its small (last) chunk record, or 0xffffffff
 };
 static_assert(sizeof(BatchList) == 64, "BatchList is four 16-byte loads");
 
@@ -413,8 +413,14 @@ struct BatchArgs {
     void* out;
     const uint32_t* nunits;    // optional device count of units (overrides `units` when set)
     uint32_t units;            // chunks to decode (the batch's, or the selection's)
+    uint32_t small0;           // units [small0, units) are small (<= kSmallUnit keys): one lane each
     uint32_t warp_bytes;       // shared memory per warp (widest b of the batch)
 };
+
+// Small units (a posting list of <= 64 keys is one, and most lists of a Zipf vocabulary are
+// that short): one LANE decodes a whole unit serially from global memory (L1), so a warp
+// serves 32 of them at once instead of paying a staging round trip per list.
+constexpr uint32_t kSmallUnit = 64;
 
 __device__ __forceinline__ BatchChunk load_chunk(const BatchChunk* p) {
     BatchChunk r;
@@ -455,17 +461,52 @@ __global__ void __launch_bounds__(kThreads, 4)
     Ins ins;  // unused (no insertions)
     ins.rho = nullptr;
 
+    const uint32_t big = a.sel ? units : min(a.small0, units);
+    // ---- small units, one per lane (their records are at the end of the batch's array)
+    for (uint32_t u = big + (blockIdx.x * kWarpsPerCta + warp) * 32 + lane; u < units;
+         u += nwarps * 32) {
+        const BatchChunk r = load_chunk(a.chunks + u);
+        const uint8_t* blob = (const uint8_t*)r.blob;
+        const uint32_t* S = (const uint32_t*)(blob + 256);
+        const ulonglong2* P = (const ulonglong2*)(blob + r.off_params);
+        const uint32_t* W = (const uint32_t*)(blob + r.off_words);
+        const uint32_t nk = r.nk_b & 0xffff, b = r.nk_b >> 16;
+        const uint32_t mask = b >= 32 ? kFull : (1u << b) - 1;
+        uint32_t j = r.j0, s0 = __ldg(S + j), e = __ldg(S + j + 1);
+        ulonglong2 pr = __ldg(P + j);
+        uint8_t* o = (uint8_t*)a.out + r.out * kw;
+        for (uint32_t k = 0; k < nk; ++k) {
+            const uint32_t i = r.key0 + k;
+            while (i >= e) {  // next segment
+                ++j;
+                s0 = e;
+                e = __ldg(S + j + 1);
+                pr = __ldg(P + j);
+            }
+            uint32_t uf = 0;
+            if (b) {
+                const uint64_t bit = (uint64_t)i * b;
+                const uint32_t* wp = W + (bit >> 5);
+                uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & mask;
+            }
+            const uint32_t t = pred_plus(pr.y, i - s0, uf - r.bias);
+            if (K64) __stcs((unsigned long long*)o + k, (unsigned long long)(pr.x + t));
+            else __stcs((unsigned int*)o + k, (unsigned int)pr.x + t);
+        }
+    }
+
+    // ---- the other units, one per warp (1024-key chunks and longer partial chunks)
     uint32_t c = blockIdx.x * kWarpsPerCta + warp;
     BatchChunk nr;  // the warp's next chunk record, loaded one chunk ahead
     uint64_t nout = 0;
-    if (c < units) {
+    if (c < big) {
         nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c) : c));
         nout = a.sel ? __ldg(a.sel_out + c) : nr.out;
     }
-    for (; c < units; c += nwarps) {
+    for (; c < big; c += nwarps) {
         const BatchChunk r = nr;
         const uint64_t out0 = nout;
-        if (c + nwarps < units) {
+        if (c + nwarps < big) {
             nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c + nwarps) : c + nwarps));
             nout = a.sel ? __ldg(a.sel_out + c + nwarps) : nr.out;
         }

@@ -135,6 +135,7 @@ const void* batch_kernel(bool k64, bool sparse) {
 int32_t launch_batch_decode(const lc_batch* b, const uint32_t* sel, const uint64_t* sel_out,
                             const uint32_t* nunits, uint32_t units, void* d_out, cudaStream_t st) {
     BatchArgs a;
+    a.small0 = sel ? units : (uint32_t)(b->n_chunks - b->n_small);
     a.chunks = (const BatchChunk*)b->d_chunks;
     a.sel = sel;
     a.sel_out = sel_out;
@@ -723,7 +724,16 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
     std::vector<uint8_t> host(need);
     BatchList* lists = (BatchList*)host.data();
     BatchChunk* chunks = (BatchChunk*)(host.data() + sizeof(BatchList) * (uint64_t)m);
-    uint64_t c = 0, pos = 0, segs = 0, payload = 0;
+    // chunk records: units of more than kSmallUnit keys first (one warp each), then the small
+    // ones (one lane each); a list's chunk0 is its first record's index
+    uint64_t nsmall = 0;
+    for (uint32_t k = 0; k < m; ++k) {
+        lc_header h;
+        std::memcpy(&h, (const uint8_t*)h_blobs + blob_off[k], sizeof h);
+        const uint64_t tail = h.n & 1023;  // the last chunk's keys (0: full)
+        if (tail && tail <= kSmallUnit) ++nsmall;
+    }
+    uint64_t c = 0, cs = nc - nsmall, pos = 0, segs = 0, payload = 0;
     uint32_t maxb = 0;
     for (uint32_t k = 0; k < m; ++k) {
         const uint8_t* B = (const uint8_t*)h_blobs + blob_off[k];
@@ -748,10 +758,13 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
         e.bias = bias;
         e.eps = h.eps;
         e.flags = h.flags;
-        e.pad[0] = e.pad[1] = 0;
+        e.pad[1] = 0;
+        const uint64_t tail = h.n & 1023;
+        e.pad[0] = tail && tail <= kSmallUnit ? (uint32_t)cs : 0xffffffffu;  // small record
         if (h.off_words >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
-        for (uint64_t q = 0; q < H; ++q, ++c) {
-            BatchChunk& r = chunks[c];
+        for (uint64_t q = 0; q < H; ++q) {
+            const uint64_t nkq = h.n - (q << 10) < 1024 ? h.n - (q << 10) : 1024;
+            BatchChunk& r = chunks[nkq <= kSmallUnit ? cs++ : c++];
             r.blob = e.blob;
             r.out = out + (q << 10);
             r.off_params = e.off_params;
@@ -759,8 +772,7 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
             r.j0 = hint[q];
             r.jlast = hint[q + 1];
             r.key0 = (uint32_t)(q << 10);
-            const uint64_t nk = h.n - (q << 10) < 1024 ? h.n - (q << 10) : 1024;
-            r.nk_b = (uint32_t)nk | ((uint32_t)h.res_bits << 16);
+            r.nk_b = (uint32_t)nkq | ((uint32_t)h.res_bits << 16);
             r.bias = bias;
             r.list = k;
         }
@@ -780,6 +792,7 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
     b->sparse = segs * 64 < pos;
     b->n_total = pos;
     b->n_chunks = nc;
+    b->n_small = nsmall;
     b->payload_bytes = payload;
     b->d_lists = d_dir;
     b->d_chunks = (const uint8_t*)d_dir + sizeof(BatchList) * (uint64_t)m;
