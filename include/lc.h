@@ -302,6 +302,28 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
  * out_off[k] + n_k) (elements of key_bits / 8 bytes).  Dec(K^c) per list (Def. 1). */
 int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream);
 
+/* Batched AND / OR queries (inverted-index processing, §III-A, Fig. 4):
+ * pair p = (h_pairs[2 p], h_pairs[2 p + 1]) names two lists of the batch; h_n[k] is list k's
+ * key count (host, m entries, as given to lc_batch_init).  All pairs run in a fixed number of
+ * launches whatever their number.  The shorter list s_p of each pair is decoded; for AND each
+ * of its keys is searched in the compressed longer list l_p (next_geq: segments as skip
+ * pointers), for OR both are decoded and every key placed in its union slot by ranks.
+ * Results: pair p's keys at d_out[d_out_off[p] .. d_out_off[p] + d_counts[p]) (device arrays
+ * of P + 1 and P uint64; AND results are packed, OR results sit at capacity offsets
+ * sum_{q < p} (n_s + n_l)).  d_scratch: >= *scratch_bytes (256-byte aligned); d_out: >=
+ * *out_keys keys, both from lc_setop_batch_scratch_bytes.  Errors: LC_ERR_ARG (bad pair index,
+ * h_n not matching the batch, buffers too small), LC_ERR_TOO_LARGE (>= 2^32 short keys). */
+enum { LC_SETOP_AND = 0, LC_SETOP_OR = 1 };
+int32_t lc_setop_batch_scratch_bytes(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                                     uint32_t n_pairs, int32_t op, uint64_t* scratch_bytes,
+                                     uint64_t* out_keys);
+int32_t lc_intersect_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                           uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+                           uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream);
+int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                       uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+                       uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream);
+
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer
  * d_blob (>= blob_bytes, 256-byte aligned), decodes into the caller's device buffer d_out

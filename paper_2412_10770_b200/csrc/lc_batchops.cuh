@@ -1,0 +1,191 @@
+// lc_batchops.cuh -- AND / OR of many list pairs of a batch in a fixed number of launches
+// Internal part of lc_kernels.cu: included inside its anonymous namespace.
+//
+// The paper's inverted-index queries (§III-A, Fig. 4) over a batch of posting
+// lists (lc_batch_init): for each pair p of lists, the shorter s_p and the longer l_p.
+//  * AND: s_p's keys are decoded (one batch decode of a selection of chunk records), each is
+//    searched in the COMPRESSED l_p with next_geq (segments as skip pointers: segments of l_p
+//    holding no key of s_p are never read), matches flagged, counted, scanned and written
+//    packed; pair p's result is out[out_off[p] .. out_off[p + 1]).
+//  * OR: both lists are decoded into scratch; every key gets its union slot from ranks:
+//    slot(x in s, index i) = i + #{l < x} - #{matched s keys before i} and
+//    slot(y in l, index j) = j + #{s < y} - #{matched s keys below y} (a key present in both
+//    lists gets the same slot from both sides), so no merge pass runs; pair p's result is
+//    out[out_off[p] .. out_off[p] + count[p]) with out_off[p] = sum over earlier pairs of
+//    n_s + n_l (capacity).
+
+struct SetopArgs {
+    const BatchList* lists;
+    const uint32_t* sl;       // [2 p] short list, [2 p + 1] long list
+    const uint64_t* s_off;    // P + 1: short keys of pair p at keys_s[s_off[p] .. s_off[p + 1])
+    const uint64_t* l_off;    // P + 1: long keys of pair p at keys_l[l_off[p] ..) (OR)
+    const uint64_t* cap_off;  // P + 1: OR output capacity offsets
+    const void* keys_s;
+    const void* keys_l;
+    uint32_t* flags;          // match bit per short key (ceil(S / 32) + 1 words, zeroed)
+    uint32_t* counts;         // matches per 256 short keys, then exclusive offsets; [nblk] total
+    uint32_t* mw;             // matches before each flags word
+    uint32_t* rank;           // OR: #{l < x} per short key
+    uint64_t* total;          // scan total (device scalar)
+    void* out;
+    uint64_t* d_out_off;      // P + 1 result offsets
+    uint64_t* d_counts;       // P result sizes
+    uint64_t S, Lt;
+    uint32_t P, nblk, nwords;
+};
+
+template <bool K64>
+__device__ __forceinline__ uint64_t key_at(const void* base, uint64_t i) {
+    return K64 ? __ldg((const uint64_t*)base + i) : (uint64_t)__ldg((const uint32_t*)base + i);
+}
+
+// pair of element g: max{p : off[p] <= g} over the P + 1 offsets (off[0] = 0)
+__device__ __forceinline__ uint32_t pair_of(const uint64_t* off, uint32_t P, uint64_t g) {
+    uint32_t lo = 0, hi = P;  // off[P] = total > g
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// #{t < n : keys[t] < x} over decoded keys
+template <bool K64>
+__device__ __forceinline__ uint64_t lower_bound_keys(const void* keys, uint64_t lo, uint64_t n,
+                                                     uint64_t x) {
+    uint64_t l = 0, r = n;
+    while (l < r) {
+        const uint64_t mid = (l + r) >> 1;
+        if (key_at<K64>(keys, lo + mid) < x) l = mid + 1;
+        else r = mid;
+    }
+    return l;
+}
+
+// matches among short keys [0, g)
+__device__ __forceinline__ uint64_t matches_before(const SetopArgs& a, uint64_t g) {
+    const uint32_t w = (uint32_t)(g >> 5);
+    return __ldg(a.mw + w) + __popc(__ldg(a.flags + w) & ((1u << (g & 31)) - 1));
+}
+
+__device__ __forceinline__ Sections list_sections(const BatchList& e) {
+    const uint8_t* B = (const uint8_t*)e.blob;
+    Sections s;
+    s.starts = (const uint32_t*)(B + 256);
+    s.params = (const ulonglong2*)(B + e.off_params);
+    s.hint = (const uint32_t*)(B + e.off_hint);
+    s.words = (const uint32_t*)(B + e.off_words);
+    s.first = nullptr;
+    s.dir = nullptr;
+    s.acc = nullptr;
+    s.L = e.L;
+    s.W = 0;
+    return s;
+}
+
+// one thread per short key: found in its pair's long list?  AND searches the compressed list
+// (next_geq), OR the decoded one (and keeps the rank)
+template <bool K64, bool OR>
+__global__ void __launch_bounds__(256) lc_bprobe_kernel(const SetopArgs a) {
+    __shared__ uint32_t warp_cnt[8];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t g = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    const bool live = g < a.S;
+    bool found = false;
+    if (live) {
+        const uint64_t x = key_at<K64>(a.keys_s, g);
+        const uint32_t p = pair_of(a.s_off, a.P, g);
+        if (OR) {
+            const uint64_t lo = __ldg(a.l_off + p), nl = __ldg(a.l_off + p + 1) - lo;
+            const uint64_t r = lower_bound_keys<K64>(a.keys_l, lo, nl, x);
+            found = r < nl && key_at<K64>(a.keys_l, lo + r) == x;
+            a.rank[g] = (uint32_t)r;
+        } else {
+            const BatchList e = a.lists[__ldg(a.sl + 2 * p + 1)];
+            const Sections sec = list_sections(e);
+            const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+            const uint64_t xs[1] = {x};
+            const bool lv[1] = {true};
+            SuccResult r[1] = {{e.n, 0}};
+            const uint32_t mask = e.b >= 32 ? kFull : (1u << e.b) - 1;
+            if (e.flags & LC_FLAG_FREE_INTERCEPT)
+                next_geq_q<true, false, 1>(sec, e.n, e.L, e.b, mask, e.bias, 2 * (uint64_t)e.eps,
+                                           xs, lv, r, keep, once, once);
+            else
+                next_geq_q<false, false, 1>(sec, e.n, e.L, e.b, mask, e.bias, 2 * (uint64_t)e.eps,
+                                            xs, lv, r, keep, once, once);
+            found = r[0].idx < e.n && r[0].key == x;
+        }
+    }
+    const uint32_t bal = __ballot_sync(kFull, found);
+    if (lane == 0) {
+        if (g < a.S) a.flags[g >> 5] = bal;
+        warp_cnt[warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (int w = 0; w < 8; ++w) c += warp_cnt[w];
+        a.counts[blockIdx.x] = c;
+    }
+}
+
+// mw[w] = matches before flags word w (counts hold the exclusive per-256 offsets)
+__global__ void __launch_bounds__(256) lc_bmw_kernel(const SetopArgs a) {
+    const uint32_t w = blockIdx.x * 256 + threadIdx.x;
+    if (w >= a.nwords) return;
+    uint32_t m = a.counts[min(w >> 3, a.nblk)];
+    for (uint32_t v = w & ~7u; v < w; ++v) m += __popc(a.flags[v]);
+    a.mw[w] = m;
+}
+
+// AND: matched short keys to their packed slot; OR: unmatched short keys to their union slot
+template <bool K64, bool OR>
+__global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
+    const uint64_t g = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (g >= a.S) return;
+    const bool found = (__ldg(a.flags + (g >> 5)) >> (g & 31)) & 1;
+    if (found == OR) return;
+    const uint64_t x = key_at<K64>(a.keys_s, g);
+    uint64_t pos;
+    if (!OR) {
+        pos = matches_before(a, g);
+    } else {
+        const uint32_t p = pair_of(a.s_off, a.P, g);
+        const uint64_t s0 = __ldg(a.s_off + p);
+        pos = __ldg(a.cap_off + p) + (g - s0) + __ldg(a.rank + g) -
+              (matches_before(a, g) - matches_before(a, s0));
+    }
+    if (K64) ((uint64_t*)a.out)[pos] = x;
+    else ((uint32_t*)a.out)[pos] = (uint32_t)x;
+}
+
+// OR: every long key to its union slot
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
+    const uint64_t gl = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (gl >= a.Lt) return;
+    const uint32_t p = pair_of(a.l_off, a.P, gl);
+    const uint64_t y = key_at<K64>(a.keys_l, gl);
+    const uint64_t s0 = __ldg(a.s_off + p), ns = __ldg(a.s_off + p + 1) - s0;
+    const uint64_t ra = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
+    const uint64_t pos = __ldg(a.cap_off + p) + (gl - __ldg(a.l_off + p)) + ra -
+                         (matches_before(a, s0 + ra) - matches_before(a, s0));
+    if (K64) ((uint64_t*)a.out)[pos] = y;
+    else ((uint32_t*)a.out)[pos] = (uint32_t)y;
+}
+
+// per pair: result offset and size
+template <bool OR>
+__global__ void __launch_bounds__(256) lc_bpairs_kernel(const SetopArgs a) {
+    const uint32_t p = blockIdx.x * 256 + threadIdx.x;
+    if (p > a.P) return;
+    const uint64_t m0 = matches_before(a, __ldg(a.s_off + p));
+    a.d_out_off[p] = OR ? __ldg(a.cap_off + p) : m0;
+    if (p == a.P) return;
+    const uint64_t m1 = matches_before(a, __ldg(a.s_off + p + 1));
+    a.d_counts[p] = OR ? (__ldg(a.s_off + p + 1) - __ldg(a.s_off + p)) +
+                             (__ldg(a.l_off + p + 1) - __ldg(a.l_off + p)) - (m1 - m0)
+                       : m1 - m0;
+}

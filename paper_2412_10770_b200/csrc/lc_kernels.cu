@@ -42,6 +42,7 @@ namespace {
 #include "lc_decode.cuh"
 #include "lc_gather.cuh"
 #include "lc_setops.cuh"
+#include "lc_batchops.cuh"
 
 // ------------------------------------------------------------------------------ launchers
 uint32_t mask_of(uint32_t b) { return b >= 32 ? 0xffffffffu : ((1u << b) - 1); }
@@ -797,6 +798,198 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
     b->d_lists = d_dir;
     b->d_chunks = (const uint8_t*)d_dir + sizeof(BatchList) * (uint64_t)m;
     return LC_OK;
+}
+
+namespace {
+// Host plan of a batched AND / OR (lc_batchops.cuh): which list of each pair is short, the key
+// offsets, the chunk records to decode (the same record order as lc_batch_init: a list's chunks
+// of more than kSmallUnit keys from its big-region index on, its small last chunk after all big
+// records) and the scratch layout.
+struct SetopPlan {
+    uint64_t P, S, Lt, U, nwords, nblk;
+    uint64_t o_sl, o_soff, o_loff, o_cap, o_sel, o_selout, head;  // uploaded head
+    uint64_t o_keys, o_flags, o_mw, o_counts, o_rank, o_total, total;
+    uint64_t out_cap;  // output elements the caller provides
+    std::vector<uint8_t> host;  // the head's bytes
+};
+
+int32_t setop_plan(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pairs, uint32_t P,
+                   bool OR, bool fill, SetopPlan* y) {
+    if (!bt || !h_n || (!h_pairs && P) || !bt->d_lists) return LC_ERR_ARG;
+    const uint32_t m = bt->m;
+    const uint64_t kw = bt->key_bits / 8;
+    // record index of every list's first big chunk and of its small chunk
+    std::vector<uint64_t> big0(m), small_idx(m);
+    uint64_t nbig = 0, nsm = 0;
+    for (uint32_t k = 0; k < m; ++k) {
+        const uint64_t n = h_n[k], H = (n + 1023) >> 10, tail = n & 1023;
+        const bool sm = tail && tail <= kSmallUnit;
+        big0[k] = nbig;
+        nbig += H - sm;
+        small_idx[k] = sm ? nsm++ : ~0ULL;
+    }
+    if (nbig + nsm != bt->n_chunks) return LC_ERR_ARG;  // h_n does not describe this batch
+    uint64_t S = 0, Lt = 0, U = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint32_t a = h_pairs[2 * p], b = h_pairs[2 * p + 1];
+        if (a >= m || b >= m) return LC_ERR_ARG;
+        const uint64_t ns = h_n[a] <= h_n[b] ? h_n[a] : h_n[b], nl = h_n[a] <= h_n[b] ? h_n[b] : h_n[a];
+        S += ns;
+        U += (ns + 1023) >> 10;
+        if (OR) {
+            Lt += nl;
+            U += (nl + 1023) >> 10;
+        }
+    }
+    if (S >= (1ULL << 32) || U >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
+    y->P = P;
+    y->S = S;
+    y->Lt = Lt;
+    y->U = U;
+    y->nwords = (S + 31) / 32 + 1;
+    y->nblk = (S + 255) / 256;
+    y->o_sl = 0;
+    y->o_soff = r256(8ULL * P);
+    y->o_loff = y->o_soff + r256(8 * (P + 1));
+    y->o_cap = y->o_loff + r256(8 * (P + 1));
+    y->o_sel = y->o_cap + r256(8 * (P + 1));
+    y->o_selout = y->o_sel + r256(4 * U);
+    y->head = y->o_selout + r256(8 * U);
+    y->o_keys = y->head;
+    y->o_flags = y->o_keys + r256(kw * (S + Lt));
+    y->o_mw = y->o_flags + r256(4 * y->nwords);
+    y->o_counts = y->o_mw + r256(4 * y->nwords);
+    y->o_rank = y->o_counts + r256(4 * (y->nblk + 1));
+    y->o_total = y->o_rank + (OR ? r256(4 * S) : 0);
+    y->total = y->o_total + 256;
+    y->out_cap = OR ? S + Lt : S;
+    if (!fill) return LC_OK;
+    y->host.assign(y->head, 0);
+    uint8_t* H = y->host.data();
+    uint32_t* sl = (uint32_t*)(H + y->o_sl);
+    uint64_t* soff = (uint64_t*)(H + y->o_soff);
+    uint64_t* loff = (uint64_t*)(H + y->o_loff);
+    uint64_t* cap = (uint64_t*)(H + y->o_cap);
+    uint32_t* sel = (uint32_t*)(H + y->o_sel);
+    uint64_t* selout = (uint64_t*)(H + y->o_selout);
+    uint64_t so = 0, lo = 0, co = 0, u = 0;
+    auto add_list = [&](uint32_t k, uint64_t dst) {  // decode list k to keys[dst ..)
+        const uint64_t n = h_n[k], Hk = (n + 1023) >> 10;
+        for (uint64_t q = 0; q < Hk; ++q, ++u) {
+            sel[u] = (uint32_t)(small_idx[k] != ~0ULL && q == Hk - 1 ? nbig + small_idx[k] : big0[k] + q);
+            selout[u] = dst + (q << 10);
+        }
+    };
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint32_t a = h_pairs[2 * p], b = h_pairs[2 * p + 1];
+        const uint32_t sh = h_n[a] <= h_n[b] ? a : b, lg = h_n[a] <= h_n[b] ? b : a;
+        sl[2 * p] = sh;
+        sl[2 * p + 1] = lg;
+        soff[p] = so;
+        loff[p] = lo;
+        cap[p] = co;
+        add_list(sh, so);
+        if (OR) add_list(lg, S + lo);
+        so += h_n[sh];
+        if (OR) lo += h_n[lg];
+        co += h_n[sh] + (OR ? h_n[lg] : 0);
+    }
+    soff[P] = so;
+    loff[P] = lo;
+    cap[P] = co;
+    return LC_OK;
+}
+
+int32_t setop_batch(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pairs, uint32_t P,
+                    bool OR, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+                    uint64_t* d_out_off, uint64_t* d_counts, cudaStream_t st) {
+    if (!d_scratch || ((uintptr_t)d_scratch & 255) || !d_out || !d_out_off || !d_counts)
+        return LC_ERR_ARG;
+    if (!P) return LC_OK;
+    SetopPlan y;
+    int32_t rc = setop_plan(bt, h_n, h_pairs, P, OR, true, &y);
+    if (rc) return rc;
+    if (scratch_bytes < y.total) return LC_ERR_ARG;
+    uint8_t* D = (uint8_t*)d_scratch;
+    if (cudaMemcpyAsync(D, y.host.data(), y.head, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemsetAsync(D + y.o_flags, 0, 4 * y.nwords, st) != cudaSuccess)
+        return LC_ERR_CUDA;
+    if ((rc = launch_batch_decode(bt, (const uint32_t*)(D + y.o_sel),
+                                  (const uint64_t*)(D + y.o_selout), nullptr, (uint32_t)y.U,
+                                  D + y.o_keys, st)))
+        return rc;
+    const bool k64 = bt->key_bits == 64;
+    SetopArgs a;
+    a.lists = (const BatchList*)bt->d_lists;
+    a.sl = (const uint32_t*)(D + y.o_sl);
+    a.s_off = (const uint64_t*)(D + y.o_soff);
+    a.l_off = (const uint64_t*)(D + y.o_loff);
+    a.cap_off = (const uint64_t*)(D + y.o_cap);
+    a.keys_s = D + y.o_keys;
+    a.keys_l = D + y.o_keys + (bt->key_bits / 8) * y.S;
+    a.flags = (uint32_t*)(D + y.o_flags);
+    a.mw = (uint32_t*)(D + y.o_mw);
+    a.counts = (uint32_t*)(D + y.o_counts);
+    a.rank = (uint32_t*)(D + y.o_rank);
+    a.total = (uint64_t*)(D + y.o_total);
+    a.out = d_out;
+    a.d_out_off = d_out_off;
+    a.d_counts = d_counts;
+    a.S = y.S;
+    a.Lt = y.Lt;
+    a.P = P;
+    a.nblk = (uint32_t)y.nblk;
+    a.nwords = (uint32_t)y.nwords;
+    const unsigned gs = (unsigned)y.nblk;
+    if (k64) OR ? lc_bprobe_kernel<true, true><<<gs, 256, 0, st>>>(a) : lc_bprobe_kernel<true, false><<<gs, 256, 0, st>>>(a);
+    else OR ? lc_bprobe_kernel<false, true><<<gs, 256, 0, st>>>(a) : lc_bprobe_kernel<false, false><<<gs, 256, 0, st>>>(a);
+    IsectArgs sa{};
+    sa.counts = a.counts;
+    sa.nblk = a.nblk;
+    sa.d_count = a.total;
+    lc_isect_scan_kernel<<<1, 1024, 0, st>>>(sa);
+    lc_bmw_kernel<<<(unsigned)((y.nwords + 255) / 256), 256, 0, st>>>(a);
+    if (k64) OR ? lc_bwrite_s_kernel<true, true><<<gs, 256, 0, st>>>(a) : lc_bwrite_s_kernel<true, false><<<gs, 256, 0, st>>>(a);
+    else OR ? lc_bwrite_s_kernel<false, true><<<gs, 256, 0, st>>>(a) : lc_bwrite_s_kernel<false, false><<<gs, 256, 0, st>>>(a);
+    uint32_t nl = 5;
+    if (OR && y.Lt) {
+        const unsigned gl = (unsigned)((y.Lt + 255) / 256);
+        if (k64) lc_bwrite_l_kernel<true><<<gl, 256, 0, st>>>(a);
+        else lc_bwrite_l_kernel<false><<<gl, 256, 0, st>>>(a);
+        ++nl;
+    }
+    const unsigned gp = (unsigned)((P + 1 + 255) / 256);
+    if (OR) lc_bpairs_kernel<true><<<gp, 256, 0, st>>>(a);
+    else lc_bpairs_kernel<false><<<gp, 256, 0, st>>>(a);
+    lc_detail::count_launch(nl);
+    return cuda_status();
+}
+}  // namespace
+
+int32_t lc_setop_batch_scratch_bytes(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                                     uint32_t n_pairs, int32_t op, uint64_t* scratch_bytes,
+                                     uint64_t* out_keys) {
+    if (!scratch_bytes || !out_keys || (op != LC_SETOP_AND && op != LC_SETOP_OR)) return LC_ERR_ARG;
+    SetopPlan y;
+    const int32_t rc = setop_plan(b, h_n, h_pairs, n_pairs, op == LC_SETOP_OR, false, &y);
+    if (rc) return rc;
+    *scratch_bytes = y.total;
+    *out_keys = y.out_cap;
+    return LC_OK;
+}
+
+int32_t lc_intersect_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                           uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+                           uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream) {
+    return setop_batch(b, h_n, h_pairs, n_pairs, false, d_scratch, scratch_bytes, d_out, d_out_off,
+                       d_counts, (cudaStream_t)stream);
+}
+
+int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                       uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+                       uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream) {
+    return setop_batch(b, h_n, h_pairs, n_pairs, true, d_scratch, scratch_bytes, d_out, d_out_off,
+                       d_counts, (cudaStream_t)stream);
 }
 
 int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream) {

@@ -78,6 +78,10 @@ _sig = {
     "lc_batch_dir_bytes": ([_p, _u64, _p, _u32, C.POINTER(_u64)], _i32),
     "lc_batch_init": ([C.POINTER(lc_batch), _p, _u64, _p, _u32, _p, _p, _p, _u64, _p], _i32),
     "lc_decode_batch": ([C.POINTER(lc_batch), _p, _p], _i32),
+    "lc_setop_batch_scratch_bytes": ([C.POINTER(lc_batch), _p, _p, _u32, _i32, C.POINTER(_u64),
+                                      C.POINTER(_u64)], _i32),
+    "lc_intersect_batch": ([C.POINTER(lc_batch), _p, _p, _u32, _p, _u64, _p, _p, _p, _p], _i32),
+    "lc_union_batch": ([C.POINTER(lc_batch), _p, _p, _u32, _p, _u64, _p, _p, _p, _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
 }
@@ -520,3 +524,54 @@ def decode_batch(batch: Batch, out=None, stream=None):
         _check(_lib.lc_decode_batch(C.byref(batch.b), out.data_ptr(), on.handle),
                "lc_decode_batch")
     return out
+
+
+LC_SETOP_AND, LC_SETOP_OR = 0, 1
+
+
+class SetopBuffers:
+    """Scratch, output and result arrays of one batched AND / OR over fixed pairs (reusable)."""
+
+    def __init__(self, batch: Batch, pairs, op: int):
+        import torch
+        self.pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)
+        self.h_n = np.ascontiguousarray(batch.n, np.uint64)
+        self.op = op
+        sb, ok = C.c_uint64(), C.c_uint64()
+        _check(_lib.lc_setop_batch_scratch_bytes(C.byref(batch.b), self.h_n.ctypes.data,
+                                                 self.pairs.ctypes.data, len(self.pairs), op,
+                                                 C.byref(sb), C.byref(ok)),
+               "lc_setop_batch_scratch_bytes")
+        dev = batch.d_blobs.device
+        self.scratch = torch.empty(max(sb.value, 256), dtype=torch.uint8, device=dev)
+        self.out = torch.empty(max(ok.value, 1), dtype=batch.torch_dtype, device=dev)
+        self.out_off = torch.zeros(len(self.pairs) + 1, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(max(len(self.pairs), 1), dtype=torch.int64, device=dev)
+
+    def tensors(self):
+        return (self.scratch, self.out, self.out_off, self.counts)
+
+
+def _setop_batch(fn, what, batch: Batch, pairs, op, bufs, stream):
+    if bufs is None:
+        bufs = SetopBuffers(batch, pairs, op)
+    with _On(stream, *batch.tensors(), *bufs.tensors()) as on:
+        _check(fn(C.byref(batch.b), bufs.h_n.ctypes.data, bufs.pairs.ctypes.data,
+                  len(bufs.pairs), bufs.scratch.data_ptr(), bufs.scratch.numel(),
+                  bufs.out.data_ptr(), bufs.out_off.data_ptr(), bufs.counts.data_ptr(),
+                  on.handle), what)
+    return bufs
+
+
+def intersect_batch(batch: Batch, pairs=None, bufs=None, stream=None) -> SetopBuffers:
+    """lc_intersect_batch: AND of every pair (a, b) of list indices; pair p's keys at
+    bufs.out[bufs.out_off[p] : bufs.out_off[p] + bufs.counts[p]] (packed)."""
+    return _setop_batch(_lib.lc_intersect_batch, "lc_intersect_batch", batch, pairs,
+                        LC_SETOP_AND, bufs, stream)
+
+
+def union_batch(batch: Batch, pairs=None, bufs=None, stream=None) -> SetopBuffers:
+    """lc_union_batch: OR of every pair; pair p's keys at
+    bufs.out[bufs.out_off[p] : bufs.out_off[p] + bufs.counts[p]]."""
+    return _setop_batch(_lib.lc_union_batch, "lc_union_batch", batch, pairs, LC_SETOP_OR, bufs,
+                        stream)

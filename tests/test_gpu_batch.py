@@ -117,3 +117,58 @@ def test_batch_full_corpus(lc):
     torch.cuda.synchronize()
     assert torch.equal(out[:want.numel()], want)
     assert list_eps(10) == (1 << 31) - 1
+
+
+# ------------------------------------------------------------------ batched AND / OR
+def _setop_check(lc, lists, blobs, pairs):
+    from oracle import setops
+    bt = lc.Batch(blobs, device=DEV)
+    ia = lc.intersect_batch(bt, pairs)
+    ua = lc.union_batch(bt, pairs)
+    torch.cuda.synchronize()
+    dt = np.uint32 if bt.b.key_bits == 32 else np.uint64
+    for name, r, fn in (("AND", ia, setops.intersect), ("OR", ua, setops.union)):
+        out = r.out.cpu().numpy().view(dt)
+        off = r.out_off.cpu().numpy()
+        cnt = r.counts.cpu().numpy()
+        for p, (a, b) in enumerate(pairs):
+            want = fn(lists[a].astype(np.uint64), lists[b].astype(np.uint64))
+            got = out[off[p]:off[p] + cnt[p]].astype(np.uint64)
+            assert cnt[p] == want.size and np.array_equal(got, want), (name, p, a, b)
+    return bt
+
+
+@pytest.mark.gpu
+def test_setop_batch_corpus_small(lc):
+    lists, eps, pairs = make_corpus(m=2000, seed=12, n_max=100_000, pairs=600)
+    blobs = [lc.encode(k, e) for k, e in zip(lists, eps)]
+    # plus pairs with shared keys (subsets, identical lists, single keys)
+    rng = np.random.default_rng(5)
+    big = int(np.argmax([k.size for k in lists]))
+    sub = np.unique(np.concatenate([lists[big][::7], rng.integers(0, 1 << 32, 500, dtype=np.uint64).astype(np.uint32)]))
+    lists.append(sub)
+    blobs.append(lc.encode(sub, 1023))
+    lists.append(lists[big][:1].copy())
+    blobs.append(lc.encode(lists[-1], 0))
+    extra = np.array([[len(lists) - 2, big], [big, len(lists) - 2], [big, big], [len(lists) - 1, big],
+                      [len(lists) - 1, len(lists) - 1]])
+    _setop_check(lc, lists, blobs, np.concatenate([pairs, extra]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [3, 4])
+def test_setop_batch_fuzz_u64_free(lc, seed):
+    """u64 lists with F4 and F7 blobs, eps from 0 to 2^30 - 1; overlapping lists (one list's
+    subset plus noise) so intersections are not empty."""
+    rng = np.random.default_rng(seed)
+    base = make_keys(5, 200_000)
+    lists, blobs = [], []
+    for k in range(40):
+        take = np.sort(rng.choice(base.size, int(rng.integers(1, 50_000)), replace=False))
+        noise = rng.integers(0, int(base[-1]), int(rng.integers(0, 3000)), dtype=np.uint64)
+        keys = np.unique(np.concatenate([base[take], noise]))
+        e = int(rng.choice([0, 1, 31, 127, 4095, (1 << 30) - 1]))
+        lists.append(keys)
+        blobs.append(lc.encode(keys, e, free=bool(k % 2)))
+    pairs = rng.integers(0, len(lists), (200, 2))
+    _setop_check(lc, lists, blobs, pairs)

@@ -56,6 +56,28 @@ def main():
            "batch_ms": ms, "batch_GBps": alg / ms / 1e6, "batch_keys_per_s": bt.n_total / ms * 1e3,
            "gen_s": t_gen, "encode_s": t_enc, "sparse": int(bt.b.sparse),
            "max_res_bits": int(bt.b.max_res_bits)}
+    # where the time goes: the corpus cut by list length, each class one batch
+    sizes = np.array([x.size for x in lists])
+    res["classes"] = {}
+    for name, lo, hi in (("n<=64", 0, 64), ("64<n<1024", 65, 1023), ("n>=1024", 1024, 1 << 40)):
+        idx = np.flatnonzero((sizes >= lo) & (sizes <= hi))
+        sb = lc.Batch([blobs[i] for i in idx], device=dev)
+        so = lc.decode_batch(sb)
+        for _ in range(3):
+            lc.decode_batch(sb, so)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            lc.decode_batch(sb, so)
+        e1.record()
+        torch.cuda.synchronize()
+        cms = e0.elapsed_time(e1) / args.reps
+        calg = sb.b.payload_bytes + sb.n_total * 4
+        res["classes"][name] = {"lists": int(idx.size), "keys": sb.n_total, "ms": cms,
+                                "GBps": calg / cms / 1e6, "chunks": int(sb.b.n_chunks),
+                                "small": int(sb.b.n_small)}
+        del sb, so
     # one launch per list (the same kernels through lc_decode) for the first per_list lists
     k = min(args.per_list, len(blobs))
     views = [lc.View(b, device=dev) for b in blobs[:k]]
