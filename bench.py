@@ -360,6 +360,63 @@ def _free_block(keys, dev, stream, reps, peak):
     }
 
 
+def _corpus_block(dev, stream, reps, peak, no_cpu):
+    """NEXT-2's posting-list corpus (synth/corpus.py): 1e5 lists with Zipf-like lengths 10..1e6
+    and per-list eps, decoded in one lc_decode_batch launch; 1e4 AND / OR pairs in one
+    lc_intersect_batch / lc_union_batch call each.  Decode GB/s counts the lists' payload bytes
+    (header + sections without alignment padding) read once plus the keys written once."""
+    import torch
+
+    from paper_2412_10770_b200 import lc
+    from synth import make_corpus
+    lists, eps, pairs = make_corpus()
+    blobs = [lc.encode(k, e) for k, e in zip(lists, eps)]
+    bt = lc.Batch(blobs, device=dev)
+    out = torch.empty(bt.n_total, dtype=torch.int32, device=dev)
+    ia = lc.SetopBuffers(bt, pairs, lc.LC_SETOP_AND)
+    ua = lc.SetopBuffers(bt, pairs, lc.LC_SETOP_OR)
+    with torch.cuda.stream(stream):
+        _, pd = _time_launches(lambda: lc.decode_batch(bt, out, stream=stream), stream, reps, 3)
+        _, pi = _time_launches(lambda: lc.intersect_batch(bt, bufs=ia, stream=stream), stream,
+                               reps, 2)
+        _, pu = _time_launches(lambda: lc.union_batch(bt, bufs=ua, stream=stream), stream, reps, 2)
+    want = torch.from_numpy(np.concatenate(lists).view(np.int32)).to(dev)
+    ok = bool(torch.equal(out, want))
+    del want
+    # AND / OR results of a sample of pairs against numpy's set definitions, all the counts
+    from oracle import setops
+    rng = np.random.default_rng(3)
+    io, ic = ia.out_off.cpu().numpy(), ia.counts.cpu().numpy()
+    uo, uc = ua.out_off.cpu().numpy(), ua.counts.cpu().numpy()
+    iout, uout = ia.out.cpu().numpy().view(np.uint32), ua.out.cpu().numpy().view(np.uint32)
+    for p in rng.choice(len(pairs), 300, replace=False):
+        a, b = lists[pairs[p][0]], lists[pairs[p][1]]
+        wi, wu = setops.intersect(a, b), setops.union(a, b)
+        ok &= ic[p] == wi.size and np.array_equal(iout[io[p]:io[p] + ic[p]], wi)
+        ok &= uc[p] == wu.size and np.array_equal(uout[uo[p]:uo[p] + uc[p]], wu)
+    sz = np.array([k.size for k in lists])
+    ok &= int(uc.sum()) == int(sz[pairs].sum()) - int(ic.sum())  # |A u B| = |A| + |B| - |A n B|
+    if not ok:
+        raise SystemExit("corpus batch mismatch")
+    md, mi, mu = statistics.mean(pd), statistics.mean(pi), statistics.mean(pu)
+    alg = bt.b.payload_bytes + bt.n_total * 4
+    res = {
+        "workload": "posting-list corpus: 1e5 u32 lists, lengths min(floor(10 U^(-1/0.7)), 1e6) "
+                    "(seed 10), docIDs a uniform sorted sample of [0, 2^32), per-list eps "
+                    "2^(ceil(log2(2^32/n)) + 2) - 1; 1e4 query pairs, terms ~ n^0.25",
+        "lists": int(bt.b.m), "keys": int(bt.n_total), "chunks": int(bt.b.n_chunks),
+        "payload_bytes": int(bt.b.payload_bytes), "bits_per_int": 8 * bt.b.payload_bytes / bt.n_total,
+        "decode_ms": md * 1e3, "decode_GBps": alg / md / 1e9, "decode_keys_per_s": bt.n_total / md,
+        "decode_frac": alg / md / 1e9 / peak, "launches_per_decode": 1,
+        "pairs": int(len(pairs)), "and_ms": mi * 1e3, "and_pairs_per_s": len(pairs) / mi,
+        "and_short_keys": int(np.minimum(sz[pairs[:, 0]], sz[pairs[:, 1]]).sum()),
+        "and_matches": int(ic.sum()),
+        "or_ms": mu * 1e3, "or_pairs_per_s": len(pairs) / mu, "or_keys_out": int(uc.sum()),
+        "bit_exact": True,
+    }
+    return res
+
+
 def _access_block(dev, stream, reps, no_cpu):
     """Config 5: random access, range decodes, quantiles, successor search, intersection and
     union (with and without the successor-search index), each verified."""
@@ -385,6 +442,24 @@ def _access_block(dev, stream, reps, no_cpu):
     del d5, sel
     if not (ok_a and ok_r):
         raise SystemExit("access/range mismatch")
+    # the access layout (lc_access_layout_build): directory instead of the binary search,
+    # params and residual field from one record
+    lay_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    lay = v5.build_access_layout(stream=stream)
+    with torch.cuda.stream(stream):
+        lay_ev[0].record(stream)
+        v5.build_access_layout(stream=stream, out=lay)
+        lay_ev[1].record(stream)
+        a_out.zero_()
+        _, pal = _time_launches(lambda: lc.access(v5, d_idx, a_out, stream=stream), stream, reps, 2)
+    torch.cuda.synchronize()
+    d5 = torch.from_numpy(k5.view(np.int64)).to(dev)
+    if not torch.equal(a_out, d5[d_idx]):
+        raise SystemExit("access (layout) mismatch")
+    del d5
+    layout = {"bytes": v5.access_layout_bytes(), "build_ms": lay_ev[0].elapsed_time(lay_ev[1]),
+              "lookups_per_s": idx.size / statistics.mean(pal),
+              "ns_per_lookup": statistics.mean(pal) / idx.size * 1e9}
     # NEXT-1 quantiles and NEXT-2 successor search / intersection / union on the same list
     qrng = np.random.default_rng(55)
     mq = 10_000_000
@@ -411,6 +486,12 @@ def _access_block(dev, stream, reps, no_cpu):
                                                     stream=stream), stream, reps, 2)
         _, pqa = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, False, q_out,
                                                     stream=stream), stream, reps, 2)
+    v5.d_acc, v5.v.d_acc = None, None  # quantiles again without the layout
+    with torch.cuda.stream(stream):
+        _, pqe0 = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, True, q_out,
+                                                     stream=stream), stream, reps, 2)
+        _, pqa0 = _time_launches(lambda: lc.quantile(v5, d_ranks, (1 << 32) - 1, False, q_out,
+                                                     stream=stream), stream, reps, 2)
         _, png = _time_launches(lambda: lc.next_geq(v5, d_probe, p_idx, p_key, stream=stream),
                                 stream, reps, 2)
         _, pis = _time_launches(lambda: lc.intersect(va, v5, i_scr, i_out, i_cnt, stream=stream),
@@ -451,13 +532,17 @@ def _access_block(dev, stream, reps, no_cpu):
         "workload": "config5: N=1e8 u64 keys, gaps uniform [1,256], eps=127; 1e8 uniform "
                     "lookups; 1e7 ranges x 64 keys",
         "cpu_oracle": cpu_rows,
-        "lookups_per_s": idx.size / statistics.mean(pa),
-        "ns_per_lookup": statistics.mean(pa) / idx.size * 1e9,
+        "lookups_per_s": idx.size / statistics.mean(pal),
+        "ns_per_lookup": statistics.mean(pal) / idx.size * 1e9,
+        "lookups_per_s_no_layout": idx.size / statistics.mean(pa),
+        "access_layout": layout,
         "ranges_per_s": rs.size / statistics.mean(pr),
         "range_keys_per_s": rs.size * 64 / statistics.mean(pr),
         "range_out_GBps": rs.size * 64 * 8 / statistics.mean(pr) / 1e9,
         "quantiles_exact_per_s": mq / statistics.mean(pqe),
         "quantiles_approx_per_s": mq / statistics.mean(pqa),
+        "quantiles_exact_per_s_no_layout": mq / statistics.mean(pqe0),
+        "quantiles_approx_per_s_no_layout": mq / statistics.mean(pqa0),
         "next_geq_per_s": mq / statistics.mean(png),
         "intersect": {"a_keys": int(a_keys.size), "b_keys": int(k5.size),
                       "matches": want_cnt, "ms": statistics.mean(pis) * 1e3,
@@ -668,6 +753,11 @@ def run_gpu(args):
                            max(5, min(args.steps, 50)), peak)
     del keys2
 
+    # ---- NEXT-2: the posting-list corpus (batched decode, AND / OR pairs)
+    corpus = None
+    if ws == 1 and not args.no_corpus:
+        corpus = _corpus_block(dev, stream, max(5, min(args.steps, 20)), peak, args.no_cpu)
+
     # ---- random access + range decodes (config 5), reported beside the headline
     access = None
     if ws == 1 and not args.no_access:
@@ -704,6 +794,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "decode_configs": decode_configs or None,
         "access": access,
+        "corpus": corpus,
         "free_intercept": free,
     }
     if ws == 1 and not args.no_cpu:
@@ -724,6 +815,7 @@ def main():
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the decode_configs lines of the other 1e8+ configs")
     ap.add_argument("--no-access", action="store_true")
+    ap.add_argument("--no-corpus", action="store_true", help="skip the posting-list corpus block")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-free", action="store_true", help="skip the FORMAT F7 block")
     args = ap.parse_args()

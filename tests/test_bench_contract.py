@@ -38,7 +38,7 @@ def test_reference_arm_line():
 @pytest.mark.gpu
 def test_product_arm_line():
     d = _run("--config", "1", "--steps", "5", "--warmup", "3", "--no-access", "--no-cpu",
-             "--no-free", "--no-configs")
+             "--no-free", "--no-configs", "--no-corpus")
     assert BASE_KEYS - {"cpu_baseline"} <= set(d)
     assert {"roofline", "gpu_launches", "clocks"} <= set(d)
     assert d["value"] > 0 and d["gpu_launches"] >= d["steps"]

@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--per-list", type=int, default=2000, help="lists timed one launch each")
+    ap.add_argument("--only-class", default=None, help="time only this length class (for ncu)")
     args = ap.parse_args()
     dev = "cuda:0"
     t0 = time.perf_counter()
@@ -33,6 +34,17 @@ def main():
     t0 = time.perf_counter()
     blobs = [lc.encode(k, e) for k, e in zip(lists, eps)]
     t_enc = time.perf_counter() - t0
+    if args.only_class:
+        sizes = np.array([x.size for x in lists])
+        lo, hi = {"small": (0, 64), "mid": (65, 1023), "big": (1024, 1 << 40)}[args.only_class]
+        idx = np.flatnonzero((sizes >= lo) & (sizes <= hi))
+        sb = lc.Batch([blobs[i] for i in idx], device=dev)
+        so = lc.decode_batch(sb)
+        torch.cuda.synchronize()
+        want = torch.from_numpy(np.concatenate([lists[i] for i in idx]).view(np.int32)).to(dev)
+        assert torch.equal(so[:want.numel()], want)
+        print(json.dumps({"class": args.only_class, "lists": int(idx.size)}))
+        return
     bt = lc.Batch(blobs, device=dev)
     out = lc.decode_batch(bt)
     want = torch.from_numpy(np.concatenate(lists).view(np.int32)).to(dev)
