@@ -299,8 +299,10 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
                       uint64_t dir_bytes, lc_stream stream);
 
 /* Decode every list of the batch in one launch: list k's keys to d_out[out_off[k] ..
- * out_off[k] + n_k) (elements of key_bits / 8 bytes).  Dec(K^c) per list (Def. 1). */
-int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream);
+ * out_off[k] + n_k) (elements of key_bits / 8 bytes).  Dec(K^c) per list (Def. 1).
+ * d_work: a caller-owned 4-byte device counter (the launch's work queue), zeroed on `stream`
+ * by the call; concurrent calls need distinct counters. */
+int32_t lc_decode_batch(const lc_batch* b, void* d_out, uint32_t* d_work, lc_stream stream);
 
 /* Batched AND / OR queries (inverted-index processing, §III-A, Fig. 4):
  * pair p = (h_pairs[2 p], h_pairs[2 p + 1]) names two lists of the batch; h_n[k] is list k's

@@ -412,6 +412,7 @@ struct BatchArgs {
     const uint64_t* sel_out;   // ... to output element offset sel_out[c] (both or neither)
     void* out;
     const uint32_t* nunits;    // optional device count of units (overrides `units` when set)
+    uint32_t* work;            // work-queue counter, zero at launch
     uint32_t units;            // chunks to decode (the batch's, or the selection's)
     uint32_t small0;           // units [small0, units) are small (<= kSmallUnit keys): one lane each
     uint32_t warp_bytes;       // shared memory per warp (widest b of the batch)
@@ -462,54 +463,68 @@ __global__ void __launch_bounds__(kThreads, 4)
     ins.rho = nullptr;
 
     const uint32_t big = a.sel ? units : min(a.small0, units);
-    // ---- small units, one per lane (their records are at the end of the batch's array)
-    for (uint32_t u = big + (blockIdx.x * kWarpsPerCta + warp) * 32 + lane; u < units;
-         u += nwarps * 32) {
-        const BatchChunk r = load_chunk(a.chunks + u);
-        const uint8_t* blob = (const uint8_t*)r.blob;
-        const uint32_t* S = (const uint32_t*)(blob + 256);
-        const ulonglong2* P = (const ulonglong2*)(blob + r.off_params);
-        const uint32_t* W = (const uint32_t*)(blob + r.off_words);
-        const uint32_t nk = r.nk_b & 0xffff, b = r.nk_b >> 16;
-        const uint32_t mask = b >= 32 ? kFull : (1u << b) - 1;
-        uint32_t j = r.j0, s0 = __ldg(S + j), e = __ldg(S + j + 1);
-        ulonglong2 pr = __ldg(P + j);
-        uint8_t* o = (uint8_t*)a.out + r.out * kw;
-        for (uint32_t k = 0; k < nk; ++k) {
-            const uint32_t i = r.key0 + k;
-            while (i >= e) {  // next segment
-                ++j;
-                s0 = e;
-                e = __ldg(S + j + 1);
-                pr = __ldg(P + j);
-            }
-            uint32_t uf = 0;
-            if (b) {
-                const uint64_t bit = (uint64_t)i * b;
-                const uint32_t* wp = W + (bit >> 5);
-                uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & mask;
-            }
-            const uint32_t t = pred_plus(pr.y, i - s0, uf - r.bias);
-            if (K64) __stcs((unsigned long long*)o + k, (unsigned long long)(pr.x + t));
-            else __stcs((unsigned int*)o + k, (unsigned int)pr.x + t);
-        }
-    }
-
-    // ---- the other units, one per warp (1024-key chunks and longer partial chunks)
-    uint32_t c = blockIdx.x * kWarpsPerCta + warp;
-    BatchChunk nr;  // the warp's next chunk record, loaded one chunk ahead
+    const uint32_t ngroups = (units - big + 31) / 32;  // small units, 32 per group
+    const uint32_t items = ngroups + big;
+    // Work queue (a.work, zeroed before the launch): items [0, ngroups) are groups of 32 small
+    // units (one lane each), then the big units (one warp each).  Warps take items as they
+    // finish, so the latency-bound small groups overlap with other warps' chunk decodes instead
+    // of delaying a fixed share of them.
+    auto grab = [&]() {
+        uint32_t v = 0;
+        if (lane == 0) v = atomicAdd(a.work, 1u);
+        return __shfl_sync(kFull, v, 0);
+    };
+    auto load_big = [&](uint32_t item, BatchChunk& rr, uint64_t& oo) {
+        const uint32_t cc = item - ngroups;
+        rr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + cc) : cc));
+        oo = a.sel ? __ldg(a.sel_out + cc) : rr.out;
+    };
+    uint32_t item = grab();
+    BatchChunk nr;  // the record of `item` when it is a big unit (loaded one item ahead)
     uint64_t nout = 0;
-    if (c < big) {
-        nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c) : c));
-        nout = a.sel ? __ldg(a.sel_out + c) : nr.out;
-    }
-    for (; c < big; c += nwarps) {
+    if (item >= ngroups && item < items) load_big(item, nr, nout);
+    while (item < items) {
+        const uint32_t nitem = grab();
+        if (item < ngroups) {  // ---- a group of 32 small units, one per lane
+            const uint32_t u = big + item * 32 + lane;
+            if (nitem >= ngroups && nitem < items) load_big(nitem, nr, nout);
+            item = nitem;
+            if (u >= units) continue;
+            const BatchChunk r = load_chunk(a.chunks + u);
+            const uint8_t* blob = (const uint8_t*)r.blob;
+            const uint32_t* S = (const uint32_t*)(blob + 256);
+            const ulonglong2* P = (const ulonglong2*)(blob + r.off_params);
+            const uint32_t* W = (const uint32_t*)(blob + r.off_words);
+            const uint32_t nk = r.nk_b & 0xffff, b = r.nk_b >> 16;
+            const uint32_t mask = b >= 32 ? kFull : (1u << b) - 1;
+            uint32_t j = r.j0, s0 = __ldg(S + j), e = __ldg(S + j + 1);
+            ulonglong2 pr = __ldg(P + j);
+            uint8_t* o = (uint8_t*)a.out + r.out * kw;
+            for (uint32_t k = 0; k < nk; ++k) {
+                const uint32_t i = r.key0 + k;
+                while (i >= e) {  // next segment
+                    ++j;
+                    s0 = e;
+                    e = __ldg(S + j + 1);
+                    pr = __ldg(P + j);
+                }
+                uint32_t uf = 0;
+                if (b) {
+                    const uint64_t bit = (uint64_t)i * b;
+                    const uint32_t* wp = W + (bit >> 5);
+                    uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & mask;
+                }
+                const uint32_t t = pred_plus(pr.y, i - s0, uf - r.bias);
+                if (K64) __stcs((unsigned long long*)o + k, (unsigned long long)(pr.x + t));
+                else __stcs((unsigned int*)o + k, (unsigned int)pr.x + t);
+            }
+            continue;
+        }
+        // ---- a big unit, one warp (1024-key chunks and longer partial chunks)
         const BatchChunk r = nr;
         const uint64_t out0 = nout;
-        if (c + nwarps < big) {
-            nr = load_chunk(a.chunks + (a.sel ? __ldg(a.sel + c + nwarps) : c + nwarps));
-            nout = a.sel ? __ldg(a.sel_out + c + nwarps) : nr.out;
-        }
+        if (nitem >= ngroups && nitem < items) load_big(nitem, nr, nout);
+        item = nitem;
         const uint8_t* blob = (const uint8_t*)r.blob;
         Sections sec;
         sec.starts = (const uint32_t*)(blob + 256);

@@ -134,8 +134,11 @@ const void* batch_kernel(bool k64, bool sparse) {
 }
 
 int32_t launch_batch_decode(const lc_batch* b, const uint32_t* sel, const uint64_t* sel_out,
-                            const uint32_t* nunits, uint32_t units, void* d_out, cudaStream_t st) {
+                            const uint32_t* nunits, uint32_t units, void* d_out, uint32_t* work,
+                            cudaStream_t st) {
+    if (cudaMemsetAsync(work, 0, sizeof(uint32_t), st) != cudaSuccess) return LC_ERR_CUDA;
     BatchArgs a;
+    a.work = work;
     a.small0 = sel ? units : (uint32_t)(b->n_chunks - b->n_small);
     a.chunks = (const BatchChunk*)b->d_chunks;
     a.sel = sel;
@@ -154,7 +157,7 @@ int32_t launch_batch_decode(const lc_batch* b, const uint32_t* sel, const uint64
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
     const uint32_t full = (uint32_t)(sms * (occ > 0 ? occ : 1));
     const uint32_t need = (units + kWarpsPerCta - 1) / kWarpsPerCta;
-    const uint32_t grid = nunits ? full : (need < full ? need : full);
+    const uint32_t grid = nunits ? full : (need + 1 < full ? need + 1 : full);
     if (!grid) return LC_OK;
     void* args[] = {&a};
     if (cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st) != cudaSuccess)
@@ -916,7 +919,7 @@ int32_t setop_batch(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_p
         return LC_ERR_CUDA;
     if ((rc = launch_batch_decode(bt, (const uint32_t*)(D + y.o_sel),
                                   (const uint64_t*)(D + y.o_selout), nullptr, (uint32_t)y.U,
-                                  D + y.o_keys, st)))
+                                  D + y.o_keys, (uint32_t*)(D + y.o_total + 8), st)))
         return rc;
     const bool k64 = bt->key_bits == 64;
     SetopArgs a;
@@ -992,10 +995,12 @@ int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h
                        d_counts, (cudaStream_t)stream);
 }
 
-int32_t lc_decode_batch(const lc_batch* b, void* d_out, lc_stream stream) {
-    if (!b || !b->d_chunks || !d_out || ((uintptr_t)d_out % (b->key_bits / 8))) return LC_ERR_ARG;
+int32_t lc_decode_batch(const lc_batch* b, void* d_out, uint32_t* d_work, lc_stream stream) {
+    if (!b || !b->d_chunks || !d_out || ((uintptr_t)d_out % (b->key_bits / 8)) || !d_work ||
+        ((uintptr_t)d_work & 3))
+        return LC_ERR_ARG;
     if (!b->n_chunks) return LC_OK;
-    return launch_batch_decode(b, nullptr, nullptr, nullptr, (uint32_t)b->n_chunks, d_out,
+    return launch_batch_decode(b, nullptr, nullptr, nullptr, (uint32_t)b->n_chunks, d_out, d_work,
                                (cudaStream_t)stream);
 }
 

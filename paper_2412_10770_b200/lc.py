@@ -77,7 +77,7 @@ _sig = {
     "lc_shard_upload": ([_p, _u64, _u64, _u64, _p, _u64, C.POINTER(lc_view), _p], _i32),
     "lc_batch_dir_bytes": ([_p, _u64, _p, _u32, C.POINTER(_u64)], _i32),
     "lc_batch_init": ([C.POINTER(lc_batch), _p, _u64, _p, _u32, _p, _p, _p, _u64, _p], _i32),
-    "lc_decode_batch": ([C.POINTER(lc_batch), _p, _p], _i32),
+    "lc_decode_batch": ([C.POINTER(lc_batch), _p, _p, _p], _i32),
     "lc_setop_batch_scratch_bytes": ([C.POINTER(lc_batch), _p, _p, _u32, _i32, C.POINTER(_u64),
                                       C.POINTER(_u64)], _i32),
     "lc_intersect_batch": ([C.POINTER(lc_batch), _p, _p, _u32, _p, _u64, _p, _p, _p, _p], _i32),
@@ -494,6 +494,7 @@ class Batch:
                                       None if oo is None else oo.ctypes.data,
                                       self.d_dir.data_ptr(), self.d_dir.numel(), on.handle),
                    "lc_batch_init")
+            self.d_work = on.use(torch.zeros(4, dtype=torch.int32, device=device))
         headers = [lc_header.from_buffer_copy(bl[:128]) for bl in blobs]
         self.n = np.array([h.n for h in headers], np.int64)
         self.out_off = (np.concatenate([[0], np.cumsum(self.n)[:-1]]).astype(np.int64)
@@ -509,7 +510,7 @@ class Batch:
         return torch.int64 if self.b.key_bits == 64 else torch.int32
 
     def tensors(self):
-        return (self.d_blobs, self.d_dir)
+        return (self.d_blobs, self.d_dir, self.d_work)
 
 
 def decode_batch(batch: Batch, out=None, stream=None):
@@ -521,8 +522,8 @@ def decode_batch(batch: Batch, out=None, stream=None):
             size = int((batch.out_off + batch.n).max()) if batch.m else 0
             out = torch.empty(max(size, 1), dtype=batch.torch_dtype, device=batch.d_blobs.device)
         on.use(out)
-        _check(_lib.lc_decode_batch(C.byref(batch.b), out.data_ptr(), on.handle),
-               "lc_decode_batch")
+        _check(_lib.lc_decode_batch(C.byref(batch.b), out.data_ptr(), batch.d_work.data_ptr(),
+                                    on.handle), "lc_decode_batch")
     return out
 
 
