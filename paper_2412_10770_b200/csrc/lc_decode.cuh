@@ -500,6 +500,21 @@ __global__ void __launch_bounds__(kThreads, 4)
             uint32_t j = r.j0, s0 = __ldg(S + j), e = __ldg(S + j + 1);
             ulonglong2 pr = __ldg(P + j);
             uint8_t* o = (uint8_t*)a.out + r.out * kw;
+            // residual fields through a 64-bit bit buffer refilled from words fetched two ahead,
+            // so no iteration waits on its own load (words [wi, wend) hold the unit's bits)
+            const uint64_t bit0 = (uint64_t)r.key0 * b;
+            const uint32_t wend = (uint32_t)((bit0 + (uint64_t)nk * b + 31) >> 5);
+            uint32_t wi = (uint32_t)(bit0 >> 5);
+            uint64_t buf = 0;
+            uint32_t have = 64, n1 = 0, n2 = 0;
+            if (b) {
+                const uint32_t w0 = __ldg(W + wi), w1 = wi + 1 < wend ? __ldg(W + wi + 1) : 0;
+                n1 = wi + 2 < wend ? __ldg(W + wi + 2) : 0;
+                n2 = wi + 3 < wend ? __ldg(W + wi + 3) : 0;
+                buf = (((uint64_t)w1 << 32) | w0) >> (bit0 & 31);
+                have = 64 - (uint32_t)(bit0 & 31);
+                wi += 4;
+            }
             for (uint32_t k = 0; k < nk; ++k) {
                 const uint32_t i = r.key0 + k;
                 while (i >= e) {  // next segment
@@ -508,12 +523,16 @@ __global__ void __launch_bounds__(kThreads, 4)
                     e = __ldg(S + j + 1);
                     pr = __ldg(P + j);
                 }
-                uint32_t uf = 0;
-                if (b) {
-                    const uint64_t bit = (uint64_t)i * b;
-                    const uint32_t* wp = W + (bit >> 5);
-                    uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) & mask;
+                if (have < b) {  // have + 32 <= 64: the next word fits above the buffered bits
+                    buf |= (uint64_t)n1 << have;
+                    have += 32;
+                    n1 = n2;
+                    n2 = wi < wend ? __ldg(W + wi) : 0;
+                    ++wi;
                 }
+                const uint32_t uf = (uint32_t)buf & mask;
+                buf = b < 64 ? buf >> b : 0;
+                have -= b;
                 const uint32_t t = pred_plus(pr.y, i - s0, uf - r.bias);
                 if (K64) __stcs((unsigned long long*)o + k, (unsigned long long)(pr.x + t));
                 else __stcs((unsigned int*)o + k, (unsigned int)pr.x + t);
@@ -545,16 +564,17 @@ __global__ void __launch_bounds__(kThreads, 4)
         uint32_t jb = r.j0, sb = pg.sS[LC_BOUND(true, r.j0 - pg.pj, pg.cs)];
         uint8_t* outl = (uint8_t*)a.out + (out0 + lane) * kw;
         const uint32_t key0 = r.key0, jlast = r.jlast;
-        if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged
+        if (jlast < pg.pj + pg.cp) {  // every segment of the unit staged: no re-page checks
+            const uint32_t nq = nk >> 7;  // whole 128-key quads
 #pragma unroll 1
-            for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
-#pragma unroll
-                for (uint32_t k = 0; k < 2; ++k)
-                    decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast,
-                                                                 key0 + 128 * (g + k), g + k, lane,
-                                                                 lmask, lw, ls, r.bias,
-                                                                 outl + 128 * kw * k, ins);
-            }
+            for (uint32_t g = 0; g < nq; ++g, outl += 128 * kw)
+                decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * g,
+                                                             g, lane, lmask, lw, ls, r.bias, outl,
+                                                             ins);
+            for (uint32_t w = 4 * nq; 32 * w < nk; ++w, outl += 32 * kw)
+                decode_window<K64, kRtB, false, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
+                                                              w, lane, lmask, lw, ls, r.bias, outl,
+                                                              nk - 32 * w, ins);
         } else if (nk == 1024) {  // dense chunk: paged
 #pragma unroll 1
             for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
@@ -564,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 4)
                                                         g + k, lane, lmask, lw, ls, r.bias,
                                                         outl + 64 * kw * k, ins);
             }
-        } else {  // a list's last (partial) chunk: short lists are only this
+        } else {  // a dense partial chunk (a list's last)
             for (uint32_t w = 0; 32 * w < nk; ++w)
                 decode_window<K64, kRtB, true, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
                                                              w, lane, lmask, lw, ls, r.bias,
