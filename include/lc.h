@@ -275,10 +275,13 @@ typedef struct lc_batch {
     uint64_t n_total;       /* keys over all lists */
     uint64_t n_chunks;      /* 1024-key chunks over all lists (a list's last one may be partial) */
     uint64_t n_small;       /* of which partial chunks of <= 64 keys (records stored last) */
+    uint64_t small_keys;    /* keys in those small chunks */
     uint64_t payload_bytes; /* bytes of the lists' headers and sections, without the 256-byte
                                alignment padding: what a decode reads */
     const void* d_lists;    /* device directory: m list records (64 B each) ... */
-    const void* d_chunks;   /* ... then n_chunks chunk records (48 B each) */
+    const void* d_chunks;   /* ... then n_chunks chunk records (48 B each) ... */
+    const void* d_small;    /* ... then the small chunks' key prefix (n_small + 1 uint32) and the
+                               small chunk of every 32nd small key (ceil(small_keys / 32)) */
 } lc_batch;
 
 /* Directory bytes of the batch of m blobs at host byte offsets blob_off[k] of h_blobs (each a

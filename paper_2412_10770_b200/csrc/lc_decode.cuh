@@ -414,14 +414,20 @@ struct BatchArgs {
     const uint32_t* nunits;    // optional device count of units (overrides `units` when set)
     uint32_t* work;            // work-queue counter, zero at launch
     uint32_t units;            // chunks to decode (the batch's, or the selection's)
-    uint32_t small0;           // units [small0, units) are small (<= kSmallUnit keys): one lane each
+    uint32_t small0;           // units [small0, units) are small (<= kSmallUnit keys) ...
+    const uint32_t* sk0;       // ... their keys flattened: small unit u holds flat keys
+                               //     [sk0[u], sk0[u + 1]), ...
+    const uint32_t* sblk;      // ... sblk[f / 32] = the small unit holding flat key f (f % 32 == 0)
+    uint32_t small_keys;       // flat small keys (0: no small path)
     uint32_t warp_bytes;       // shared memory per warp (widest b of the batch)
 };
 
 // Small units (a posting list of <= 64 keys is one, and most lists of a Zipf vocabulary are
-// that short): one LANE decodes a whole unit serially from global memory (L1), so a warp
-// serves 32 of them at once instead of paying a staging round trip per list.
+// that short): their keys are flattened into one index space and decoded one THREAD per key
+// from global memory (L1 / L2), 256 keys per work item, instead of one staging round trip per
+// list.
 constexpr uint32_t kSmallUnit = 64;
+constexpr uint32_t kSmallItem = 256;  // flat small keys per work item (8 per lane)
 
 __device__ __forceinline__ BatchChunk load_chunk(const BatchChunk* p) {
     BatchChunk r;
@@ -463,12 +469,11 @@ __global__ void __launch_bounds__(kThreads, 4)
     ins.rho = nullptr;
 
     const uint32_t big = a.sel ? units : min(a.small0, units);
-    const uint32_t ngroups = (units - big + 31) / 32;  // small units, 32 per group
+    const uint32_t ngroups = (a.small_keys + kSmallItem - 1) / kSmallItem;  // small-key items
     const uint32_t items = ngroups + big;
-    // Work queue (a.work, zeroed before the launch): items [0, ngroups) are groups of 32 small
-    // units (one lane each), then the big units (one warp each).  Warps take items as they
-    // finish, so the latency-bound small groups overlap with other warps' chunk decodes instead
-    // of delaying a fixed share of them.
+    // Work queue (a.work, zeroed before the launch): items [0, ngroups) are 256 flat small keys
+    // each, then the big units (one warp each).  Warps take items as they finish, so the
+    // latency-bound small keys overlap with other warps' chunk decodes.
     auto grab = [&]() {
         uint32_t v = 0;
         if (lane == 0) v = atomicAdd(a.work, 1u);
@@ -485,57 +490,35 @@ __global__ void __launch_bounds__(kThreads, 4)
     if (item >= ngroups && item < items) load_big(item, nr, nout);
     while (item < items) {
         const uint32_t nitem = grab();
-        if (item < ngroups) {  // ---- a group of 32 small units, one per lane
-            const uint32_t u = big + item * 32 + lane;
+        if (item < ngroups) {  // ---- 256 flat small keys: 8 per lane, consecutive per warp step
+            const uint32_t f0 = item * kSmallItem;
             if (nitem >= ngroups && nitem < items) load_big(nitem, nr, nout);
             item = nitem;
-            if (u >= units) continue;
-            const BatchChunk r = load_chunk(a.chunks + u);
-            const uint8_t* blob = (const uint8_t*)r.blob;
-            const uint32_t* S = (const uint32_t*)(blob + 256);
-            const ulonglong2* P = (const ulonglong2*)(blob + r.off_params);
-            const uint32_t* W = (const uint32_t*)(blob + r.off_words);
-            const uint32_t nk = r.nk_b & 0xffff, b = r.nk_b >> 16;
-            const uint32_t mask = b >= 32 ? kFull : (1u << b) - 1;
-            uint32_t j = r.j0, s0 = __ldg(S + j), e = __ldg(S + j + 1);
-            ulonglong2 pr = __ldg(P + j);
-            uint8_t* o = (uint8_t*)a.out + r.out * kw;
-            // residual fields through a 64-bit bit buffer refilled from words fetched two ahead,
-            // so no iteration waits on its own load (words [wi, wend) hold the unit's bits)
-            const uint64_t bit0 = (uint64_t)r.key0 * b;
-            const uint32_t wend = (uint32_t)((bit0 + (uint64_t)nk * b + 31) >> 5);
-            uint32_t wi = (uint32_t)(bit0 >> 5);
-            uint64_t buf = 0;
-            uint32_t have = 64, n1 = 0, n2 = 0;
-            if (b) {
-                const uint32_t w0 = __ldg(W + wi), w1 = wi + 1 < wend ? __ldg(W + wi + 1) : 0;
-                n1 = wi + 2 < wend ? __ldg(W + wi + 2) : 0;
-                n2 = wi + 3 < wend ? __ldg(W + wi + 3) : 0;
-                buf = (((uint64_t)w1 << 32) | w0) >> (bit0 & 31);
-                have = 64 - (uint32_t)(bit0 & 31);
-                wi += 4;
-            }
-            for (uint32_t k = 0; k < nk; ++k) {
-                const uint32_t i = r.key0 + k;
-                while (i >= e) {  // next segment
-                    ++j;
-                    s0 = e;
-                    e = __ldg(S + j + 1);
-                    pr = __ldg(P + j);
+            uint32_t u = __ldg(a.sblk + (f0 >> 5));
+#pragma unroll 1
+            for (uint32_t q = 0; q < kSmallItem / 32; ++q) {
+                const uint32_t f = f0 + 32 * q + lane;
+                if (f >= a.small_keys) break;
+                while (__ldg(a.sk0 + u + 1) <= f) ++u;  // the unit holding flat key f
+                const BatchChunk r = load_chunk(a.chunks + big + u);
+                const uint32_t k = f - __ldg(a.sk0 + u), i = r.key0 + k;
+                const uint8_t* blob = (const uint8_t*)r.blob;
+                const uint32_t* S = (const uint32_t*)(blob + 256);
+                uint32_t j = r.j0;
+                while (j < r.jlast && __ldg(S + j + 1) <= i) ++j;  // its segment (few)
+                const ulonglong2 pr = __ldg((const ulonglong2*)(blob + r.off_params) + j);
+                const uint32_t b = r.nk_b >> 16;
+                uint32_t uf = 0;
+                if (b) {
+                    const uint64_t bit = (uint64_t)i * b;
+                    const uint32_t* wp = (const uint32_t*)(blob + r.off_words) + (bit >> 5);
+                    uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) &
+                         (b >= 32 ? kFull : (1u << b) - 1);
                 }
-                if (have < b) {  // have + 32 <= 64: the next word fits above the buffered bits
-                    buf |= (uint64_t)n1 << have;
-                    have += 32;
-                    n1 = n2;
-                    n2 = wi < wend ? __ldg(W + wi) : 0;
-                    ++wi;
-                }
-                const uint32_t uf = (uint32_t)buf & mask;
-                buf = b < 64 ? buf >> b : 0;
-                have -= b;
-                const uint32_t t = pred_plus(pr.y, i - s0, uf - r.bias);
-                if (K64) __stcs((unsigned long long*)o + k, (unsigned long long)(pr.x + t));
-                else __stcs((unsigned int*)o + k, (unsigned int)pr.x + t);
+                const uint32_t t = pred_plus(pr.y, i - __ldg(S + j), uf - r.bias);
+                uint8_t* o = (uint8_t*)a.out + (r.out + k) * kw;
+                if (K64) __stcs((unsigned long long*)o, (unsigned long long)(pr.x + t));
+                else __stcs((unsigned int*)o, (unsigned int)pr.x + t);
             }
             continue;
         }

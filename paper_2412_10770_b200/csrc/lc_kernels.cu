@@ -140,6 +140,9 @@ int32_t launch_batch_decode(const lc_batch* b, const uint32_t* sel, const uint64
     BatchArgs a;
     a.work = work;
     a.small0 = sel ? units : (uint32_t)(b->n_chunks - b->n_small);
+    a.sk0 = (const uint32_t*)b->d_small;
+    a.sblk = a.sk0 ? a.sk0 + b->n_small + 1 : nullptr;
+    a.small_keys = sel ? 0 : (uint32_t)b->small_keys;
     a.chunks = (const BatchChunk*)b->d_chunks;
     a.sel = sel;
     a.sel_out = sel_out;
@@ -684,9 +687,10 @@ int32_t lc_shard_upload(const void* h_blob, uint64_t blob_bytes, uint64_t i0, ui
 // ---------------------------------------------------------------------------- batches
 namespace {
 int32_t batch_scan(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off, uint32_t m,
-                   uint64_t* n_chunks, uint32_t* key_bits) {
+                   uint64_t* n_chunks, uint32_t* key_bits, uint64_t* n_small = nullptr,
+                   uint64_t* small_keys = nullptr) {
     if (!h_blobs || !blob_off || !m || !n_chunks) return LC_ERR_ARG;
-    uint64_t c = 0;
+    uint64_t c = 0, ns = 0, sk = 0;
     for (uint32_t k = 0; k < m; ++k) {
         if ((blob_off[k] & 255) || blob_off[k] + sizeof(lc_header) > h_bytes) return LC_ERR_ARG;
         lc_header h;
@@ -696,8 +700,15 @@ int32_t batch_scan(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_o
         if (k == 0) *key_bits = h.key_bits;
         else if (h.key_bits != *key_bits) return LC_ERR_ARG;
         c += h.n_hint - 1;
+        const uint64_t tail = h.n & 1023;
+        if (tail && tail <= kSmallUnit) {
+            ++ns;
+            sk += tail;
+        }
     }
     *n_chunks = c;
+    if (n_small) *n_small = ns;
+    if (small_keys) *small_keys = sk;
     return LC_OK;
 }
 }  // namespace
@@ -705,11 +716,12 @@ int32_t batch_scan(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_o
 int32_t lc_batch_dir_bytes(const void* h_blobs, uint64_t h_bytes, const uint64_t* blob_off,
                            uint32_t m, uint64_t* dir_bytes) {
     if (!dir_bytes) return LC_ERR_ARG;
-    uint64_t nc = 0;
+    uint64_t nc = 0, ns = 0, sk = 0;
     uint32_t kb = 0;
-    const int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb);
+    const int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb, &ns, &sk);
     if (st) return st;
-    *dir_bytes = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc;
+    *dir_bytes = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc + 4 * (ns + 1) +
+                 4 * ((sk + 31) / 32);
     return LC_OK;
 }
 
@@ -718,25 +730,23 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
                       uint64_t dir_bytes, lc_stream stream) {
     if (!b || !d_blobs || ((uintptr_t)d_blobs & 255) || !d_dir || ((uintptr_t)d_dir & 15))
         return LC_ERR_ARG;
-    uint64_t nc = 0;
+    uint64_t nc = 0, nsm = 0, skeys = 0;
     uint32_t kb = 0;
-    int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb);
+    int32_t st = batch_scan(h_blobs, h_bytes, blob_off, m, &nc, &kb, &nsm, &skeys);
     if (st) return st;
-    if (nc >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
-    const uint64_t need = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc;
+    if (nc >= (1ULL << 32) || skeys >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
+    const uint64_t o_small = sizeof(BatchList) * (uint64_t)m + sizeof(BatchChunk) * nc;
+    const uint64_t need = o_small + 4 * (nsm + 1) + 4 * ((skeys + 31) / 32);
     if (dir_bytes < need) return LC_ERR_ARG;
     std::vector<uint8_t> host(need);
     BatchList* lists = (BatchList*)host.data();
     BatchChunk* chunks = (BatchChunk*)(host.data() + sizeof(BatchList) * (uint64_t)m);
     // chunk records: units of more than kSmallUnit keys first (one warp each), then the small
-    // ones (one lane each); a list's chunk0 is its first record's index
-    uint64_t nsmall = 0;
-    for (uint32_t k = 0; k < m; ++k) {
-        lc_header h;
-        std::memcpy(&h, (const uint8_t*)h_blobs + blob_off[k], sizeof h);
-        const uint64_t tail = h.n & 1023;  // the last chunk's keys (0: full)
-        if (tail && tail <= kSmallUnit) ++nsmall;
-    }
+    // ones (their keys flattened, one thread per key); a list's chunk0 is its first record
+    const uint64_t nsmall = nsm;
+    uint32_t* sk0 = (uint32_t*)(host.data() + o_small);        // small chunk -> first flat key
+    uint32_t* sblk = sk0 + nsm + 1;                             // 32 flat keys -> small chunk
+    uint64_t flat = 0;
     uint64_t c = 0, cs = nc - nsmall, pos = 0, segs = 0, payload = 0;
     uint32_t maxb = 0;
     for (uint32_t k = 0; k < m; ++k) {
@@ -768,6 +778,12 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
         if (h.off_words >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
         for (uint64_t q = 0; q < H; ++q) {
             const uint64_t nkq = h.n - (q << 10) < 1024 ? h.n - (q << 10) : 1024;
+            if (nkq <= kSmallUnit) {  // flattened small keys [flat, flat + nkq)
+                const uint64_t u = cs - (nc - nsmall);
+                sk0[u] = (uint32_t)flat;
+                for (uint64_t f = (flat + 31) & ~31ULL; f < flat + nkq; f += 32) sblk[f >> 5] = (uint32_t)u;
+                flat += nkq;
+            }
             BatchChunk& r = chunks[nkq <= kSmallUnit ? cs++ : c++];
             r.blob = e.blob;
             r.out = out + (q << 10);
@@ -787,6 +803,7 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
         payload += sizeof(lc_header) + 4 * (L + 1) + 16 * L + 4 * h.n_hint +
                    4 * ((h.n * h.res_bits + 31) / 32);
     }
+    sk0[nsmall] = (uint32_t)flat;
     if (cudaMemcpyAsync(d_dir, host.data(), need, cudaMemcpyHostToDevice, (cudaStream_t)stream) !=
         cudaSuccess)
         return LC_ERR_CUDA;
@@ -797,9 +814,11 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
     b->n_total = pos;
     b->n_chunks = nc;
     b->n_small = nsmall;
+    b->small_keys = skeys;
     b->payload_bytes = payload;
     b->d_lists = d_dir;
     b->d_chunks = (const uint8_t*)d_dir + sizeof(BatchList) * (uint64_t)m;
+    b->d_small = (const uint8_t*)d_dir + o_small;
     return LC_OK;
 }
 

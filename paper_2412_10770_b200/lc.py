@@ -43,7 +43,8 @@ assert C.sizeof(lc_header) == 128
 class lc_batch(C.Structure):
     _fields_ = [("m", C.c_uint32), ("key_bits", C.c_uint32), ("max_res_bits", C.c_uint32),
                 ("sparse", C.c_uint32), ("n_total", C.c_uint64), ("n_chunks", C.c_uint64),
-                ("n_small", C.c_uint64), ("payload_bytes", C.c_uint64), ("d_lists", C.c_void_p), ("d_chunks", C.c_void_p)]
+                ("n_small", C.c_uint64), ("small_keys", C.c_uint64), ("payload_bytes", C.c_uint64),
+                ("d_lists", C.c_void_p), ("d_chunks", C.c_void_p), ("d_small", C.c_void_p)]
 
 
 class lc_view(C.Structure):
