@@ -39,7 +39,12 @@ def test_batch_dir_bytes_and_errors(lc):
     host, offs = _pack(blobs)
     nb = C.c_uint64()
     assert lc._lib.lc_batch_dir_bytes(host.ctypes.data, host.nbytes, offs.ctypes.data, 2, C.byref(nb)) == 0
-    assert nb.value == 64 * 2 + 48 * (5 + 3)  # list records + one record per 1024-key chunk
+    # list records + one record per 1024-key chunk + the (empty) small-chunk key prefix
+    assert nb.value == 64 * 2 + 48 * (5 + 3) + 4
+    tiny = [make_keys(1, 1024 + 40), make_keys(1, 7), make_keys(1, 2048)]  # tails 40, 7, none
+    ht, ot = _pack([lc.encode(k, 63) for k in tiny])
+    assert lc._lib.lc_batch_dir_bytes(ht.ctypes.data, ht.nbytes, ot.ctypes.data, 3, C.byref(nb)) == 0
+    assert nb.value == 64 * 3 + 48 * (2 + 1 + 2) + 4 * (2 + 1) + 4 * ((40 + 7 + 31) // 32)
     bad = offs.copy()
     bad[1] += 16  # not 256-byte aligned
     assert lc._lib.lc_batch_dir_bytes(host.ctypes.data, host.nbytes, bad.ctypes.data, 2, C.byref(nb)) == lc.LC_ERR_ARG
