@@ -544,6 +544,17 @@ __global__ void __launch_bounds__(kThreads, 4)
         const uint32_t lw = (lane * b) >> 5, ls = (lane * b) & 31;
         const uint32_t wbytes = b ? ((((nk * b + 31) >> 5) + 1 + 3) & ~3u) * 4 : 0;
         stage(pg, sec, r.j0, r.jlast, sec.words + (size_t)(r.key0 >> 10) * 32 * b, wbytes, lane);
+        if (lane == 0 && item >= ngroups && item < items) {  // the next big unit's slices -> L2
+            const uint8_t* nb = (const uint8_t*)nr.blob;
+            const uint32_t nnk = nr.nk_b & 0xffff, nbits = nr.nk_b >> 16;
+            if (nbits)
+                bulk_prefetch_l2((const uint32_t*)(nb + nr.off_words) + (size_t)(nr.key0 >> 10) * 32 * nbits,
+                                 ((((nnk * nbits + 31) >> 5) + 1 + 3) & ~3u) * 4);
+            const uint32_t npj = nr.j0 & ~3u;
+            const uint32_t ncs = min(kSegCap + 4, nr.jlast + 2 - npj);
+            bulk_prefetch_l2((const uint32_t*)(nb + 256) + npj, ((ncs + 3) & ~3u) * 4);
+            bulk_prefetch_l2((const ulonglong2*)(nb + nr.off_params) + npj, min(kSegCap, nr.jlast + 1 - npj) * 16);
+        }
         uint32_t jb = r.j0, sb = pg.sS[LC_BOUND(true, r.j0 - pg.pj, pg.cs)];
         uint8_t* outl = (uint8_t*)a.out + (out0 + lane) * kw;
         const uint32_t key0 = r.key0, jlast = r.jlast;
