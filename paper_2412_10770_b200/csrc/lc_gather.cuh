@@ -167,11 +167,20 @@ __host__ __device__ constexpr uint32_t r64_bytes(uint32_t b) {  // per slot: par
 }
 
 // 64-key ranges (BASELINE config 5).  Phase 1: lane r binary-searches range r's first segment
-// (32 independent searches).  Phase 2: the warp walks its 32 ranges through a 4-slot shared-
-// memory ring: the lanes gather range k+3's params[j..j+8), starts[j+1..j+9) and residual
-// words with cp.async (one 16-byte copy per lane) while range k is decoded from smem with the
-// pair-window scheme, so the decode never waits on a dependent global load.  A range crossing
-// more than 7 segment starts is decoded through L2 instead.
+// (32 independent searches) and parks {start, segment, segment start, first word} in shared
+// memory.  Phase 2: the warp walks its 32 ranges through a 4-slot shared-memory ring: lane g
+// gathers 16-byte group g of range k+3's slot (params[j..j+8), starts[j+1..j+9), residual
+// words) with cp.async while range k is decoded from smem with the pair-window scheme, so the
+// decode never waits on a dependent global load.  A range crossing more than 7 segment starts
+// is decoded through L2 instead.  Each lane's copy role (section, stride, bound) is fixed for
+// the whole warp walk, so a range costs it one address computation and one cp.async.
+constexpr uint32_t kR64Info = 32 * 16;  // per-warp range info: 32 x {rk, jk (~0: invalid), sb, wlo}
+static_assert(kR64Segs + kR64StartGroups + (((64 * 32 + 31) >> 5) + 2 + 3 + 3) / 4 <= 32,
+              "one 16-byte copy group per lane for every residual width");
+__host__ __device__ constexpr uint32_t r64_smem_per_warp(uint32_t b) {
+    return kR64Slots * r64_bytes(b) + kR64Info;
+}
+
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -182,63 +191,52 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     const Sections sec = a.sec;
     const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
     const uint32_t RB = r64_bytes(b), nw16 = r64_words(b) / 4;
-    uint8_t* ring = smem + warp * kR64Slots * RB;
+    uint8_t* wbase = smem + warp * r64_smem_per_warp(b);
+    uint4* info = (uint4*)(wbase + kR64Slots * RB);
+    uint8_t* ring = wbase;
     const uint32_t lmask = lanemask_le();
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
 
-    // ---- phase 1: lane-parallel search
-    uint32_t rs = 0, j = 0, sj = 0, ok = 0;
-    if (r0 + lane < a.q) {
-        const uint64_t s64 = __ldg(a.start + r0 + lane);
-        if (s64 <= a.n && 64 <= a.n - s64) {
-            ok = 1;
-            rs = (uint32_t)s64;
-            j = seg_search(sec, rs, keep);
-            sj = ldh(sec.starts + j, keep);
-        } else if (a.err) {
-            atomicOr(a.err, 1u);
+    // ---- phase 1: lane-parallel search, results parked in shared memory
+    {
+        uint32_t rs = 0, j = kFull, sj = 0;
+        if (r0 + lane < a.q) {
+            const uint64_t s64 = __ldg(a.start + r0 + lane);
+            if (s64 <= a.n && 64 <= a.n - s64) {
+                rs = (uint32_t)s64;
+                j = seg_search(sec, rs, keep);
+                sj = ldh(sec.starts + j, keep);
+            } else if (a.err) {
+                atomicOr(a.err, 1u);
+            }
         }
+        // first residual word of the range's staged words (16-byte aligned)
+        info[lane] = make_uint4(rs, j, sj, (uint32_t)(((uint64_t)rs * b) >> 5) & ~3u);
     }
+    __syncwarp();
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
-    // first residual word of the range's staged words (16-byte aligned), per lane = range
-    const uint32_t wlo = (uint32_t)(((uint64_t)rs * b) >> 5) & ~3u;
 
-    // gather range k into ring slot k % kR64Slots: copy groups 0..11 = params, 12..16 = starts,
-    // then words; group g is done by lane g % 32.  Each lane's role (source section, offset in
-    // the slot) is fixed, so per range it only adds the range's uniform section offset.
-    const uint32_t ngroups = kR64Segs + kR64StartGroups + nw16;
-    struct Role {
-        const uint8_t* src;  // section base + 16 t
-        uint32_t dst, kind, t;
-    };
-    auto role_of = [&](uint32_t g) {
-        Role r;
-        const uint32_t gw = kR64Segs + kR64StartGroups;
-        if (g < kR64Segs) r = {(const uint8_t*)(sec.params + g), 16 * g, 0, g};
-        else if (g < gw)
-            r = {(const uint8_t*)(sec.starts + 4 * (g - kR64Segs)), 16 * g, 1, g - kR64Segs};
-        else
-            r = {(const uint8_t*)(sec.words + 4 * (g - gw)), 16 * g, 2, g - gw};
-        return r;
-    };
-    const Role ra = role_of(lane), rb = role_of(lane + 32);
-    const bool has_a = lane < ngroups, has_b = lane + 32 < ngroups;
-    auto copy = [&](const Role& r, uint8_t* slot, uint32_t jk, uint32_t s0, uint32_t w0) {
-        const uint64_t off = r.kind == 0 ? (uint64_t)jk * 16 : r.kind == 1 ? (uint64_t)s0 * 4
-                                                                            : (uint64_t)w0 * 4;
-        const bool valid = r.kind == 0 ? jk + r.t < L
-                                       : (r.kind == 1 || (uint64_t)w0 + 4 * r.t + 4 <= a.nwords);
-        cp16(slot + r.dst, r.src + off, valid);
-    };
+    // ---- this lane's copy role: 16-byte group `lane` of every slot
+    //   lanes [0, S8): params[j + lane]           (valid while j + lane < L)
+    //   lanes [S8, S8 + SG): starts[4 ((j+1)/4) + 4 (lane - S8) ..]   (inside the section padding)
+    //   next nw16 lanes: words[wlo + 4 t ..]     (valid while wlo + 4 t + 4 <= W)
+    const uint32_t gs = kR64Segs, gw = kR64Segs + kR64StartGroups;
+    const bool has = lane < gw + nw16;
+    const int kind = lane < gs ? 0 : lane < gw ? 1 : 2;
+    const uint32_t t = kind == 0 ? lane : kind == 1 ? lane - gs : lane - gw;
+    const uint8_t* src0 = kind == 0 ? (const uint8_t*)(sec.params + t)
+                        : kind == 1 ? (const uint8_t*)(sec.starts + 4 * t)
+                                    : (const uint8_t*)(sec.words + 4 * t);
+    const uint32_t mul = kind == 0 ? 16 : 4;
+    // valid iff v < lim (v = the range's j or wlo)
+    const uint64_t lim = kind == 0 ? (uint64_t)L - t : kind == 1 ? ~0ull
+                       : (a.nwords >= 4 * (uint64_t)t + 4 ? a.nwords - 4 * (uint64_t)t - 3 : 0);
     auto issue = [&](uint32_t k) {
-        if (k < nr) {
-            const uint32_t jk = __shfl_sync(kFull, j, k), w0 = __shfl_sync(kFull, wlo, k);
-            const uint32_t okk = __shfl_sync(kFull, ok, k);
-            uint8_t* slot = ring + (k % kR64Slots) * RB;
-            if (okk) {
-                const uint32_t s0 = (jk + 1) & ~3u;
-                if (has_a) copy(ra, slot, jk, s0, w0);
-                if (has_b) copy(rb, slot, jk, s0, w0);
+        if (k < nr && has) {
+            const uint4 ri = info[k];
+            if (ri.y != kFull) {
+                const uint32_t v = kind == 0 ? ri.y : kind == 1 ? ((ri.y + 1) & ~3u) : ri.w;
+                cp16(ring + (k % kR64Slots) * RB + 16 * lane, src0 + (uint64_t)v * mul, v < lim);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
@@ -250,12 +248,10 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         issue(k + kR64Slots - 1);
         asm volatile("cp.async.wait_group %0;" ::"n"(kR64Slots - 1) : "memory");
         __syncwarp();
-        const uint32_t rk = __shfl_sync(kFull, rs, k);
-        const uint32_t jk = __shfl_sync(kFull, j, k);
-        const uint32_t sb = __shfl_sync(kFull, sj, k);
-        const uint32_t okk = __shfl_sync(kFull, ok, k);
+        const uint4 ri = info[k];
+        const uint32_t rk = ri.x, jk = ri.y, sb = ri.z;
         uint8_t* outk = out0 + (size_t)k * 64 * kw;
-        if (!okk) {
+        if (jk == kFull) {
             put<K64>(outk, 0, 0);
             put<K64>(outk + 32 * kw, 0, 0);
             __syncwarp();
@@ -280,7 +276,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             if (b) {
                 const uint32_t* Wd = (const uint32_t*)(rsm + 16 * (kR64Segs + kR64StartGroups));
                 // bit offset inside the staged words; exact mod 2^32 (the true value is small)
-                const uint32_t bA = (rk + lane) * b - (__shfl_sync(kFull, wlo, k) << 5);
+                const uint32_t bA = (rk + lane) * b - (ri.w << 5);
                 const uint32_t bB = bA + 32 * b;
                 LC_CHECK(true, (bB >> 5) + 1, r64_words(b));
                 uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
