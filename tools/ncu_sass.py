@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""SASS of one kernel in an ncu report with executed warp-instructions per instruction (per
+`--unit` work items) and stall samples: where a kernel's instruction budget goes.
+
+  python tools/ncu_sass.py gpurun_out/x.ncu-rep --unit 1e7 [--min 0.5]
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import subprocess
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--unit", type=float, default=1.0, help="divide executions by this")
+    ap.add_argument("--min", type=float, default=0.0, help="hide instructions below this")
+    args = ap.parse_args()
+    out = subprocess.check_output(["ncu", "-i", args.rep, "--page", "source", "--csv",
+                                   "--print-source", "sass"], text=True)
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = next(r for r in rows if "Instructions Executed" in r)
+    ie, st = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+    total = 0
+    lines = []
+    for r in rows[rows.index(hdr) + 1:]:
+        try:
+            n = int(r[ie])
+        except (ValueError, IndexError):
+            continue
+        total += n
+        lines.append((r[0][-5:], n / args.unit, int(r[st] or 0), r[1].strip()))
+    print(f"total {total} = {total / args.unit:.2f} per unit")
+    for a, n, s, ins in lines:
+        if n >= args.min:
+            print(f"{a} {n:7.2f} {s:6d}  {ins[:80]}")
+
+
+if __name__ == "__main__":
+    main()
