@@ -106,16 +106,26 @@ int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
 int32_t lc_encode_ex(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
                      uint32_t flags, void** blob, uint64_t* blob_bytes);
 
-/* Release a blob returned by lc_encode / lc_encode_ex (NULL is a no-op). */
+/* Release a blob returned by lc_encode / lc_encode_ex (NULL is a no-op).  The compressed
+ * representation K^c of Def. 1 is owned by the caller until released. */
 void lc_free(void* blob);
 
 /* Full validation of a HOST copy of a blob (header, offsets, monotone starts, slope guard,
- * hint array, residual range, zero padding).  LC_OK or LC_ERR_FORMAT / LC_ERR_ARG. */
+ * hint array, residual range, zero padding): the invariants that make Dec(K^c) well defined —
+ * segments covering [0, N) in order (Eq. 1), every residual within
+ * [-eps, eps] (Def. 2) so each field fits ceil(log2(2 eps + 1)) bits
+ * (PAPER.md:186), decoded keys strictly increasing (Def. 1's sorted K).
+ * LC_OK or LC_ERR_FORMAT / LC_ERR_ARG.  The device calls trust the header checks of
+ * lc_view_init plus the hint checks of lc_decode_host / lc_shard_*; validate blobs from
+ * untrusted sources before uploading them. */
 int32_t lc_validate(const void* blob, uint64_t blob_bytes);
 
 /* Fill *v from the blob's 128-byte header (a host copy) and the device pointer of the same blob
- * (blob_bytes bytes).  Checks the header fields only (LC_ERR_FORMAT) and d_blob alignment
- * (LC_ERR_ARG). */
+ * (blob_bytes bytes): the handle every device call takes for K^c resident in HBM (the decode
+ * side of Fig. 2).  Checks the header fields only (FORMAT F1: magic, version,
+ * b = ceil(log2(2 eps + 1)) per PAPER.md:186, section offsets recomputed from N, L, b) and
+ * d_blob alignment; LC_ERR_FORMAT / LC_ERR_ARG.  Leaves the optional index, access layout and
+ * shard fields empty. */
 int32_t lc_view_init(lc_view* v, const void* host_header128, const void* d_blob,
                      uint64_t blob_bytes);
 
@@ -163,9 +173,11 @@ int32_t lc_shard_upload(const void* h_blob, uint64_t blob_bytes, uint64_t i0, ui
 int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_out,
                   uint32_t* d_err, lc_stream stream);
 
-/* Range decode: d_out[r*len + k] = K[d_start[r] + k] for r < q, k < len (BASELINE config 5:
- * 10^7 ranges of 64 keys).  A range with start + len > n yields zeros and sets bit 0 of
- * *d_err.  1 <= len <= 2^20; q == 0 is a no-op. */
+/* Range decode: d_out[r*len + k] = K[d_start[r] + k] for r < q, k < len — Dec(K^c)[i]
+ * over len consecutive indices, the blocked decode inside and across segments
+ * (K[i] = floor(f(i)) + Delta[i]; BASELINE config 5: 10^7 ranges of 64 keys).
+ * A range with start + len > n yields zeros and sets bit 0 of *d_err.  1 <= len <= 2^20;
+ * q == 0 is a no-op. */
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
                         void* d_out, uint32_t* d_err, lc_stream stream);
 
@@ -338,11 +350,15 @@ int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h
 int32_t lc_decode_host(const void* h_blob, uint64_t blob_bytes, void* d_blob, void* d_out,
                        void* h_out, lc_stream stream);
 
-/* Human-readable name of a status code (static string). */
+/* Human-readable name of a status code (static string): the error kinds of the method's
+ * interfaces (EmptyInput, UnsortedInput, CorruptPayload, IndexOutOfRange, ... SPEC.md:113,
+ * 164, 174, 184, 465; the paper's Def. 1 input is a sorted list). */
 const char* lc_status_str(int32_t status);
 
 /* Number of device kernels launched by this library in this process so far (monotone,
- * thread-safe counter; bench.py reports its delta over the timed region as gpu_launches). */
+ * thread-safe counter; bench.py reports its delta over the timed region as gpu_launches, the
+ * evidence that the measured throughput of the decode path of PAPER.md:94-95 ran in these
+ * kernels). */
 uint64_t lc_launch_count(void);
 
 #ifdef __cplusplus

@@ -9,14 +9,18 @@
 //    hint array gives the chunk's segment range [hint[h], hint[h+1]] with no search
 //    (PAPER.md:286's auxiliary localisation structure).  Lane 0 stages the chunk's starts,
 //    params and residual words into the warp's shared-memory page with cp.async.bulk (TMA 1D)
-//    on an mbarrier (dense chunks are paged) and prefetches the next chunk into L2.  The chunk
-//    is decoded as 16 pair-windows of 64 keys (2 keys per lane): warp OR-reductions (REDUX) of
-//    the next 32 segment starts give the boundary bitmasks, so each key gets its segment and
-//    offset with POPC/CLZ -- no per-key search and no serial walk ("reduce the
-//    data dependencies ... to maximize parallelism").  The prediction is exact 32-bit integer
+//    on an mbarrier (dense chunks are paged) and prefetches the next chunk into L2.  A fully
+//    staged chunk is decoded as 8 quad-windows of 128 keys (a paged one as 16 pair-windows of
+//    64): warp OR-reductions (REDUX) of the next 32 segment starts give the boundary bitmasks,
+//    so each key gets its segment and offset with POPC/CLZ -- no per-key search and no serial
+//    walk ("reduce the data dependencies ... to maximize parallelism"); sparse
+//    lists take a single-segment fast path per quad.  The prediction is exact 32-bit integer
 //    math (see pred_plus).  Each warp store writes 32 consecutive keys (coalesced, streaming).
 //  * Random access / quantiles: hint bracket + binary search, two interleaved queries per
-//    thread, L2 evict_last for the search structures and evict_first for the gathers.
+//    thread, L2 evict_last for the search structures and evict_first for the gathers; with the
+//    access layout, a directory word instead of the search and one record per query.
+//  * Batches: one launch for many lists (chunk records + a work queue; short lists' keys one
+//    thread each), batched AND / OR over list pairs (lc_batchops.cuh).
 //  * Range decode: one warp per 32 ranges (lane-parallel search); len == 64 gathers each
 //    range's slices through a per-warp cp.async ring and decodes from shared memory.
 //  * Successor search / intersection: binary search over the segments' first keys (the
@@ -427,6 +431,20 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
+    if (v->d_acc) {  // access layout attached: per-key directory + records, no staging
+        const uint64_t per = 8ull * kRdRanges;
+        const uint64_t g2 = (q + per - 1) / per;
+        if (g2 > 0x7fffffffULL) return LC_ERR_ARG;
+        if (len == 64) {
+            if (k64) lc_range_dir_kernel<true, true><<<(unsigned)g2, 256, 0, st>>>(a);
+            else lc_range_dir_kernel<false, true><<<(unsigned)g2, 256, 0, st>>>(a);
+        } else {
+            if (k64) lc_range_dir_kernel<true, false><<<(unsigned)g2, 256, 0, st>>>(a);
+            else lc_range_dir_kernel<false, false><<<(unsigned)g2, 256, 0, st>>>(a);
+        }
+        lc_detail::count_launch(1);
+        return cuda_status();
+    }
     if (len == 64) {  // the config-5 shape: cp.async ring kernel
         const uint32_t smem = 8 * r64_smem_per_warp(a.b);
         const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;

@@ -100,7 +100,22 @@ def _check_blob(lc, blob, keys, rng, m=20_000, layout_bytes=True):
     qa = lc.quantile(v, _dev(ranks), 1000, exact=False)
     bad = np.array([n, n + 5, 1 << 40], np.uint64)  # out of range: 0 and the error bit
     ab = lc.access(v, _dev(bad), err=err)
+    rgs = {}
+    for ln in (1, 33, 64, 100):  # range decode through the layout
+        if n >= ln:
+            st = rng.integers(0, n - ln, 700, endpoint=True).astype(np.uint64)
+            rgs[ln] = (st, lc.range_decode(v, _dev(st), ln))
     torch.cuda.synchronize()
+    for ln, (st, rg) in rgs.items():
+        want = keys[st.astype(np.int64)[:, None] + np.arange(ln)]
+        assert np.array_equal(_host(rg, keys.dtype).reshape(-1, ln), want), ln
+    e2 = torch.zeros(1, dtype=torch.int32, device=DEV)
+    rb = lc.range_decode(v, _dev(np.array([0, max(n - 63, 0), n], np.uint64)), 64, err=e2)
+    torch.cuda.synchronize()
+    rbh = _host(rb, keys.dtype).reshape(-1, 64)
+    assert not rbh[1:].any() and int(e2.item()) == 1
+    if n >= 64:
+        assert np.array_equal(rbh[0], keys[:64])
     assert np.array_equal(_host(a, keys.dtype), keys[idx.astype(np.int64)])
     assert np.array_equal(_host(q, keys.dtype), keys[qi])
     assert np.array_equal(_host(qa, keys.dtype), orc.predict(blob, qi.astype(np.uint64))[0])
@@ -160,6 +175,11 @@ def test_layout_full_config5(lc):
     del plain
     want, err = orc.access(blob, idx[:5000])
     assert err == 0 and np.array_equal(_host(got[:5000], np.uint64), want)
+    keys_r, _, rs = make_queries()
+    d_rs = _dev(rs)
+    rg = lc.range_decode(v, d_rs, 64)
+    assert torch.equal(rg, d_keys[d_rs[:, None] + torch.arange(64, device=DEV)[None, :]])
+    del rg
     ranks = torch.from_numpy(np.random.default_rng(9).integers(0, 1 << 20, 1_000_000)).to(DEV)
     q = lc.quantile(v, ranks, 1 << 20)
     qi = torch.clamp(ranks * keys.size // (1 << 20), max=keys.size - 1)

@@ -26,7 +26,9 @@ def main():
     ap.add_argument("--only", choices=["layout", "plain"], default=None)
     args = ap.parse_args()
     dev = "cuda:0"
-    keys, idx, _ = make_queries()
+    keys, idx, rs = make_queries()
+    d_rs = torch.from_numpy(rs.view(np.int64)).to("cuda:0")
+    r_out = torch.empty(rs.size * 64, dtype=torch.int64, device="cuda:0")
     blob = lc.encode(keys, 127)
     v = lc.View(blob, device=dev)
     d_idx = torch.from_numpy(idx.view(np.int64)).to(dev)
@@ -51,6 +53,7 @@ def main():
         assert torch.equal(out, d_keys[d_idx])
         res["plain_ms"] = ms
         res["plain_lookups_per_s"] = idx.size / ms * 1e3
+        res["plain_range64_ms"] = timeit(lambda: lc.range_decode(v, d_rs, 64, r_out), args.reps)
     if args.only != "plain":
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -67,6 +70,12 @@ def main():
         assert torch.equal(out, d_keys[d_idx])
         res["layout_ms"] = ms
         res["layout_lookups_per_s"] = idx.size / ms * 1e3
+        r_out.zero_()
+        res["layout_range64_ms"] = timeit(lambda: lc.range_decode(v, d_rs, 64, r_out), args.reps)
+        res["layout_ranges_per_s"] = rs.size / res["layout_range64_ms"] * 1e3
+        sel = (d_rs[:, None] + torch.arange(64, device="cuda:0")[None, :]).reshape(-1)
+        assert torch.equal(r_out, d_keys[sel])
+        del sel
         ranks = d_idx[:10_000_000]
         qo = torch.empty(ranks.numel(), dtype=torch.int64, device=dev)
         res["quantile_exact_layout_ms_1e7"] = timeit(
