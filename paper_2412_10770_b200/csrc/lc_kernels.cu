@@ -229,6 +229,50 @@ void pipe_release(HostPipe* p) {
     g_pipe_free.push_back(p);
 }
 
+// Pinned host staging buffers for per-call uploads (the batched AND / OR plan): a buffer is
+// reused once the event recorded after its last copy has completed, so the upload is
+// asynchronous (a pageable cudaMemcpyAsync would synchronize the stream first) and the host
+// builds the next plan while the GPU runs.  Buffers live until process exit.
+struct Staging {
+    int dev = -1;
+    void* h = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+};
+std::mutex g_stage_mu;
+std::vector<Staging*> g_stage;  // idle (or copy in flight, see ev)
+
+Staging* stage_acquire(size_t bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        for (size_t k = 0; k < g_stage.size(); ++k) {
+            Staging* s = g_stage[k];
+            if (s->dev == dev && s->cap >= bytes && cudaEventQuery(s->ev) == cudaSuccess) {
+                g_stage.erase(g_stage.begin() + k);
+                return s;
+            }
+        }
+    }
+    Staging* s = new Staging;
+    s->dev = dev;
+    s->cap = bytes < (1u << 20) ? (1u << 20) : bytes;
+    if (cudaMallocHost(&s->h, s->cap) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming) != cudaSuccess) {
+        if (s->h) cudaFreeHost(s->h);
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+
+void stage_release(Staging* s, cudaStream_t st) {
+    cudaEventRecord(s->ev, st);
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    g_stage.push_back(s);
+}
+
 // host->device copy of `bytes` bytes
 int32_t copy_up(void* d, const void* h, uint64_t bytes, cudaStream_t st) {
     if (!bytes) return LC_OK;
@@ -850,11 +894,11 @@ struct SetopPlan {
     uint64_t o_sl, o_soff, o_loff, o_cap, o_sel, o_selout, head;  // uploaded head
     uint64_t o_keys, o_flags, o_mw, o_counts, o_rank, o_total, total;
     uint64_t out_cap;  // output elements the caller provides
-    std::vector<uint8_t> host;  // the head's bytes
 };
 
+// fill: the head's bytes are written to `fill` (y->head bytes), nullptr to size only
 int32_t setop_plan(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pairs, uint32_t P,
-                   bool OR, bool fill, SetopPlan* y) {
+                   bool OR, uint8_t* fill, SetopPlan* y) {
     if (!bt || !h_n || (!h_pairs && P) || !bt->d_lists) return LC_ERR_ARG;
     const uint32_t m = bt->m;
     const uint64_t kw = bt->key_bits / 8;
@@ -904,8 +948,7 @@ int32_t setop_plan(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pa
     y->total = y->o_total + 256;
     y->out_cap = OR ? S + Lt : S;
     if (!fill) return LC_OK;
-    y->host.assign(y->head, 0);
-    uint8_t* H = y->host.data();
+    uint8_t* H = fill;
     uint32_t* sl = (uint32_t*)(H + y->o_sl);
     uint64_t* soff = (uint64_t*)(H + y->o_soff);
     uint64_t* loff = (uint64_t*)(H + y->o_loff);
@@ -947,12 +990,17 @@ int32_t setop_batch(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_p
         return LC_ERR_ARG;
     if (!P) return LC_OK;
     SetopPlan y;
-    int32_t rc = setop_plan(bt, h_n, h_pairs, P, OR, true, &y);
+    int32_t rc = setop_plan(bt, h_n, h_pairs, P, OR, nullptr, &y);  // sizes
     if (rc) return rc;
     if (scratch_bytes < y.total) return LC_ERR_ARG;
+    Staging* sg = stage_acquire(y.head);
+    if (!sg) return LC_ERR_ALLOC;
+    std::memset(sg->h, 0, y.head);
+    setop_plan(bt, h_n, h_pairs, P, OR, (uint8_t*)sg->h, &y);
     uint8_t* D = (uint8_t*)d_scratch;
-    if (cudaMemcpyAsync(D, y.host.data(), y.head, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(D + y.o_flags, 0, 4 * y.nwords, st) != cudaSuccess)
+    const bool cp_ok = cudaMemcpyAsync(D, sg->h, y.head, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    stage_release(sg, st);
+    if (!cp_ok || cudaMemsetAsync(D + y.o_flags, 0, 4 * y.nwords, st) != cudaSuccess)
         return LC_ERR_CUDA;
     if ((rc = launch_batch_decode(bt, (const uint32_t*)(D + y.o_sel),
                                   (const uint64_t*)(D + y.o_selout), nullptr, (uint32_t)y.U,
@@ -1011,7 +1059,7 @@ int32_t lc_setop_batch_scratch_bytes(const lc_batch* b, const uint64_t* h_n, con
                                      uint64_t* out_keys) {
     if (!scratch_bytes || !out_keys || (op != LC_SETOP_AND && op != LC_SETOP_OR)) return LC_ERR_ARG;
     SetopPlan y;
-    const int32_t rc = setop_plan(b, h_n, h_pairs, n_pairs, op == LC_SETOP_OR, false, &y);
+    const int32_t rc = setop_plan(b, h_n, h_pairs, n_pairs, op == LC_SETOP_OR, nullptr, &y);
     if (rc) return rc;
     *scratch_bytes = y.total;
     *out_keys = y.out_cap;
