@@ -123,7 +123,9 @@ __device__ __forceinline__ uint32_t fld(const Page& pg, uint32_t w, uint32_t lw,
 // (clamped at jlast + 1) is a real start.  Lane 0 issues, the warp waits on the mbarrier.
 __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t from, uint32_t jlast,
                                       const uint32_t* wsrc, uint32_t wbytes, uint32_t lane) {
-    __syncwarp();  // every lane is done reading the previous contents
+    __syncwarp();  // every lane is done reading the previous contents ...
+    // ... and those generic-proxy reads are ordered before the async-proxy (TMA) writes below
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     pg.pj = from & ~3u;
     pg.cp = min(kSegCap, jlast + 1 - pg.pj);
 #ifdef LC_DEBUG_BOUNDS

@@ -567,89 +567,3 @@ __global__ void __launch_bounds__(256) lc_access_kernel(const AccessArgs a) {
         }
     }
 }
-
-// ------------------------------------------------- range decode through the access layout
-// With the access layout attached, a range needs no search and no staging: every key i of a
-// range takes its segment from its 32-key directory word (j = hint + rank + popc, start from the
-// highest bit at or below i or dist) and its params and residual field from record j, exactly
-// like lc_access_dir_kernel; the records of consecutive segments are contiguous, so a range's
-// loads touch ~2-3 DRAM lines (params and residual units together) instead of three separate
-// gathers (params, starts, words).  One warp per 8 ranges; the warp's 8 len keys are flattened,
-// 4 keys per lane in flight per step; stores are 32 consecutive keys per warp instruction.
-constexpr uint32_t kRdRanges = 8;  // ranges per warp
-template <bool K64, bool LEN64>
-__global__ void __launch_bounds__(256) lc_range_dir_kernel(const RangeArgs a) {
-    constexpr uint32_t kw = K64 ? 8 : 4;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * kRdRanges;
-    if (r0 >= a.q) return;  // warp-uniform
-    const Sections sec = a.sec;
-    const uint32_t b = a.b, mask = a.mask, bias = a.bias, len = LEN64 ? 64 : a.len;
-    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-    const uint32_t nr = (uint32_t)min((uint64_t)kRdRanges, a.q - r0);
-    uint32_t rs = kFull;  // lane < nr: start of range r0 + lane (kFull: out of bounds)
-    if (lane < nr) {
-        const uint64_t s64 = __ldg(a.start + r0 + lane);
-        if (s64 <= a.n && len <= a.n - s64) rs = (uint32_t)s64;
-        else if (a.err) atomicOr(a.err, 1u);
-    }
-    const uint32_t T = nr * len;
-    uint8_t* const out0 = (uint8_t*)a.out + (size_t)r0 * len * kw;
-    for (uint32_t k0 = 0; k0 < T; k0 += 4 * 32) {
-        uint32_t i[4], j[4], s[4];
-        uint2 de[4];
-        bool live[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t kk = k0 + 32 * u + lane;
-            const uint32_t r = LEN64 ? kk >> 6 : kk / len;
-            const uint32_t rk = __shfl_sync(kFull, rs, r & 31);
-            live[u] = kk < T && rk != kFull;
-            i[u] = rk + (LEN64 ? kk & 63 : kk - r * len);
-            j[u] = 0;
-            de[u] = make_uint2(0, 0);
-            if (live[u]) {  // one L2 round trip: hint and the 32-key directory word
-                j[u] = ldh(sec.hint + (i[u] >> 10), keep);
-                de[u] = ldh(sec.dir + (i[u] >> 5), keep);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            s[u] = 0;
-            if (!live[u]) continue;
-            const uint32_t m = de[u].x & ((2u << (i[u] & 31)) - 1);
-            j[u] += (de[u].y & 2047) + __popc(m);
-            const uint32_t dist = de[u].y >> 11;
-            if (m) s[u] = (i[u] & ~31u) + (31 - __clz(m));
-            else if (dist != kDistNone) s[u] = (i[u] & ~31u) - dist;
-            else s[u] = ldh(sec.starts + j[u], keep);
-        }
-        ulonglong2 pr[4];
-        uint2 w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            pr[u] = make_ulonglong2(0, 0);
-            w[u] = make_uint2(0, 0);
-            if (!live[u]) continue;
-            const ulonglong2* rec = sec.acc + acc_unit(j[u], s[u], b);
-            pr[u] = ldh(rec, once);
-            if (b) {
-                const uint32_t p = (uint32_t)((uint64_t)i[u] * b - ((((uint64_t)s[u] * b) >> 7) << 7));
-                const uint32_t* wp = (const uint32_t*)(rec + 1) + (p >> 5);
-                w[u] = make_uint2(ldh(wp, once), ldh(wp + 1, once));
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t kk = k0 + 32 * u + lane;
-            if (kk >= T) continue;
-            uint8_t* o = out0 + (size_t)kk * kw;
-            if (!live[u]) {
-                put<K64>(o, 0, 0);
-                continue;
-            }
-            const uint32_t uf = b ? field_of(w[u], i[u], b, mask) : 0;
-            put<K64>(o, pr[u].x, pred_plus(pr[u].y, i[u] - s[u], uf - bias));
-        }
-    }
-}

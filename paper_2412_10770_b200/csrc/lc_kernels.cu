@@ -475,20 +475,6 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
-    if (v->d_acc) {  // access layout attached: per-key directory + records, no staging
-        const uint64_t per = 8ull * kRdRanges;
-        const uint64_t g2 = (q + per - 1) / per;
-        if (g2 > 0x7fffffffULL) return LC_ERR_ARG;
-        if (len == 64) {
-            if (k64) lc_range_dir_kernel<true, true><<<(unsigned)g2, 256, 0, st>>>(a);
-            else lc_range_dir_kernel<false, true><<<(unsigned)g2, 256, 0, st>>>(a);
-        } else {
-            if (k64) lc_range_dir_kernel<true, false><<<(unsigned)g2, 256, 0, st>>>(a);
-            else lc_range_dir_kernel<false, false><<<(unsigned)g2, 256, 0, st>>>(a);
-        }
-        lc_detail::count_launch(1);
-        return cuda_status();
-    }
     if (len == 64) {  // the config-5 shape: cp.async ring kernel
         const uint32_t smem = 8 * r64_smem_per_warp(a.b);
         const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;
