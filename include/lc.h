@@ -320,26 +320,39 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
 int32_t lc_decode_batch(const lc_batch* b, void* d_out, uint32_t* d_work, lc_stream stream);
 
 /* Batched AND / OR queries (inverted-index processing, §III-A, Fig. 4):
- * pair p = (h_pairs[2 p], h_pairs[2 p + 1]) names two lists of the batch; h_n[k] is list k's
- * key count (host, m entries, as given to lc_batch_init).  All pairs run in a fixed number of
- * launches whatever their number.  The shorter list s_p of each pair is decoded; for AND each
- * of its keys is searched in the compressed longer list l_p (next_geq: segments as skip
- * pointers), for OR both are decoded and every key placed in its union slot by ranks.
- * Results: pair p's keys at d_out[d_out_off[p] .. d_out_off[p] + d_counts[p]) (device arrays
- * of P + 1 and P uint64; AND results are packed, OR results sit at capacity offsets
- * sum_{q < p} (n_s + n_l)).  d_scratch: >= *scratch_bytes (256-byte aligned); d_out: >=
- * *out_keys keys, both from lc_setop_batch_scratch_bytes.  Errors: LC_ERR_ARG (bad pair index,
- * h_n not matching the batch, buffers too small), LC_ERR_TOO_LARGE (>= 2^32 short keys). */
+ * pair p = (pairs[2 p], pairs[2 p + 1]) names two lists of the batch.  All pairs run in a fixed
+ * number of launches whatever their number, planned on the device (no host pass over the
+ * batch, no upload).  The shorter list s_p of each pair is decoded; for AND each of its keys is
+ * searched in the compressed longer list l_p (next_geq: segments as skip pointers), for OR both
+ * are decoded and every key is placed in its union slot by ranks.
+ *
+ * lc_setop_batch_plan sizes one query batch on the host (O(pairs)): h_n[k] is list k's key
+ * count (m entries, as given to lc_batch_init), h_pairs the 2 P list indices.  The device calls
+ * then take the same pairs in device memory (d_pairs); other pairs give unspecified results but
+ * never write outside d_scratch / d_out (a pair index >= m is clamped and flagged).
+ * Results: pair p's keys at d_out[d_out_off[p] .. d_out_off[p] + d_counts[p]) (device arrays of
+ * P + 1 and P uint64; AND results are packed, OR results sit at capacity offsets
+ * sum_{q < p} (n_s + n_l)).  d_scratch: >= plan->scratch_bytes (256-byte aligned); d_out:
+ * >= plan->out_keys keys.  Errors: LC_ERR_ARG (bad pair index on the host, buffers too small,
+ * a plan of the other operation), LC_ERR_TOO_LARGE (>= 2^32 short keys). */
 enum { LC_SETOP_AND = 0, LC_SETOP_OR = 1 };
-int32_t lc_setop_batch_scratch_bytes(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                                     uint32_t n_pairs, int32_t op, uint64_t* scratch_bytes,
-                                     uint64_t* out_keys);
-int32_t lc_intersect_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                           uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+typedef struct lc_setop_plan {
+    uint32_t n_pairs;
+    int32_t op;              /* LC_SETOP_AND | LC_SETOP_OR */
+    uint64_t short_keys;     /* sum over pairs of the shorter list's keys */
+    uint64_t long_keys;      /* OR: sum of the longer lists' keys (0 for AND) */
+    uint64_t units;          /* 1024-key chunk records decoded */
+    uint64_t scratch_bytes;  /* device scratch the call needs */
+    uint64_t out_keys;       /* output capacity in keys */
+} lc_setop_plan;
+int32_t lc_setop_batch_plan(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                            uint32_t n_pairs, int32_t op, lc_setop_plan* plan);
+int32_t lc_intersect_batch(const lc_batch* b, const lc_setop_plan* plan, const uint32_t* d_pairs,
+                           void* d_scratch, uint64_t scratch_bytes, void* d_out,
                            uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream);
-int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                       uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
-                       uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream);
+int32_t lc_union_batch(const lc_batch* b, const lc_setop_plan* plan, const uint32_t* d_pairs,
+                       void* d_scratch, uint64_t scratch_bytes, void* d_out, uint64_t* d_out_off,
+                       uint64_t* d_counts, lc_stream stream);
 
 /* End-to-end decode from HOST memory to HOST memory on one stream: copies the blob
  * (h_blob, blob_bytes; pinned memory for true asynchrony) into the caller's device buffer

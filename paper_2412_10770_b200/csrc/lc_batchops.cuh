@@ -189,3 +189,96 @@ __global__ void __launch_bounds__(256) lc_bpairs_kernel(const SetopArgs a) {
                              (__ldg(a.l_off + p + 1) - __ldg(a.l_off + p)) - (m1 - m0)
                        : m1 - m0;
 }
+
+// ---- device-side plan (no host pass over the batch, no upload): per pair the short / long
+// list, then exclusive scans of the key and unit counts, then the chunk records to decode
+struct PlanArgs {
+    const BatchList* lists;
+    const uint32_t* pairs;  // 2 P list indices (device)
+    uint32_t* sl;           // [2 p] short, [2 p + 1] long
+    uint64_t* s_off;        // P + 1 (counts, then exclusive offsets; [P] = total)
+    uint64_t* l_off;
+    uint64_t* cap_off;
+    uint64_t* u_off;
+    uint32_t* sel;          // U chunk-record indices ...
+    uint64_t* sel_out;      // ... and output element offsets (short keys, then S + long keys)
+    uint32_t* err;          // bit 0: a pair index >= m
+    uint64_t U, S;          // the host plan's totals (capacities)
+    uint32_t P, m, n_chunks, OR;
+};
+
+__device__ __forceinline__ uint32_t list_chunks(uint32_t n) { return (n + 1023) >> 10; }
+
+__global__ void __launch_bounds__(256) lc_bplan_kernel(const PlanArgs a) {
+    const uint32_t p = blockIdx.x * 256 + threadIdx.x;
+    if (p >= a.P) return;
+    uint32_t x = __ldg(a.pairs + 2 * p), y = __ldg(a.pairs + 2 * p + 1);
+    if (x >= a.m || y >= a.m) {
+        atomicOr(a.err, 1u);
+        x = min(x, a.m - 1);
+        y = min(y, a.m - 1);
+    }
+    const uint32_t nx = a.lists[x].n, ny = a.lists[y].n;
+    const uint32_t sh = nx <= ny ? x : y, lg = nx <= ny ? y : x;
+    const uint32_t ns = min(nx, ny), nl = max(nx, ny);
+    a.sl[2 * p] = sh;
+    a.sl[2 * p + 1] = lg;
+    a.s_off[p] = ns;
+    a.l_off[p] = a.OR ? nl : 0;
+    a.cap_off[p] = ns + (a.OR ? nl : 0);
+    a.u_off[p] = list_chunks(ns) + (a.OR ? list_chunks(nl) : 0);
+}
+
+// exclusive scans of the four count arrays in one CTA ([P] receives the total)
+__global__ void __launch_bounds__(1024) lc_bscan_kernel(const PlanArgs a) {
+    __shared__ uint64_t part[32];
+    uint64_t* arr[4] = {a.s_off, a.l_off, a.cap_off, a.u_off};
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = (a.P + 1023) / 1024, lo = threadIdx.x * per, hi = min(lo + per, a.P);
+    for (int k = 0; k < 4; ++k) {
+        uint64_t* v = arr[k];
+        uint64_t sum = 0;
+        for (uint32_t i = lo; i < hi; ++i) sum += v[i];
+        uint64_t x = sum;  // inclusive scan of the thread sums
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) part[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint64_t q = part[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(kFull, q, o);
+                if (lane >= (uint32_t)o) q += y;
+            }
+            part[lane] = q;
+        }
+        __syncthreads();
+        uint64_t run = (warp ? part[warp - 1] : 0) + x - sum;
+        for (uint32_t i = lo; i < hi; ++i) {
+            const uint64_t c = v[i];
+            v[i] = run;
+            run += c;
+        }
+        if (threadIdx.x == 1023) v[a.P] = run;
+        __syncthreads();
+    }
+}
+
+// the chunk records of pair p's short list (and long list for OR), in key order
+__global__ void __launch_bounds__(256) lc_bexpand_kernel(const PlanArgs a) {
+    const uint32_t p = blockIdx.x * 256 + threadIdx.x;
+    if (p >= a.P) return;
+    uint64_t u = a.u_off[p];
+    for (int side = 0; side < (a.OR ? 2 : 1); ++side) {
+        const BatchList e = a.lists[a.sl[2 * p + side]];
+        const uint32_t H = list_chunks(e.n);
+        const bool small = e.pad[0] != 0xffffffffu;
+        const uint64_t dst = side ? a.S + a.l_off[p] : a.s_off[p];
+        for (uint32_t q = 0; q < H && u < a.U; ++q, ++u) {
+            a.sel[u] = small && q == H - 1 ? e.pad[0] : e.chunk0 + q;
+            a.sel_out[u] = dst + ((uint64_t)q << 10);
+        }
+    }
+}

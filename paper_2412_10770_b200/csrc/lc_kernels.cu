@@ -229,50 +229,6 @@ void pipe_release(HostPipe* p) {
     g_pipe_free.push_back(p);
 }
 
-// Pinned host staging buffers for per-call uploads (the batched AND / OR plan): a buffer is
-// reused once the event recorded after its last copy has completed, so the upload is
-// asynchronous (a pageable cudaMemcpyAsync would synchronize the stream first) and the host
-// builds the next plan while the GPU runs.  Buffers live until process exit.
-struct Staging {
-    int dev = -1;
-    void* h = nullptr;
-    size_t cap = 0;
-    cudaEvent_t ev = nullptr;
-};
-std::mutex g_stage_mu;
-std::vector<Staging*> g_stage;  // idle (or copy in flight, see ev)
-
-Staging* stage_acquire(size_t bytes) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    {
-        std::lock_guard<std::mutex> lk(g_stage_mu);
-        for (size_t k = 0; k < g_stage.size(); ++k) {
-            Staging* s = g_stage[k];
-            if (s->dev == dev && s->cap >= bytes && cudaEventQuery(s->ev) == cudaSuccess) {
-                g_stage.erase(g_stage.begin() + k);
-                return s;
-            }
-        }
-    }
-    Staging* s = new Staging;
-    s->dev = dev;
-    s->cap = bytes < (1u << 20) ? (1u << 20) : bytes;
-    if (cudaMallocHost(&s->h, s->cap) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming) != cudaSuccess) {
-        if (s->h) cudaFreeHost(s->h);
-        delete s;
-        return nullptr;
-    }
-    return s;
-}
-
-void stage_release(Staging* s, cudaStream_t st) {
-    cudaEventRecord(s->ev, st);
-    std::lock_guard<std::mutex> lk(g_stage_mu);
-    g_stage.push_back(s);
-}
-
 // host->device copy of `bytes` bytes
 int32_t copy_up(void* d, const void* h, uint64_t bytes, cudaStream_t st) {
     if (!bytes) return LC_OK;
@@ -871,146 +827,94 @@ int32_t lc_batch_init(lc_batch* b, const void* h_blobs, uint64_t h_bytes, const 
 }
 
 namespace {
-// Host plan of a batched AND / OR (lc_batchops.cuh): which list of each pair is short, the key
-// offsets, the chunk records to decode (the same record order as lc_batch_init: a list's chunks
-// of more than kSmallUnit keys from its big-region index on, its small last chunk after all big
-// records) and the scratch layout.
-struct SetopPlan {
-    uint64_t P, S, Lt, U, nwords, nblk;
-    uint64_t o_sl, o_soff, o_loff, o_cap, o_sel, o_selout, head;  // uploaded head
-    uint64_t o_keys, o_flags, o_mw, o_counts, o_rank, o_total, total;
-    uint64_t out_cap;  // output elements the caller provides
+// Scratch layout of a batched AND / OR (lc_batchops.cuh) from the plan's totals.
+struct SetopLayout {
+    uint64_t nwords, nblk;
+    uint64_t o_sl, o_soff, o_loff, o_cap, o_uoff, o_sel, o_selout, o_keys, o_flags, o_mw,
+        o_counts, o_rank, o_misc, total;
 };
-
-// fill: the head's bytes are written to `fill` (y->head bytes), nullptr to size only
-int32_t setop_plan(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pairs, uint32_t P,
-                   bool OR, uint8_t* fill, SetopPlan* y) {
-    if (!bt || !h_n || (!h_pairs && P) || !bt->d_lists) return LC_ERR_ARG;
-    const uint32_t m = bt->m;
-    const uint64_t kw = bt->key_bits / 8;
-    // record index of every list's first big chunk and of its small chunk
-    std::vector<uint64_t> big0(m), small_idx(m);
-    uint64_t nbig = 0, nsm = 0;
-    for (uint32_t k = 0; k < m; ++k) {
-        const uint64_t n = h_n[k], H = (n + 1023) >> 10, tail = n & 1023;
-        const bool sm = tail && tail <= kSmallUnit;
-        big0[k] = nbig;
-        nbig += H - sm;
-        small_idx[k] = sm ? nsm++ : ~0ULL;
-    }
-    if (nbig + nsm != bt->n_chunks) return LC_ERR_ARG;  // h_n does not describe this batch
-    uint64_t S = 0, Lt = 0, U = 0;
-    for (uint32_t p = 0; p < P; ++p) {
-        const uint32_t a = h_pairs[2 * p], b = h_pairs[2 * p + 1];
-        if (a >= m || b >= m) return LC_ERR_ARG;
-        const uint64_t ns = h_n[a] <= h_n[b] ? h_n[a] : h_n[b], nl = h_n[a] <= h_n[b] ? h_n[b] : h_n[a];
-        S += ns;
-        U += (ns + 1023) >> 10;
-        if (OR) {
-            Lt += nl;
-            U += (nl + 1023) >> 10;
-        }
-    }
-    if (S >= (1ULL << 32) || U >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
-    y->P = P;
-    y->S = S;
-    y->Lt = Lt;
-    y->U = U;
-    y->nwords = (S + 31) / 32 + 1;
-    y->nblk = (S + 255) / 256;
-    y->o_sl = 0;
-    y->o_soff = r256(8ULL * P);
-    y->o_loff = y->o_soff + r256(8 * (P + 1));
-    y->o_cap = y->o_loff + r256(8 * (P + 1));
-    y->o_sel = y->o_cap + r256(8 * (P + 1));
-    y->o_selout = y->o_sel + r256(4 * U);
-    y->head = y->o_selout + r256(8 * U);
-    y->o_keys = y->head;
-    y->o_flags = y->o_keys + r256(kw * (S + Lt));
-    y->o_mw = y->o_flags + r256(4 * y->nwords);
-    y->o_counts = y->o_mw + r256(4 * y->nwords);
-    y->o_rank = y->o_counts + r256(4 * (y->nblk + 1));
-    y->o_total = y->o_rank + (OR ? r256(4 * S) : 0);
-    y->total = y->o_total + 256;
-    y->out_cap = OR ? S + Lt : S;
-    if (!fill) return LC_OK;
-    uint8_t* H = fill;
-    uint32_t* sl = (uint32_t*)(H + y->o_sl);
-    uint64_t* soff = (uint64_t*)(H + y->o_soff);
-    uint64_t* loff = (uint64_t*)(H + y->o_loff);
-    uint64_t* cap = (uint64_t*)(H + y->o_cap);
-    uint32_t* sel = (uint32_t*)(H + y->o_sel);
-    uint64_t* selout = (uint64_t*)(H + y->o_selout);
-    uint64_t so = 0, lo = 0, co = 0, u = 0;
-    auto add_list = [&](uint32_t k, uint64_t dst) {  // decode list k to keys[dst ..)
-        const uint64_t n = h_n[k], Hk = (n + 1023) >> 10;
-        for (uint64_t q = 0; q < Hk; ++q, ++u) {
-            sel[u] = (uint32_t)(small_idx[k] != ~0ULL && q == Hk - 1 ? nbig + small_idx[k] : big0[k] + q);
-            selout[u] = dst + (q << 10);
-        }
-    };
-    for (uint32_t p = 0; p < P; ++p) {
-        const uint32_t a = h_pairs[2 * p], b = h_pairs[2 * p + 1];
-        const uint32_t sh = h_n[a] <= h_n[b] ? a : b, lg = h_n[a] <= h_n[b] ? b : a;
-        sl[2 * p] = sh;
-        sl[2 * p + 1] = lg;
-        soff[p] = so;
-        loff[p] = lo;
-        cap[p] = co;
-        add_list(sh, so);
-        if (OR) add_list(lg, S + lo);
-        so += h_n[sh];
-        if (OR) lo += h_n[lg];
-        co += h_n[sh] + (OR ? h_n[lg] : 0);
-    }
-    soff[P] = so;
-    loff[P] = lo;
-    cap[P] = co;
-    return LC_OK;
+SetopLayout setop_layout(const lc_setop_plan& q, uint32_t key_bits) {
+    const uint64_t P = q.n_pairs, S = q.short_keys, Lt = q.long_keys, U = q.units;
+    SetopLayout y;
+    y.nwords = (S + 31) / 32 + 1;
+    y.nblk = (S + 255) / 256;
+    y.o_sl = 0;
+    y.o_soff = r256(8ULL * P);
+    y.o_loff = y.o_soff + r256(8 * (P + 1));
+    y.o_cap = y.o_loff + r256(8 * (P + 1));
+    y.o_uoff = y.o_cap + r256(8 * (P + 1));
+    y.o_sel = y.o_uoff + r256(8 * (P + 1));
+    y.o_selout = y.o_sel + r256(4 * U);
+    y.o_keys = y.o_selout + r256(8 * U);
+    y.o_flags = y.o_keys + r256((key_bits / 8) * (S + Lt));
+    y.o_mw = y.o_flags + r256(4 * y.nwords);
+    y.o_counts = y.o_mw + r256(4 * y.nwords);
+    y.o_rank = y.o_counts + r256(4 * (y.nblk + 1));
+    y.o_misc = y.o_rank + (q.op == LC_SETOP_OR ? r256(4 * S) : 0);  // total, work, err
+    y.total = y.o_misc + 256;
+    return y;
 }
 
-int32_t setop_batch(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_pairs, uint32_t P,
-                    bool OR, void* d_scratch, uint64_t scratch_bytes, void* d_out,
-                    uint64_t* d_out_off, uint64_t* d_counts, cudaStream_t st) {
-    if (!d_scratch || ((uintptr_t)d_scratch & 255) || !d_out || !d_out_off || !d_counts)
+int32_t setop_batch(const lc_batch* bt, const lc_setop_plan* q, const uint32_t* d_pairs, bool OR,
+                    void* d_scratch, uint64_t scratch_bytes, void* d_out, uint64_t* d_out_off,
+                    uint64_t* d_counts, cudaStream_t st) {
+    if (!bt || !q || !bt->d_lists || !d_scratch || ((uintptr_t)d_scratch & 255) || !d_out ||
+        !d_out_off || !d_counts || (q->op == LC_SETOP_OR) != OR || (q->n_pairs && !d_pairs))
         return LC_ERR_ARG;
+    const uint32_t P = q->n_pairs;
     if (!P) return LC_OK;
-    SetopPlan y;
-    int32_t rc = setop_plan(bt, h_n, h_pairs, P, OR, nullptr, &y);  // sizes
-    if (rc) return rc;
+    const SetopLayout y = setop_layout(*q, bt->key_bits);
     if (scratch_bytes < y.total) return LC_ERR_ARG;
-    Staging* sg = stage_acquire(y.head);
-    if (!sg) return LC_ERR_ALLOC;
-    std::memset(sg->h, 0, y.head);
-    setop_plan(bt, h_n, h_pairs, P, OR, (uint8_t*)sg->h, &y);
     uint8_t* D = (uint8_t*)d_scratch;
-    const bool cp_ok = cudaMemcpyAsync(D, sg->h, y.head, cudaMemcpyHostToDevice, st) == cudaSuccess;
-    stage_release(sg, st);
-    if (!cp_ok || cudaMemsetAsync(D + y.o_flags, 0, 4 * y.nwords, st) != cudaSuccess)
+    uint64_t* misc = (uint64_t*)(D + y.o_misc);  // [0] scan total, [1] work counter, [2] error
+    if (cudaMemsetAsync(D + y.o_flags, 0, 4 * y.nwords, st) != cudaSuccess ||
+        cudaMemsetAsync(misc + 2, 0, 8, st) != cudaSuccess)
         return LC_ERR_CUDA;
-    if ((rc = launch_batch_decode(bt, (const uint32_t*)(D + y.o_sel),
-                                  (const uint64_t*)(D + y.o_selout), nullptr, (uint32_t)y.U,
-                                  D + y.o_keys, (uint32_t*)(D + y.o_total + 8), st)))
-        return rc;
+    // ---- plan on the device: short / long sides, offsets, chunk records to decode
+    PlanArgs pa;
+    pa.lists = (const BatchList*)bt->d_lists;
+    pa.pairs = d_pairs;
+    pa.sl = (uint32_t*)(D + y.o_sl);
+    pa.s_off = (uint64_t*)(D + y.o_soff);
+    pa.l_off = (uint64_t*)(D + y.o_loff);
+    pa.cap_off = (uint64_t*)(D + y.o_cap);
+    pa.u_off = (uint64_t*)(D + y.o_uoff);
+    pa.sel = (uint32_t*)(D + y.o_sel);
+    pa.sel_out = (uint64_t*)(D + y.o_selout);
+    pa.err = (uint32_t*)(misc + 2);
+    pa.U = q->units;
+    pa.S = q->short_keys;
+    pa.P = P;
+    pa.m = bt->m;
+    pa.n_chunks = (uint32_t)bt->n_chunks;
+    pa.OR = OR;
+    const unsigned gp = (P + 255) / 256;
+    lc_bplan_kernel<<<gp, 256, 0, st>>>(pa);
+    lc_bscan_kernel<<<1, 1024, 0, st>>>(pa);
+    lc_bexpand_kernel<<<gp, 256, 0, st>>>(pa);
+    lc_detail::count_launch(3);
+    int32_t rc = launch_batch_decode(bt, pa.sel, pa.sel_out, nullptr, (uint32_t)q->units,
+                                     D + y.o_keys, (uint32_t*)(misc + 1), st);
+    if (rc) return rc;
     const bool k64 = bt->key_bits == 64;
     SetopArgs a;
-    a.lists = (const BatchList*)bt->d_lists;
-    a.sl = (const uint32_t*)(D + y.o_sl);
-    a.s_off = (const uint64_t*)(D + y.o_soff);
-    a.l_off = (const uint64_t*)(D + y.o_loff);
-    a.cap_off = (const uint64_t*)(D + y.o_cap);
+    a.lists = pa.lists;
+    a.sl = pa.sl;
+    a.s_off = pa.s_off;
+    a.l_off = pa.l_off;
+    a.cap_off = pa.cap_off;
     a.keys_s = D + y.o_keys;
-    a.keys_l = D + y.o_keys + (bt->key_bits / 8) * y.S;
+    a.keys_l = D + y.o_keys + (bt->key_bits / 8) * q->short_keys;
     a.flags = (uint32_t*)(D + y.o_flags);
     a.mw = (uint32_t*)(D + y.o_mw);
     a.counts = (uint32_t*)(D + y.o_counts);
     a.rank = (uint32_t*)(D + y.o_rank);
-    a.total = (uint64_t*)(D + y.o_total);
+    a.total = misc;
     a.out = d_out;
     a.d_out_off = d_out_off;
     a.d_counts = d_counts;
-    a.S = y.S;
-    a.Lt = y.Lt;
+    a.S = q->short_keys;
+    a.Lt = q->long_keys;
     a.P = P;
     a.nblk = (uint32_t)y.nblk;
     a.nwords = (uint32_t)y.nwords;
@@ -1026,43 +930,59 @@ int32_t setop_batch(const lc_batch* bt, const uint64_t* h_n, const uint32_t* h_p
     if (k64) OR ? lc_bwrite_s_kernel<true, true><<<gs, 256, 0, st>>>(a) : lc_bwrite_s_kernel<true, false><<<gs, 256, 0, st>>>(a);
     else OR ? lc_bwrite_s_kernel<false, true><<<gs, 256, 0, st>>>(a) : lc_bwrite_s_kernel<false, false><<<gs, 256, 0, st>>>(a);
     uint32_t nl = 5;
-    if (OR && y.Lt) {
-        const unsigned gl = (unsigned)((y.Lt + 255) / 256);
+    if (OR && q->long_keys) {
+        const unsigned gl = (unsigned)((q->long_keys + 255) / 256);
         if (k64) lc_bwrite_l_kernel<true><<<gl, 256, 0, st>>>(a);
         else lc_bwrite_l_kernel<false><<<gl, 256, 0, st>>>(a);
         ++nl;
     }
-    const unsigned gp = (unsigned)((P + 1 + 255) / 256);
-    if (OR) lc_bpairs_kernel<true><<<gp, 256, 0, st>>>(a);
-    else lc_bpairs_kernel<false><<<gp, 256, 0, st>>>(a);
+    const unsigned gq = (unsigned)((P + 1 + 255) / 256);
+    if (OR) lc_bpairs_kernel<true><<<gq, 256, 0, st>>>(a);
+    else lc_bpairs_kernel<false><<<gq, 256, 0, st>>>(a);
     lc_detail::count_launch(nl);
     return cuda_status();
 }
 }  // namespace
 
-int32_t lc_setop_batch_scratch_bytes(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                                     uint32_t n_pairs, int32_t op, uint64_t* scratch_bytes,
-                                     uint64_t* out_keys) {
-    if (!scratch_bytes || !out_keys || (op != LC_SETOP_AND && op != LC_SETOP_OR)) return LC_ERR_ARG;
-    SetopPlan y;
-    const int32_t rc = setop_plan(b, h_n, h_pairs, n_pairs, op == LC_SETOP_OR, nullptr, &y);
-    if (rc) return rc;
-    *scratch_bytes = y.total;
-    *out_keys = y.out_cap;
+int32_t lc_setop_batch_plan(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
+                            uint32_t n_pairs, int32_t op, lc_setop_plan* plan) {
+    if (!b || !h_n || !plan || (!h_pairs && n_pairs) || (op != LC_SETOP_AND && op != LC_SETOP_OR))
+        return LC_ERR_ARG;
+    const bool OR = op == LC_SETOP_OR;
+    uint64_t S = 0, Lt = 0, U = 0;
+    for (uint32_t p = 0; p < n_pairs; ++p) {
+        const uint32_t x = h_pairs[2 * p], y = h_pairs[2 * p + 1];
+        if (x >= b->m || y >= b->m) return LC_ERR_ARG;
+        const uint64_t ns = h_n[x] <= h_n[y] ? h_n[x] : h_n[y], nl = h_n[x] <= h_n[y] ? h_n[y] : h_n[x];
+        S += ns;
+        U += (ns + 1023) >> 10;
+        if (OR) {
+            Lt += nl;
+            U += (nl + 1023) >> 10;
+        }
+    }
+    if (S >= (1ULL << 32) || U >= (1ULL << 32)) return LC_ERR_TOO_LARGE;
+    plan->n_pairs = n_pairs;
+    plan->op = op;
+    plan->short_keys = S;
+    plan->long_keys = Lt;
+    plan->units = U;
+    plan->scratch_bytes = setop_layout(*plan, b->key_bits).total;
+    plan->out_keys = S + Lt;
     return LC_OK;
 }
 
-int32_t lc_intersect_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                           uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
+int32_t lc_intersect_batch(const lc_batch* b, const lc_setop_plan* plan, const uint32_t* d_pairs,
+                           void* d_scratch, uint64_t scratch_bytes, void* d_out,
                            uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream) {
-    return setop_batch(b, h_n, h_pairs, n_pairs, false, d_scratch, scratch_bytes, d_out, d_out_off,
+    return setop_batch(b, plan, d_pairs, false, d_scratch, scratch_bytes, d_out, d_out_off,
                        d_counts, (cudaStream_t)stream);
 }
 
-int32_t lc_union_batch(const lc_batch* b, const uint64_t* h_n, const uint32_t* h_pairs,
-                       uint32_t n_pairs, void* d_scratch, uint64_t scratch_bytes, void* d_out,
-                       uint64_t* d_out_off, uint64_t* d_counts, lc_stream stream) {
-    return setop_batch(b, h_n, h_pairs, n_pairs, true, d_scratch, scratch_bytes, d_out, d_out_off,
+int32_t lc_union_batch(const lc_batch* b, const lc_setop_plan* plan, const uint32_t* d_pairs,
+                       void* d_scratch, uint64_t scratch_bytes, void* d_out, uint64_t* d_out_off,
+                       uint64_t* d_counts, lc_stream stream) {
+    return setop_batch(b, plan, d_pairs, true, d_scratch, scratch_bytes, d_out, d_out_off,
                        d_counts, (cudaStream_t)stream);
 }
 

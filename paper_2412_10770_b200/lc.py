@@ -47,6 +47,12 @@ class lc_batch(C.Structure):
                 ("d_lists", C.c_void_p), ("d_chunks", C.c_void_p), ("d_small", C.c_void_p)]
 
 
+class lc_setop_plan(C.Structure):
+    _fields_ = [("n_pairs", C.c_uint32), ("op", C.c_int32), ("short_keys", C.c_uint64),
+                ("long_keys", C.c_uint64), ("units", C.c_uint64), ("scratch_bytes", C.c_uint64),
+                ("out_keys", C.c_uint64)]
+
+
 class lc_view(C.Structure):
     _fields_ = [("h", lc_header), ("d_blob", C.c_void_p), ("d_first", C.c_void_p),
                 ("d_acc", C.c_void_p), ("span_lo", C.c_uint64), ("span_hi", C.c_uint64), ("sec_base", C.c_uint64 * 4)]
@@ -79,10 +85,12 @@ _sig = {
     "lc_batch_dir_bytes": ([_p, _u64, _p, _u32, C.POINTER(_u64)], _i32),
     "lc_batch_init": ([C.POINTER(lc_batch), _p, _u64, _p, _u32, _p, _p, _p, _u64, _p], _i32),
     "lc_decode_batch": ([C.POINTER(lc_batch), _p, _p, _p], _i32),
-    "lc_setop_batch_scratch_bytes": ([C.POINTER(lc_batch), _p, _p, _u32, _i32, C.POINTER(_u64),
-                                      C.POINTER(_u64)], _i32),
-    "lc_intersect_batch": ([C.POINTER(lc_batch), _p, _p, _u32, _p, _u64, _p, _p, _p, _p], _i32),
-    "lc_union_batch": ([C.POINTER(lc_batch), _p, _p, _u32, _p, _u64, _p, _p, _p, _p], _i32),
+    "lc_setop_batch_plan": ([C.POINTER(lc_batch), _p, _p, _u32, _i32, C.POINTER(lc_setop_plan)],
+                            _i32),
+    "lc_intersect_batch": ([C.POINTER(lc_batch), C.POINTER(lc_setop_plan), _p, _p, _u64, _p, _p,
+                            _p, _p], _i32),
+    "lc_union_batch": ([C.POINTER(lc_batch), C.POINTER(lc_setop_plan), _p, _p, _u64, _p, _p, _p,
+                        _p], _i32),
     "lc_status_str": ([_i32], C.c_char_p),
     "lc_launch_count": ([], _u64),
 }
@@ -532,36 +540,36 @@ LC_SETOP_AND, LC_SETOP_OR = 0, 1
 
 
 class SetopBuffers:
-    """Scratch, output and result arrays of one batched AND / OR over fixed pairs (reusable)."""
+    """One batched AND / OR query batch: its host plan (lc_setop_batch_plan), the pairs on the
+    device, and the scratch / output / result arrays (reusable for repeated runs)."""
 
     def __init__(self, batch: Batch, pairs, op: int):
         import torch
         self.pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)
         self.h_n = np.ascontiguousarray(batch.n, np.uint64)
         self.op = op
-        sb, ok = C.c_uint64(), C.c_uint64()
-        _check(_lib.lc_setop_batch_scratch_bytes(C.byref(batch.b), self.h_n.ctypes.data,
-                                                 self.pairs.ctypes.data, len(self.pairs), op,
-                                                 C.byref(sb), C.byref(ok)),
-               "lc_setop_batch_scratch_bytes")
+        self.plan = lc_setop_plan()
+        _check(_lib.lc_setop_batch_plan(C.byref(batch.b), self.h_n.ctypes.data,
+                                        self.pairs.ctypes.data, len(self.pairs), op,
+                                        C.byref(self.plan)), "lc_setop_batch_plan")
         dev = batch.d_blobs.device
-        self.scratch = torch.empty(max(sb.value, 256), dtype=torch.uint8, device=dev)
-        self.out = torch.empty(max(ok.value, 1), dtype=batch.torch_dtype, device=dev)
+        self.d_pairs = torch.from_numpy(self.pairs.view(np.int32).reshape(-1).copy()).to(dev)
+        self.scratch = torch.empty(max(self.plan.scratch_bytes, 256), dtype=torch.uint8, device=dev)
+        self.out = torch.empty(max(self.plan.out_keys, 1), dtype=batch.torch_dtype, device=dev)
         self.out_off = torch.zeros(len(self.pairs) + 1, dtype=torch.int64, device=dev)
         self.counts = torch.zeros(max(len(self.pairs), 1), dtype=torch.int64, device=dev)
 
     def tensors(self):
-        return (self.scratch, self.out, self.out_off, self.counts)
+        return (self.d_pairs, self.scratch, self.out, self.out_off, self.counts)
 
 
 def _setop_batch(fn, what, batch: Batch, pairs, op, bufs, stream):
     if bufs is None:
         bufs = SetopBuffers(batch, pairs, op)
     with _On(stream, *batch.tensors(), *bufs.tensors()) as on:
-        _check(fn(C.byref(batch.b), bufs.h_n.ctypes.data, bufs.pairs.ctypes.data,
-                  len(bufs.pairs), bufs.scratch.data_ptr(), bufs.scratch.numel(),
-                  bufs.out.data_ptr(), bufs.out_off.data_ptr(), bufs.counts.data_ptr(),
-                  on.handle), what)
+        _check(fn(C.byref(batch.b), C.byref(bufs.plan), bufs.d_pairs.data_ptr(),
+                  bufs.scratch.data_ptr(), bufs.scratch.numel(), bufs.out.data_ptr(),
+                  bufs.out_off.data_ptr(), bufs.counts.data_ptr(), on.handle), what)
     return bufs
 
 
