@@ -30,6 +30,8 @@ struct SetopArgs {
     void* out;
     uint64_t* d_out_off;      // P + 1 result offsets
     uint64_t* d_counts;       // P result sizes
+    const uint32_t* blk_s;    // pair holding short key 1024 g (or the pair before it)
+    const uint32_t* blk_l;    // pair holding long key 1024 g (OR)
     uint64_t S, Lt;
     uint32_t P, nblk, nwords;
 };
@@ -39,15 +41,12 @@ __device__ __forceinline__ uint64_t key_at(const void* base, uint64_t i) {
     return K64 ? __ldg((const uint64_t*)base + i) : (uint64_t)__ldg((const uint32_t*)base + i);
 }
 
-// pair of element g: max{p : off[p] <= g} over the P + 1 offsets (off[0] = 0)
-__device__ __forceinline__ uint32_t pair_of(const uint64_t* off, uint32_t P, uint64_t g) {
-    uint32_t lo = 0, hi = P;  // off[P] = total > g
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(off + mid) <= g) lo = mid;
-        else hi = mid;
-    }
-    return lo;
+// pair of element g: max{p : off[p] <= g} over the P + 1 offsets (off[0] = 0), from the pair
+// recorded for g's 1024-element block (blk[g / 1024] <= the answer) and a short forward walk
+__device__ __forceinline__ uint32_t pair_of(const uint32_t* blk, const uint64_t* off, uint64_t g) {
+    uint32_t p = __ldg(blk + (g >> 10));
+    while (__ldg(off + p + 1) <= g) ++p;
+    return p;
 }
 
 // #{t < n : keys[t] < x} over decoded keys
@@ -95,7 +94,7 @@ __global__ void __launch_bounds__(256) lc_bprobe_kernel(const SetopArgs a) {
     bool found = false;
     if (live) {
         const uint64_t x = key_at<K64>(a.keys_s, g);
-        const uint32_t p = pair_of(a.s_off, a.P, g);
+        const uint32_t p = pair_of(a.blk_s, a.s_off, g);
         if (OR) {
             const uint64_t lo = __ldg(a.l_off + p), nl = __ldg(a.l_off + p + 1) - lo;
             const uint64_t r = lower_bound_keys<K64>(a.keys_l, lo, nl, x);
@@ -152,7 +151,7 @@ __global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
     if (!OR) {
         pos = matches_before(a, g);
     } else {
-        const uint32_t p = pair_of(a.s_off, a.P, g);
+        const uint32_t p = pair_of(a.blk_s, a.s_off, g);
         const uint64_t s0 = __ldg(a.s_off + p);
         pos = __ldg(a.cap_off + p) + (g - s0) + __ldg(a.rank + g) -
               (matches_before(a, g) - matches_before(a, s0));
@@ -166,7 +165,7 @@ template <bool K64>
 __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
     const uint64_t gl = (uint64_t)blockIdx.x * 256 + threadIdx.x;
     if (gl >= a.Lt) return;
-    const uint32_t p = pair_of(a.l_off, a.P, gl);
+    const uint32_t p = pair_of(a.blk_l, a.l_off, gl);
     const uint64_t y = key_at<K64>(a.keys_l, gl);
     const uint64_t s0 = __ldg(a.s_off + p), ns = __ldg(a.s_off + p + 1) - s0;
     const uint64_t ra = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
@@ -202,6 +201,8 @@ struct PlanArgs {
     uint64_t* u_off;
     uint32_t* sel;          // U chunk-record indices ...
     uint64_t* sel_out;      // ... and output element offsets (short keys, then S + long keys)
+    uint32_t* blk_s;        // pair of short key 1024 g, for g < ceil(S / 1024)
+    uint32_t* blk_l;        // pair of long key 1024 g (OR)
     uint32_t* err;          // bit 0: a pair index >= m
     uint64_t U, S;          // the host plan's totals (capacities)
     uint32_t P, m, n_chunks, OR;
@@ -270,6 +271,13 @@ __global__ void __launch_bounds__(1024) lc_bscan_kernel(const PlanArgs a) {
 __global__ void __launch_bounds__(256) lc_bexpand_kernel(const PlanArgs a) {
     const uint32_t p = blockIdx.x * 256 + threadIdx.x;
     if (p >= a.P) return;
+    // block tables: every 1024-key block starting inside this pair's keys names it
+    for (uint64_t g = (a.s_off[p] + 1023) >> 10; (g << 10) < a.s_off[p + 1]; ++g) a.blk_s[g] = p;
+    if (p == 0) a.blk_s[0] = 0;
+    if (a.OR) {
+        for (uint64_t g = (a.l_off[p] + 1023) >> 10; (g << 10) < a.l_off[p + 1]; ++g) a.blk_l[g] = p;
+        if (p == 0) a.blk_l[0] = 0;
+    }
     uint64_t u = a.u_off[p];
     for (int side = 0; side < (a.OR ? 2 : 1); ++side) {
         const BatchList e = a.lists[a.sl[2 * p + side]];

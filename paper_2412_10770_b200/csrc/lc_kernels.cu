@@ -830,8 +830,8 @@ namespace {
 // Scratch layout of a batched AND / OR (lc_batchops.cuh) from the plan's totals.
 struct SetopLayout {
     uint64_t nwords, nblk;
-    uint64_t o_sl, o_soff, o_loff, o_cap, o_uoff, o_sel, o_selout, o_keys, o_flags, o_mw,
-        o_counts, o_rank, o_misc, total;
+    uint64_t o_sl, o_soff, o_loff, o_cap, o_uoff, o_sel, o_selout, o_blks, o_blkl, o_keys,
+        o_flags, o_mw, o_counts, o_rank, o_misc, total;
 };
 SetopLayout setop_layout(const lc_setop_plan& q, uint32_t key_bits) {
     const uint64_t P = q.n_pairs, S = q.short_keys, Lt = q.long_keys, U = q.units;
@@ -845,7 +845,9 @@ SetopLayout setop_layout(const lc_setop_plan& q, uint32_t key_bits) {
     y.o_uoff = y.o_cap + r256(8 * (P + 1));
     y.o_sel = y.o_uoff + r256(8 * (P + 1));
     y.o_selout = y.o_sel + r256(4 * U);
-    y.o_keys = y.o_selout + r256(8 * U);
+    y.o_blks = y.o_selout + r256(8 * U);
+    y.o_blkl = y.o_blks + r256(4 * ((S + 1023) / 1024 + 1));
+    y.o_keys = y.o_blkl + r256(4 * ((Lt + 1023) / 1024 + 1));
     y.o_flags = y.o_keys + r256((key_bits / 8) * (S + Lt));
     y.o_mw = y.o_flags + r256(4 * y.nwords);
     y.o_counts = y.o_mw + r256(4 * y.nwords);
@@ -882,6 +884,8 @@ int32_t setop_batch(const lc_batch* bt, const lc_setop_plan* q, const uint32_t* 
     pa.sel = (uint32_t*)(D + y.o_sel);
     pa.sel_out = (uint64_t*)(D + y.o_selout);
     pa.err = (uint32_t*)(misc + 2);
+    pa.blk_s = (uint32_t*)(D + y.o_blks);
+    pa.blk_l = (uint32_t*)(D + y.o_blkl);
     pa.U = q->units;
     pa.S = q->short_keys;
     pa.P = P;
@@ -913,6 +917,8 @@ int32_t setop_batch(const lc_batch* bt, const lc_setop_plan* q, const uint32_t* 
     a.out = d_out;
     a.d_out_off = d_out_off;
     a.d_counts = d_counts;
+    a.blk_s = pa.blk_s;
+    a.blk_l = pa.blk_l;
     a.S = q->short_keys;
     a.Lt = q->long_keys;
     a.P = P;
