@@ -7,7 +7,9 @@ import sys
 from collections import defaultdict
 
 
-def main(path: str, out: str, alg_bytes: float = 1086177040.0, steps: int = 5, warmup: int = 3):
+def main(path: str, out: str, alg_bytes: float = 4396297936.0, steps: int = 5, warmup: int = 3,
+         raw: str = "r02_launches_bench.csv"):
+    """alg_bytes: algorithmic bytes of one headline decode (config 4 = blob + 5e8 x 8 B)."""
     rows = list(csv.reader(open(path)))
     hdr, recs = None, []
     for r in rows:
@@ -26,14 +28,16 @@ def main(path: str, out: str, alg_bytes: float = 1086177040.0, steps: int = 5, w
     lines = [
         f"# ncu launch list of `python bench.py --steps {steps} --warmup {warmup} --no-cpu`",
         "# (ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised)",
-        f"total kernels launched: {len(recs)} (raw list: r01_launches_bench.csv)",
+        f"total kernels launched: {len(recs)} (raw list: {raw})",
         f"lc_decode_kernel full-list launches ({warmup} warm-up + {steps} timed): "
         + ", ".join(f"{t:.1f} us" for t in full),
-        f"  mean of the timed launches: {mean:.1f} us -> {alg_bytes / (mean * 1e-6) / 1e9:.0f} GB/s algorithmic",
+        f"  mean of the timed launches: {mean:.1f} us -> {alg_bytes / (mean * 1e-6) / 1e9:.0f} GB/s "
+        f"algorithmic ({alg_bytes:.0f} B per launch)",
         f"other lc_decode_kernel launches (e2e spans, intersect/union decodes): {len(spans)}, "
         f"mean {sum(spans) / max(len(spans), 1):.1f} us",
         "a bench step is exactly one lc_decode_kernel launch (100% of the timed region); torch",
-        "kernels (compare/index) are the post-timing bit-exact checks, outside the timed region.",
+        "kernels (compare/index) are the post-timing bit-exact checks, outside the timed region;",
+        "the other lc_* kernels are the decode_configs / F7 / corpus / access blocks of the line.",
         "",
         "per-kernel totals (count, total us):",
     ]
@@ -48,4 +52,4 @@ def main(path: str, out: str, alg_bytes: float = 1086177040.0, steps: int = 5, w
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], *(float(x) for x in sys.argv[3:4]))
