@@ -448,54 +448,6 @@ __device__ __forceinline__ BatchChunk load_chunk(const BatchChunk* p) {
     return r;
 }
 
-// quads [0, nq) of a staged chunk with the residual width as a compile-time constant, for
-// widths LC_BATCH_CT_LO .. LC_BATCH_CT_HI; false (nothing done) for other widths
-#ifndef LC_BATCH_CT_LO
-#define LC_BATCH_CT_LO 8
-#endif
-#ifndef LC_BATCH_CT_HI
-#define LC_BATCH_CT_HI 28
-#endif
-template <bool K64, bool SPARSE, uint32_t B>
-__device__ __forceinline__ bool batch_quads_b(uint32_t nq, Page& pg, const Sections& sec, uint32_t& jb,
-                                              uint32_t& sb, uint32_t jlast, uint32_t key0,
-                                              uint32_t lane, uint32_t lmask, uint32_t lw, uint32_t ls,
-                                              uint32_t bias, uint8_t* outl, Ins& ins) {
-    constexpr uint32_t kw = K64 ? 8 : 4;
-#pragma unroll 1
-    for (uint32_t g = 0; g < nq; ++g)
-        decode_quad<K64, B, false, false, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * g, g, lane,
-                                                  lmask, lw, ls, bias, outl + 128 * kw * g, ins);
-    return true;
-}
-template <bool K64, bool SPARSE, uint32_t... Bs>
-__device__ __forceinline__ bool batch_quads_dispatch(std::integer_sequence<uint32_t, Bs...>, uint32_t b,
-                                                     uint32_t nq, Page& pg, const Sections& sec,
-                                                     uint32_t& jb, uint32_t& sb, uint32_t jlast,
-                                                     uint32_t key0, uint32_t lane, uint32_t lmask,
-                                                     uint32_t lw, uint32_t ls, uint32_t bias,
-                                                     uint8_t* outl, Ins& ins) {
-    bool done = false;
-    ((b == LC_BATCH_CT_LO + Bs && !done
-          ? (done = batch_quads_b<K64, SPARSE, LC_BATCH_CT_LO + Bs>(nq, pg, sec, jb, sb, jlast, key0,
-                                                                    lane, lmask, lw, ls, bias, outl,
-                                                                    ins))
-          : false),
-     ...);
-    return done;
-}
-template <bool K64, bool SPARSE>
-__device__ __forceinline__ bool batch_quads_ct(uint32_t b, uint32_t nq, Page& pg, const Sections& sec,
-                                               uint32_t& jb, uint32_t& sb, uint32_t jlast,
-                                               uint32_t key0, uint32_t lane, uint32_t lmask,
-                                               uint32_t lw, uint32_t ls, uint32_t bias, uint8_t* outl,
-                                               Ins& ins) {
-    if (b < LC_BATCH_CT_LO || b > LC_BATCH_CT_HI) return false;
-    return batch_quads_dispatch<K64, SPARSE>(
-        std::make_integer_sequence<uint32_t, LC_BATCH_CT_HI - LC_BATCH_CT_LO + 1>{}, b, nq, pg, sec,
-        jb, sb, jlast, key0, lane, lmask, lw, ls, bias, outl, ins);
-}
-
 template <bool K64, bool SPARSE>
 __global__ void __launch_bounds__(kThreads, 4)
     lc_decode_batch_kernel(const BatchArgs a) {
@@ -610,18 +562,11 @@ __global__ void __launch_bounds__(kThreads, 4)
         const uint32_t key0 = r.key0, jlast = r.jlast;
         if (jlast < pg.pj + pg.cp) {  // every segment of the unit staged: no re-page checks
             const uint32_t nq = nk >> 7;  // whole 128-key quads
-            // the hot loop with a compile-time width for the common posting-list widths (the
-            // field then needs no runtime multiply / second word), runtime otherwise
-            if (!batch_quads_ct<K64, SPARSE>(b, nq, pg, sec, jb, sb, jlast, key0, lane, lmask, lw,
-                                              ls, r.bias, outl, ins)) {
 #pragma unroll 1
-                for (uint32_t g = 0; g < nq; ++g)
-                    decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast,
-                                                                 key0 + 128 * g, g, lane, lmask, lw,
-                                                                 ls, r.bias, outl + 128 * kw * g,
-                                                                 ins);
-            }
-            outl += 128 * kw * nq;
+            for (uint32_t g = 0; g < nq; ++g, outl += 128 * kw)
+                decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * g,
+                                                             g, lane, lmask, lw, ls, r.bias, outl,
+                                                             ins);
             for (uint32_t w = 4 * nq; 32 * w < nk; ++w, outl += 32 * kw)
                 decode_window<K64, kRtB, false, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
                                                               w, lane, lmask, lw, ls, r.bias, outl,
