@@ -572,10 +572,18 @@ def _sync_barrier(ws):
     torch.cuda.synchronize()
 
 
+def _coll_device(dev):
+    """Device of the timing collectives: the GPU under NCCL, the host under gloo (test runs)."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return dev
+
+
 def _max_over_ranks(x, ws, dev):
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_coll_device(dev))
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -620,10 +628,17 @@ def run_gpu(args):
     from synth import make_keys
 
     ws, rank, local = _env_dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # LC_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0, gloo for the timing collectives,
+    # to exercise the N > 1 control flow on a one-GPU box
+    one_gpu = os.environ.get("LC_BENCH_ONE_GPU") == "1"
+    gpu = 0 if one_gpu else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
     cid = args.config
     spec = _spec(cid)
@@ -660,7 +675,7 @@ def run_gpu(args):
     _sync_barrier(ws)
     c0 = lc.launch_count()
     with torch.cuda.stream(stream):
-        with ClockSampler(local) as clk:
+        with ClockSampler(gpu) as clk:
             total, per = _time_launches(step, stream, args.steps, args.warmup, ws)
         launches = lc.launch_count() - c0 - args.warmup * (view is not None)
         t_max = _max_over_ranks(total, ws, dev)
@@ -704,7 +719,7 @@ def run_gpu(args):
     e2e_t = _max_over_ranks(e2e_total, ws, dev)
     h2d_all = h2d
     if ws > 1:  # bytes every rank uploads per step (its shard)
-        tt = torch.tensor([float(h2d)], dtype=torch.float64, device=dev)
+        tt = torch.tensor([float(h2d)], dtype=torch.float64, device=_coll_device(dev))
         dist.all_reduce(tt)
         h2d_all = int(tt.item())
     e2e_value = alg_bytes * e2e_steps / e2e_t / 1e9
@@ -740,7 +755,7 @@ def run_gpu(args):
             keys2 = kc
         if k + 1 < len(extra):
             pending[extra[k + 1]] = pool.submit(make_keys, extra[k + 1])
-        with ClockSampler(local) as clk_c:
+        with ClockSampler(gpu) as clk_c:
             decode_configs[f"config{c}"] = _decode_config(c, kc, dev, stream, cfg_steps, 3, peak)
         decode_configs[f"config{c}"]["clocks"] = clk_c.summary()
         del kc

@@ -52,3 +52,28 @@ def test_product_arm_line():
     # both arms name the same workload with the same config dict
     r = _run("--impl", "reference", "--config", "1", "--steps", "2", "--warmup", "3")
     assert r["config"] == d["config"]
+
+
+@pytest.mark.gpu
+def test_product_arm_two_ranks_on_one_gpu():
+    """The N > 1 path (torchrun, strong scaling over shard views, max-over-ranks timing) with
+    two ranks on the one GPU of a test box (LC_BENCH_ONE_GPU: gloo for the timing collectives;
+    the ranks' kernels never wait on each other)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, LC_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "2",
+                        "--steps", "3", "--warmup", "3"], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert "shards x2" in d["config"]["parallelism"]
+    assert d["e2e"]["h2d_bytes_per_step"] < 1.05 * d["config"]["blob_bytes"]  # each rank its shard
+    assert d["gpu_launches"] >= d["steps"]
