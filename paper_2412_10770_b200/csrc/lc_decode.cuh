@@ -26,6 +26,7 @@ struct DecodeArgs {
 struct Ins {
     const uint32_t* rho;
     uint32_t key0, cur, end, bat, v, nxt;
+    const uint2* desc;  // SH == 1: per-window {insertion bitmask, shift at the window start}
 };
 
 // chunk start: [lo, hi) = [coff[h], coff[h+1]) (loaded one chunk ahead); the first batch's
@@ -76,10 +77,17 @@ __device__ __forceinline__ uint32_t ins_shift(Ins& s, uint32_t wb, uint32_t lane
     return c0 + add;
 }
 
-template <bool K64, bool UNI>
+// Store shift of the lane's key wb + lane.  SH = 0: none (plain decode); 1: from the chunk's
+// window descriptors (built once per chunk, branch-free per window); 2: streamed (Ins), for
+// chunks whose insertions do not fit the descriptors (equal ranks, > 32 entries).
+template <bool K64, int SH>
 __device__ __forceinline__ void* shifted(void* outw, Ins& ins, uint32_t wb, uint32_t lane) {
-    if (!UNI) return outw;
-    return (uint8_t*)outw + (size_t)ins_shift<UNI>(ins, wb, lane) * (K64 ? 8 : 4);
+    if (SH == 0) return outw;
+    if (SH == 1) {
+        const uint2 d = ins.desc[(wb - ins.key0) >> 5];
+        return (uint8_t*)outw + (size_t)(d.y + __popc(d.x & lanemask_le())) * (K64 ? 8 : 4);
+    }
+    return (uint8_t*)outw + (size_t)ins_shift<true>(ins, wb, lane) * (K64 ? 8 : 4);
 }
 
 // Per-warp shared-memory page: [mbarrier | starts (kSegCap+4) | params kSegCap | words]
@@ -150,7 +158,7 @@ __device__ __forceinline__ void stage(Page& pg, const Sections& sec, uint32_t fr
 // segment and the offset d = i - s_j with no search.  key = base + t with
 // t = floor(slope d / 2^32) + u - bias = K[i] - base_j in [0, 2^32) (FORMAT F2 anchor, or the
 // F7 band floor with bias 0, plus the guard).
-template <bool K64, uint32_t B, bool CHECK, bool FULL, bool UNI>
+template <bool K64, uint32_t B, bool CHECK, bool FULL, int SH>
 __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uint32_t& jb,
                                               uint32_t& sb, uint32_t jlast, uint32_t wb,
                                               uint32_t w, uint32_t lane, uint32_t lmask,
@@ -168,7 +176,7 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
     const ulonglong2 pr = pg.sP[LC_BOUND(FULL || lane < valid, seg - pg.pj, pg.cp)];
     LC_CHECK(bits_of<B>(pg) && (FULL || lane < valid), w * bits_of<B>(pg) + lw + 1, pg.nw);
     const uint32_t t = pred_plus(pr.y, d, fld<B>(pg, w, lw, ls) - bias);
-    outw = shifted<K64, UNI>(outw, ins, wb, lane);
+    outw = shifted<K64, SH>(outw, ins, wb, lane);
     if (FULL || lane < valid) put<K64>(outw, pr.x, t);
     // candidates clamped at jlast + 1 repeat the list's final start N in the last chunk: cap
     // the advance there so jb stays a valid staged index
@@ -179,7 +187,7 @@ __device__ __forceinline__ void decode_window(Page& pg, const Sections& sec, uin
 // Two windows at once: keys [wb, wb + 64), lane handles wb + lane and wb + 32 + lane.  One
 // candidate load / vote serves both halves when fewer than 32 segment starts fall inside;
 // otherwise it falls back to two single windows.  w2 = pair index (windows 2 w2, 2 w2 + 1).
-template <bool K64, uint32_t B, bool CHECK, bool UNI>
+template <bool K64, uint32_t B, bool CHECK, int SH>
 __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w2, uint32_t lane, uint32_t lmask,
@@ -192,9 +200,9 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     const uint32_t x = pg.sS[LC_BOUND(true, cand - pg.pj, pg.cs)] - wb;
     const uint32_t inside = __ballot_sync(kFull, x < 64);
     if (inside == kFull) {  // >= 32 boundaries in 64 keys: not enough candidates, go window-wise
-        decode_window<K64, B, CHECK, true, UNI>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask,
+        decode_window<K64, B, CHECK, true, SH>(pg, sec, jb, sb, jlast, wb, 2 * w2, lane, lmask,
                                                 lw, ls, bias, outw, 32, ins);
-        decode_window<K64, B, CHECK, true, UNI>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
+        decode_window<K64, B, CHECK, true, SH>(pg, sec, jb, sb, jlast, wb + 32, 2 * w2 + 1, lane,
                                                 lmask, lw, ls, bias, (uint8_t*)outw + 32 * kw, 32,
                                                 ins);
         return;
@@ -214,8 +222,8 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
     LC_CHECK(bits_of<B>(pg), (2 * w2 + 1) * bits_of<B>(pg) + lw + 1, pg.nw);
     const uint32_t tA = pred_plus(pA.y, dA, fld<B>(pg, 2 * w2, lw, ls) - bias);
     const uint32_t tB = pred_plus(pB.y, dB, fld<B>(pg, 2 * w2 + 1, lw, ls) - bias);
-    put<K64>(shifted<K64, UNI>(outw, ins, wb, lane), pA.x, tA);
-    put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw, ins, wb + 32, lane), pB.x, tB);
+    put<K64>(shifted<K64, SH>(outw, ins, wb, lane), pA.x, tA);
+    put<K64>(shifted<K64, SH>((uint8_t*)outw + 32 * kw, ins, wb + 32, lane), pB.x, tB);
     jb = min(jb + adv, jlast + 1);  // see decode_window
     sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
 }
@@ -223,7 +231,7 @@ __device__ __forceinline__ void decode_pair(Page& pg, const Sections& sec, uint3
 // Four windows at once: keys [wb, wb + 128), lane handles wb + 32 q + lane (q = 0..3).  One
 // candidate load / advance vote serves four quarters when fewer than 32 segment starts fall
 // inside; otherwise two pair steps.  w4 = quad index (windows 4 w4 .. 4 w4 + 3).
-template <bool K64, uint32_t B, bool CHECK, bool UNI, bool FAST = false>
+template <bool K64, uint32_t B, bool CHECK, int SH, bool FAST = false>
 __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint32_t& jb,
                                             uint32_t& sb, uint32_t jlast, uint32_t wb,
                                             uint32_t w4, uint32_t lane, uint32_t lmask,
@@ -241,7 +249,7 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
             LC_CHECK(bits_of<B>(pg), (4 * w4 + q) * bits_of<B>(pg) + lw + 1, pg.nw);
-            put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
+            put<K64>(shifted<K64, SH>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
                      pred_plus(pr.y, d0 + 32 * q, fld<B>(pg, 4 * w4 + q, lw, ls) - bias));
         }
         jb = min(jb + __popc(__ballot_sync(kFull, x == 128)), jlast + 1);  // a start at wb + 128
@@ -249,9 +257,9 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         return;
     }
     if (inq == kFull) {  // >= 32 boundaries in 128 keys
-        decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls,
+        decode_pair<K64, B, CHECK, SH>(pg, sec, jb, sb, jlast, wb, 2 * w4, lane, lmask, lw, ls,
                                         bias, outw, ins);
-        decode_pair<K64, B, CHECK, UNI>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask,
+        decode_pair<K64, B, CHECK, SH>(pg, sec, jb, sb, jlast, wb + 64, 2 * w4 + 1, lane, lmask,
                                         lw, ls, bias, (uint8_t*)outw + 64 * kw, ins);
         return;
     }
@@ -264,13 +272,83 @@ __device__ __forceinline__ void decode_quad(Page& pg, const Sections& sec, uint3
         const uint32_t d = m ? lane - (31 - __clz(m)) : off + lane;
         const ulonglong2 pr = pg.sP[LC_BOUND(true, jq + __popc(m) - pg.pj, pg.cp)];
         LC_CHECK(bits_of<B>(pg), (4 * w4 + q) * bits_of<B>(pg) + lw + 1, pg.nw);
-        put<K64>(shifted<K64, UNI>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
+        put<K64>(shifted<K64, SH>((uint8_t*)outw + 32 * kw * q, ins, wb + 32 * q, lane), pr.x,
                  pred_plus(pr.y, d, fld<B>(pg, 4 * w4 + q, lw, ls) - bias));
         off = P ? __clz(P) + 1 : off + 32;
         jq += __popc(P);
     }
     jb = min(jb + adv, jlast + 1);  // see decode_window
     sb = pg.sS[LC_BOUND(true, jb - pg.pj, pg.cs)];
+}
+
+// One staged 1024-key chunk (or a ragged tail): quads when every segment is staged, paged
+// pairs for dense chunks, windows for the tail.  SH: the store shift (see shifted).
+template <bool K64, uint32_t B, bool SPARSE, int SH>
+__device__ __forceinline__ void decode_chunk(Page& pg, const Sections& sec, uint32_t j0,
+                                             uint32_t jlast, uint32_t key0, uint32_t nk,
+                                             uint32_t lane, uint32_t lmask, uint32_t lw,
+                                             uint32_t ls, uint32_t bias, uint8_t* outl, Ins& ins,
+                                             bool has_next, uint32_t nj0, uint32_t njl) {
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    uint32_t jb = j0;                                        // segment holding the window's first key
+    uint32_t sb = pg.sS[LC_BOUND(true, j0 - pg.pj, pg.cs)];  // its start
+    if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
+#pragma unroll 1
+        for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
+#pragma unroll
+            for (uint32_t k = 0; k < 2; ++k)
+                decode_quad<K64, B, false, SH, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k),
+                                                       g + k, lane, lmask, lw, ls, bias,
+                                                       outl + 128 * kw * k, ins);
+            if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
+                const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
+                const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
+                bulk_prefetch_l2(sec.starts + npj, ((ncs + 3) & ~3u) * 4);
+                bulk_prefetch_l2(sec.params + npj, min(kSegCap, njl + 1 - npj) * 16);
+            }
+        }
+    } else if (nk == 1024) {  // dense chunk: paged
+#pragma unroll 1
+        for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                decode_pair<K64, B, true, SH>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
+                                              lane, lmask, lw, ls, bias, outl + 64 * kw * k, ins);
+        }
+    } else {  // ragged tail chunk
+        for (uint32_t w = 0; 32 * w < nk; ++w)
+            decode_window<K64, B, true, false, SH>(pg, sec, jb, sb, jlast, key0 + 32 * w, w, lane,
+                                                   lmask, lw, ls, bias, outl + 32 * kw * w,
+                                                   nk - 32 * w, ins);
+    }
+}
+
+// lc_union's fused path: the chunk's window descriptors (ins.desc, 32 x {mask, shift}) from its
+// insertion entries [cur, end) (ins_begin / ins_ready loaded the first 32; v = rho - key0):
+// window w's mask has bit t for an entry at chunk offset 32 w + t, its shift counts the entries
+// before the chunk (cur) and in windows < w.  Returns false (use the streamed path) when the
+// chunk has more than 32 entries or two entries share a rank (popc would undercount).
+__device__ __forceinline__ bool ins_describe(Ins& s, uint32_t lane) {
+    const uint32_t n = s.end - s.cur;
+    if (n > 32) return false;
+    const bool has = lane < n;
+    const uint32_t prev = __shfl_up_sync(kFull, s.v, 1);
+    if (__ballot_sync(kFull, has && lane > 0 && prev == s.v)) return false;  // equal ranks
+    uint2* d = (uint2*)s.desc;
+    d[lane] = make_uint2(0, 0);
+    __syncwarp();
+    if (has) atomicOr(&d[s.v >> 5].x, 1u << (s.v & 31));
+    __syncwarp();
+    const uint32_t m = d[lane].x, c = __popc(m);
+    uint32_t inc = c;  // inclusive scan of the per-window counts
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+    }
+    d[lane].y = s.cur + inc - c;
+    __syncwarp();
+    return true;
 }
 
 // SPARSE: lists with fewer than one segment per 64 keys (config 4) read < 1 B per key: no L2
@@ -303,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     const Sections sec = a.sec;
     Ins ins;
     ins.rho = a.rho;
+    ins.desc = (const uint2*)(base + a.warp_bytes - 256);  // UNI kernels: 256 B per warp
 
     uint32_t c = blockIdx.x * kWarpsPerCta + warp;
     // hint pair of the warp's next chunk, loaded one chunk ahead (hides a DRAM round trip)
@@ -340,42 +419,17 @@ __global__ void __launch_bounds__(kThreads, 4)
             bulk_prefetch_l2(sec.words + (size_t)(h + nwarps) * 32 * B,
                              (uint32_t)min((uint64_t)(32 * B * 4 + 16),
                                        (a.nwords - (uint64_t)(h + nwarps) * 32 * B) * 4));
-        uint32_t jb = j0;                // segment holding the window's first key
-        uint32_t sb = pg.sS[LC_BOUND(true, j0 - pg.pj, pg.cs)];  // its start
         uint8_t* outl = (uint8_t*)a.out + ((size_t)(key0 - a.i0) + lane) * kw;  // lane's slot
-        if (nk == 1024 && jlast < pg.pj + pg.cp) {  // whole chunk staged: no re-page checks
-#pragma unroll 1
-            for (uint32_t g = 0; g < 8; g += 2, outl += 2 * 128 * kw) {
-#pragma unroll
-                for (uint32_t k = 0; k < 2; ++k)
-                    decode_quad<K64, B, false, UNI, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * (g + k),
-                                                    g + k, lane, lmask, lw, ls, a.bias,
-                                                    outl + 128 * kw * k, ins);
-                if (g == 2 && has_next && lane == 0) {  // next chunk's hint pair has landed:
-                    const uint32_t npj = nj0 & ~3u;     // its segment slices -> L2
-                    const uint32_t ncs = min(kSegCap + 4, njl + 2 - npj);
-                    bulk_prefetch_l2(sec.starts + npj, ((ncs + 3) & ~3u) * 4);
-                    bulk_prefetch_l2(sec.params + npj, min(kSegCap, njl + 1 - npj) * 16);
-                }
-            }
-        } else if (nk == 1024) {  // dense chunk: paged
-#pragma unroll 1
-            for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    decode_pair<K64, B, true, UNI>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k), g + k,
-                                                   lane, lmask, lw, ls, a.bias, outl + 64 * kw * k,
-                                                   ins);
-            }
-        } else {  // ragged tail chunk
-            for (uint32_t w = 0; 32 * w < nk; ++w)
-                decode_window<K64, B, true, false, UNI>(pg, sec, jb, sb, jlast, key0 + 32 * w, w,
-                                                        lane, lmask, lw, ls, a.bias,
-                                                        outl + 32 * kw * w, nk - 32 * w, ins);
+        const uint32_t nj0n = nj0, njln = njl;
+        if (UNI && !ins_describe(ins, lane)) {  // rare: equal ranks or > 32 entries: streamed
+            decode_chunk<K64, B, SPARSE, 2>(pg, sec, j0, jlast, key0, nk, lane, lmask, lw, ls,
+                                            a.bias, outl, ins, has_next, nj0n, njln);
+        } else {
+            decode_chunk<K64, B, SPARSE, UNI ? 1 : 0>(pg, sec, j0, jlast, key0, nk, lane, lmask, lw,
+                                                      ls, a.bias, outl, ins, has_next, nj0n, njln);
         }
     }
 }
-
 
 // ------------------------------------------------------------------------ batch decode
 // A batch of many lists (lc_batch_init: an inverted index's posting lists)
@@ -564,11 +618,11 @@ __global__ void __launch_bounds__(kThreads, 4)
             const uint32_t nq = nk >> 7;  // whole 128-key quads
 #pragma unroll 1
             for (uint32_t g = 0; g < nq; ++g, outl += 128 * kw)
-                decode_quad<K64, kRtB, false, false, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * g,
+                decode_quad<K64, kRtB, false, 0, SPARSE>(pg, sec, jb, sb, jlast, key0 + 128 * g,
                                                              g, lane, lmask, lw, ls, r.bias, outl,
                                                              ins);
             for (uint32_t w = 4 * nq; 32 * w < nk; ++w, outl += 32 * kw)
-                decode_window<K64, kRtB, false, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
+                decode_window<K64, kRtB, false, false, 0>(pg, sec, jb, sb, jlast, key0 + 32 * w,
                                                               w, lane, lmask, lw, ls, r.bias, outl,
                                                               nk - 32 * w, ins);
         } else if (nk == 1024) {  // dense chunk: paged
@@ -576,13 +630,13 @@ __global__ void __launch_bounds__(kThreads, 4)
             for (uint32_t g = 0; g < 16; g += 4, outl += 4 * 64 * kw) {
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
-                    decode_pair<K64, kRtB, true, false>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k),
+                    decode_pair<K64, kRtB, true, 0>(pg, sec, jb, sb, jlast, key0 + 64 * (g + k),
                                                         g + k, lane, lmask, lw, ls, r.bias,
                                                         outl + 64 * kw * k, ins);
             }
         } else {  // a dense partial chunk (a list's last)
             for (uint32_t w = 0; 32 * w < nk; ++w)
-                decode_window<K64, kRtB, true, false, false>(pg, sec, jb, sb, jlast, key0 + 32 * w,
+                decode_window<K64, kRtB, true, false, 0>(pg, sec, jb, sb, jlast, key0 + 32 * w,
                                                              w, lane, lmask, lw, ls, r.bias,
                                                              outl + 32 * kw * w, nk - 32 * w, ins);
         }

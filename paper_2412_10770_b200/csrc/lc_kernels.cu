@@ -89,7 +89,7 @@ int persistent_grid(int kind, bool k64, uint32_t b) {
     int& occ = g_grid.occ[kind][k64][b];
     if (occ == 0) {
         const void* fn = decode_kernel(kind, k64, b);
-        const int smem = (int)(warp_bytes_for(b) * kWarpsPerCta);
+        const int smem = (int)((warp_bytes_for(b) + (kind == 2 ? 256 : 0)) * kWarpsPerCta);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
         if (occ < 1) occ = 1;
@@ -112,7 +112,7 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     a.bias = bias_of(v);
     a.nwords = v->h.n_words;
     const uint32_t b = v->h.res_bits;
-    a.warp_bytes = warp_bytes_for(b);
+    a.warp_bytes = warp_bytes_for(b) + (coff ? 256 : 0);  // union: + the window descriptors
     const uint32_t smem = a.warp_bytes * kWarpsPerCta;
     const bool k64 = v->h.key_bits == 64;
     const bool sparse = v->h.n_seg * 64 < v->h.n;  // < 1 segment per 64 keys

@@ -17,10 +17,18 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("--unit", type=float, default=1.0, help="divide executions by this")
     ap.add_argument("--min", type=float, default=0.0, help="hide instructions below this")
+    ap.add_argument("--kernel", default=None, help="substring of the kernel name to select")
+    ap.add_argument("--skip", type=int, default=0, help="matching kernel blocks to skip")
     args = ap.parse_args()
-    out = subprocess.check_output(["ncu", "-i", args.rep, "--page", "source", "--csv",
-                                   "--print-source", "sass"], text=True)
+    cmd = ["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "sass"]
+    out = subprocess.check_output(cmd, text=True)
     rows = list(csv.reader(io.StringIO(out)))
+    # one block per kernel: a "Kernel Name" row, then the header and the SASS rows
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+    blocks = [(rows[i][1], rows[i:(starts[k + 1] if k + 1 < len(starts) else len(rows))])
+              for k, i in enumerate(starts)] or [("", rows)]
+    sel = [b for name, b in blocks if not args.kernel or args.kernel in name]
+    rows = sel[min(args.skip, len(sel) - 1)]
     hdr = next(r for r in rows if "Instructions Executed" in r)
     ie, st = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
     total = 0
