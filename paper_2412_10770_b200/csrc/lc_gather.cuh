@@ -147,13 +147,6 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
                  "r"(valid ? 16 : 0)
                  : "memory");
 }
-// the same with an L2 cache policy (the range ring's one-touch slices: evict_first, so the
-// L2-resident search structures of the first phase stay resident)
-__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(smem_addr(dst)),
-                 "l"(src), "r"(valid ? 16 : 0), "l"(pol)
-                 : "memory");
-}
 
 #ifndef LC_R64_SEGS
 #define LC_R64_SEGS 8
@@ -243,8 +236,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
             const uint4 ri = info[k];
             if (ri.y != kFull) {
                 const uint32_t v = kind == 0 ? ri.y : kind == 1 ? ((ri.y + 1) & ~3u) : ri.w;
-                cp16(ring + (k % kR64Slots) * RB + 16 * lane, src0 + (uint64_t)v * mul, v < lim,
-                     once);
+                cp16(ring + (k % kR64Slots) * RB + 16 * lane, src0 + (uint64_t)v * mul, v < lim);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
