@@ -58,6 +58,14 @@ typedef struct lc_header {
  * instead of the F2 anchor; params hold base = beta - eps and the decode bias is 0. */
 #define LC_FLAG_FREE_INTERCEPT 1u
 
+/* Encoder option of lc_encode_ex (not stored in blobs): the fewest segments on the format's
+ * integer lattice — the "optimal ... minimize the number of required line segments" of
+ * with the segment form of the other flags (F4 anchored, or F7 with
+ * LC_FLAG_FREE_INTERCEPT).  The greedy rules are maximal per segment but not always minimal in
+ * count on the lattice (L26); this option runs the greedy fit from every start and a
+ * shortest-cover DP (O(n * segment length) time, O(n) memory).  Decoding is unchanged. */
+#define LC_FLAG_MIN_SEGMENTS 2u
+
 /* A blob resident in device memory: a host copy of its header plus the device pointer.
  * d_blob must be 256-byte aligned (torch / cudaMalloc allocations are). */
 typedef struct lc_view {
@@ -100,8 +108,8 @@ int32_t lc_encode(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
 
 /* lc_encode with format flags: flags = LC_FLAG_FREE_INTERCEPT selects the FORMAT F7 encoder
  * (greedy maximal extension over all integer lines, the O'Rourke rule of PAPER.md:188 on the
- * format's lattice: fewer segments, same decode kernels), which needs eps <= 2^30 - 1.
- * flags = 0 is lc_encode.  Output ownership and errors as lc_encode; unknown flag bits or
+ * format's lattice: fewer segments, same decode kernels), which needs eps <= 2^30 - 1;
+ * LC_FLAG_MIN_SEGMENTS (combinable) the fewest-segments segmentation.  flags = 0 is lc_encode.  Output ownership and errors as lc_encode; unknown flag bits or
  * eps out of range give LC_ERR_ARG. */
 int32_t lc_encode_ex(const void* keys, uint64_t n, uint32_t key_bits, uint32_t eps,
                      uint32_t flags, void** blob, uint64_t* blob_bytes);

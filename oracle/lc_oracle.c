@@ -62,6 +62,42 @@ uint32_t oracle_width(uint64_t eps) {
  * Writes L segments into starts[0..L), base[0..L), slope[0..L) (caller sizes them n) and
  * returns L, or a negative status.
  */
+/* One F4 segment anchored at s over keys [s, n): the end e of the greedy extension and its
+ * slope (F5 or the P9 slope_mode).  Keys must be sorted (checked by the callers). */
+static uint64_t or_fit_f4(const uint64_t* K, uint64_t n, uint64_t s, uint64_t eps, uint32_t F,
+                          uint64_t gmax, const uint8_t* force_break, int slope_mode,
+                          uint64_t* slope) {
+    uint64_t b0 = K[s];
+    u128 lo = 0, hi = gmax;
+    uint64_t e = s + 1;
+    while (e < n) {
+        if (force_break && force_break[e]) break;
+        u128 d = e - s;
+        u128 D = (u128)(K[e] - b0); /* exact, D >= 1 */
+        /* l = ceil((D - eps) * 2^F / d), clipped at 0 when D <= eps */
+        u128 l = 0;
+        if (D > eps) {
+            u128 num = (D - eps) << F;
+            l = num / d + (num % d != 0);
+        }
+        /* h = floor(((D + eps + 1) * 2^F - 1) / d), then the overflow guard gmax / d */
+        u128 h = ((((D + eps + 1) << F) - 1) / d);
+        u128 g = (u128)gmax / d;
+        if (g < h) h = g;
+        u128 nlo = lo > l ? lo : l;
+        u128 nhi = hi < h ? hi : h;
+        if (nlo > nhi) break; /* F6: break at the first infeasible index */
+        lo = nlo;
+        hi = nhi;
+        e++;
+    }
+    if (e - s == 1) *slope = 0;
+    else if (slope_mode == 1) *slope = (uint64_t)lo;
+    else if (slope_mode == 2) *slope = (uint64_t)hi;
+    else *slope = (uint64_t)(lo + (hi - lo) / 2);
+    return e;
+}
+
 int64_t oracle_segment_ex(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t F,
                           uint64_t gmax, const uint8_t* force_break, int slope_mode,
                           uint64_t* starts, uint64_t* base, uint64_t* slope) {
@@ -72,37 +108,10 @@ int64_t oracle_segment_ex(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t 
     uint64_t L = 0;
     uint64_t s = 0;
     while (s < n) {
-        uint64_t b0 = K[s];
-        u128 lo = 0, hi = gmax;
-        uint64_t e = s + 1;
-        while (e < n) {
-            if (force_break && force_break[e]) break;
-            u128 d = e - s;
-            u128 D = (u128)(K[e] - b0); /* exact, D >= 1 */
-            /* l = ceil((D - eps) * 2^F / d), clipped at 0 when D <= eps */
-            u128 l = 0;
-            if (D > eps) {
-                u128 num = (D - eps) << F;
-                l = num / d + (num % d != 0);
-            }
-            /* h = floor(((D + eps + 1) * 2^F - 1) / d), then the overflow guard gmax / d */
-            u128 h = ((((D + eps + 1) << F) - 1) / d);
-            u128 g = (u128)gmax / d;
-            if (g < h) h = g;
-            u128 nlo = lo > l ? lo : l;
-            u128 nhi = hi < h ? hi : h;
-            if (nlo > nhi) break; /* F6: break at the first infeasible index */
-            lo = nlo;
-            hi = nhi;
-            e++;
-        }
         uint64_t sl;
-        if (e - s == 1) sl = 0;
-        else if (slope_mode == 1) sl = (uint64_t)lo;
-        else if (slope_mode == 2) sl = (uint64_t)hi;
-        else sl = (uint64_t)(lo + (hi - lo) / 2);
+        uint64_t e = or_fit_f4(K, n, s, eps, F, gmax, force_break, slope_mode, &sl);
         starts[L] = s;
-        base[L] = b0;
+        base[L] = K[s];
         slope[L] = sl;
         L++;
         s = e;
@@ -124,76 +133,160 @@ int64_t oracle_segment(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t F, 
  * purpose.  The chosen intercept is the feasible delta with the least |delta| (the negative
  * one on a tie), its slope the middle of its interval (F5); base = beta - eps (F7).
  * F / gmax as in oracle_segment_ex (reduced precision for the brute-force pins).
+ * Scratch (5 arrays of 2 eps + 1) is the caller's.
  */
+typedef __int128 or_i128;
+typedef struct {
+    or_i128 *lo, *hi, *nlo, *nhi;
+    uint8_t* alive;
+} or_free_scratch;
+
+static int or_free_alloc(or_free_scratch* w, uint64_t eps) {
+    const uint64_t m = 2 * eps + 1;
+    w->lo = malloc(m * sizeof(or_i128));
+    w->hi = malloc(m * sizeof(or_i128));
+    w->nlo = malloc(m * sizeof(or_i128));
+    w->nhi = malloc(m * sizeof(or_i128));
+    w->alive = malloc(m);
+    return w->lo && w->hi && w->nlo && w->nhi && w->alive;
+}
+
+static void or_free_release(or_free_scratch* w) {
+    free(w->lo); free(w->hi); free(w->nlo); free(w->nhi); free(w->alive);
+}
+
+/* one F7 segment from s over keys [s, n): its end, base (= beta - eps) and slope */
+static uint64_t or_fit_free(const uint64_t* K, uint64_t n, uint64_t s, uint64_t eps, uint32_t F,
+                            uint64_t gmax, or_free_scratch* w, uint64_t* base, uint64_t* slope) {
+    typedef or_i128 i128;
+    const uint64_t m = 2 * eps + 1; /* delta = t - eps, t in [0, m) */
+    i128 *lo = w->lo, *hi = w->hi, *nlo = w->nlo, *nhi = w->nhi;
+    uint8_t* alive = w->alive;
+    /* admissible intercepts: K[s] + delta - eps >= 0 */
+    const i128 dmin = K[s] >= 2 * eps ? -(i128)eps : (i128)eps - (i128)K[s];
+    for (uint64_t t = 0; t < m; t++) {
+        alive[t] = ((i128)t - (i128)eps) >= dmin;
+        lo[t] = 0;
+        hi[t] = gmax;
+    }
+    uint64_t e = s + 1;
+    while (e < n) {
+        const i128 d = (i128)(e - s);
+        int any = 0;
+        for (uint64_t t = 0; t < m; t++) {
+            if (!alive[t]) continue;
+            const i128 delta = (i128)t - (i128)eps;
+            const i128 Dp = (i128)(K[e] - K[s]) - delta; /* K[e] - beta */
+            /* S*d >= (Dp - eps) 2^F  and  S*d <= (Dp + eps + 1) 2^F - 1  and  S*d <= gmax */
+            i128 l = 0;
+            if (Dp > (i128)eps) {
+                const i128 num = (Dp - (i128)eps) << F;
+                l = num / d + (num % d != 0);
+            }
+            i128 h = ((((Dp + (i128)eps + 1) << F) - 1) / d); /* Dp + eps + 1 >= 2 */
+            if ((i128)gmax / d < h) h = (i128)gmax / d;
+            nlo[t] = lo[t] > l ? lo[t] : l;
+            nhi[t] = hi[t] < h ? hi[t] : h;
+            if (nlo[t] <= nhi[t]) any = 1;
+        }
+        if (!any) break; /* F6/F7: the first infeasible index ends the segment */
+        for (uint64_t t = 0; t < m; t++) {
+            if (!alive[t]) continue;
+            if (nlo[t] > nhi[t]) { alive[t] = 0; continue; }
+            lo[t] = nlo[t];
+            hi[t] = nhi[t];
+        }
+        e++;
+    }
+    /* least |delta|, negative first */
+    uint64_t pick = m;
+    for (uint64_t k = 0; k <= eps && pick == m; k++) {
+        if (alive[eps - k]) pick = eps - k;
+        else if (alive[eps + k]) pick = eps + k;
+    }
+    const i128 delta = (i128)pick - (i128)eps;
+    *base = (uint64_t)((i128)K[s] + delta - (i128)eps);
+    *slope = e - s == 1 ? 0 : (uint64_t)(lo[pick] + (hi[pick] - lo[pick]) / 2);
+    return e;
+}
+
 int64_t oracle_segment_free(const uint64_t* K, uint64_t n, uint64_t eps, uint32_t F,
                             uint64_t gmax, uint64_t* starts, uint64_t* base, uint64_t* slope) {
     if (n == 0) return OR_ERR_EMPTY;
     if (F > 32 || eps > 0x3fffffffULL) return OR_ERR_ARG;
     for (uint64_t i = 1; i < n; i++)
         if (K[i] <= K[i - 1]) return OR_ERR_UNSORTED;
-    typedef __int128 i128;
-    const uint64_t m = 2 * eps + 1; /* delta = t - eps, t in [0, m) */
-    i128* lo = malloc(m * sizeof(i128));
-    i128* hi = malloc(m * sizeof(i128));
-    i128* nlo = malloc(m * sizeof(i128));
-    i128* nhi = malloc(m * sizeof(i128));
-    uint8_t* alive = malloc(m);
-    if (!lo || !hi || !nlo || !nhi || !alive) {
-        free(lo); free(hi); free(nlo); free(nhi); free(alive);
+    or_free_scratch w;
+    if (!or_free_alloc(&w, eps)) {
+        or_free_release(&w);
         return OR_ERR_ALLOC;
     }
     uint64_t L = 0, s = 0;
     while (s < n) {
-        /* admissible intercepts: K[s] + delta - eps >= 0 */
-        const i128 dmin = K[s] >= 2 * eps ? -(i128)eps : (i128)eps - (i128)K[s];
-        for (uint64_t t = 0; t < m; t++) {
-            alive[t] = ((i128)t - (i128)eps) >= dmin;
-            lo[t] = 0;
-            hi[t] = gmax;
-        }
-        uint64_t e = s + 1;
-        while (e < n) {
-            const i128 d = (i128)(e - s);
-            int any = 0;
-            for (uint64_t t = 0; t < m; t++) {
-                if (!alive[t]) continue;
-                const i128 delta = (i128)t - (i128)eps;
-                const i128 Dp = (i128)(K[e] - K[s]) - delta; /* K[e] - beta */
-                /* S*d >= (Dp - eps) 2^F  and  S*d <= (Dp + eps + 1) 2^F - 1  and  S*d <= gmax */
-                i128 l = 0;
-                if (Dp > (i128)eps) {
-                    const i128 num = (Dp - (i128)eps) << F;
-                    l = num / d + (num % d != 0);
-                }
-                i128 h = ((((Dp + (i128)eps + 1) << F) - 1) / d); /* Dp + eps + 1 >= 2 */
-                if ((i128)gmax / d < h) h = (i128)gmax / d;
-                nlo[t] = lo[t] > l ? lo[t] : l;
-                nhi[t] = hi[t] < h ? hi[t] : h;
-                if (nlo[t] <= nhi[t]) any = 1;
-            }
-            if (!any) break; /* F6/F7: the first infeasible index ends the segment */
-            for (uint64_t t = 0; t < m; t++) {
-                if (!alive[t]) continue;
-                if (nlo[t] > nhi[t]) { alive[t] = 0; continue; }
-                lo[t] = nlo[t];
-                hi[t] = nhi[t];
-            }
-            e++;
-        }
-        /* least |delta|, negative first */
-        uint64_t pick = m;
-        for (uint64_t k = 0; k <= eps && pick == m; k++) {
-            if (alive[eps - k]) pick = eps - k;
-            else if (alive[eps + k]) pick = eps + k;
-        }
-        const i128 delta = (i128)pick - (i128)eps;
+        uint64_t b, sl;
+        const uint64_t e = or_fit_free(K, n, s, eps, F, gmax, &w, &b, &sl);
         starts[L] = s;
-        base[L] = (uint64_t)((i128)K[s] + delta - (i128)eps);
-        slope[L] = e - s == 1 ? 0 : (uint64_t)(lo[pick] + (hi[pick] - lo[pick]) / 2);
+        base[L] = b;
+        slope[L] = sl;
         L++;
         s = e;
     }
-    free(lo); free(hi); free(nlo); free(nhi); free(alive);
+    or_free_release(&w);
+    return (int64_t)L;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Fewest segments (NEXT-3: "optimal online eps-PLA ... to minimize the number of required line
+ * segments") on the format's integer lattice, where the greedy rules above are
+ * maximal per segment but not always minimal in count (reading L26: a suffix of a feasible
+ * integer segment need not be feasible).  Written as the definition: a segment [s, e) is
+ * feasible iff e <= emax(s), the end of the greedy fit from s (a prefix of a feasible segment is
+ * feasible with the same line), so the fewest segments covering [s, n) are
+ *   f(n) = 0,  f(s) = 1 + min { f(e) : s < e <= emax(s) },
+ * taking the LARGEST minimising e (deterministic tie-break, the product's too); every chosen
+ * [s, e) is then refitted on exactly its keys with the same rule (F4 anchor / F7 free intercept,
+ * F5 middle slope).  Plain O(n * segment length) loops; free != 0 selects F7.
+ */
+int64_t oracle_segment_min(const uint64_t* K, uint64_t n, uint64_t eps, int free_icpt,
+                           uint32_t F, uint64_t gmax, uint64_t* starts, uint64_t* base,
+                           uint64_t* slope) {
+    if (n == 0) return OR_ERR_EMPTY;
+    if (F > 32 || (free_icpt && eps > 0x3fffffffULL)) return OR_ERR_ARG;
+    for (uint64_t i = 1; i < n; i++)
+        if (K[i] <= K[i - 1]) return OR_ERR_UNSORTED;
+    uint64_t* emax = malloc(n * 8);
+    uint64_t* f = malloc((n + 1) * 8);
+    uint64_t* nxt = malloc(n * 8);
+    or_free_scratch w = {0, 0, 0, 0, 0};
+    if (!emax || !f || !nxt || (free_icpt && !or_free_alloc(&w, eps))) {
+        free(emax); free(f); free(nxt); or_free_release(&w);
+        return OR_ERR_ALLOC;
+    }
+    for (uint64_t s = 0; s < n; s++) {
+        uint64_t b, sl;
+        emax[s] = free_icpt ? or_fit_free(K, n, s, eps, F, gmax, &w, &b, &sl)
+                            : or_fit_f4(K, n, s, eps, F, gmax, 0, 0, &sl);
+    }
+    f[n] = 0;
+    for (uint64_t s = n; s-- > 0;) {
+        uint64_t best = UINT64_MAX, arg = s + 1;
+        for (uint64_t e = s + 1; e <= emax[s]; e++)
+            if (f[e] <= best) { best = f[e]; arg = e; } /* <=: the largest e among the minima */
+        f[s] = best + 1;
+        nxt[s] = arg;
+    }
+    uint64_t L = 0;
+    for (uint64_t s = 0; s < n; s = nxt[s]) {
+        const uint64_t e = nxt[s];
+        uint64_t b = K[s], sl;
+        if (free_icpt) or_fit_free(K, e, s, eps, F, gmax, &w, &b, &sl);
+        else or_fit_f4(K, e, s, eps, F, gmax, 0, 0, &sl);
+        starts[L] = s;
+        base[L] = b;
+        slope[L] = sl;
+        L++;
+    }
+    free(emax); free(f); free(nxt); or_free_release(&w);
     return (int64_t)L;
 }
 
@@ -274,10 +367,14 @@ static int32_t or_encode(const uint64_t* K, uint64_t n, uint32_t key_bits, uint6
 
     uint64_t* st = malloc(n * 8), *ba = malloc(n * 8), *sl = malloc(n * 8);
     if (!st || !ba || !sl) { free(st); free(ba); free(sl); return OR_ERR_ALLOC; }
-    int64_t L = (flags & 1u)
+    int64_t L = (flags & 2u)   /* fewest segments (encoder option, not stored in the header) */
+                    ? oracle_segment_min(K, n, eps, (int)(flags & 1u), 32, 0x7fffffffffffffffULL,
+                                         st, ba, sl)
+                : (flags & 1u)
                     ? oracle_segment_free(K, n, eps, 32, 0x7fffffffffffffffULL, st, ba, sl)
                     : oracle_segment_ex(K, n, eps, 32, 0x7fffffffffffffffULL, force_break,
                                         slope_mode, st, ba, sl);
+    flags &= 1u; /* the header records the format (F7 bit) only */
     if (L < 0) { free(st); free(ba); free(sl); return (int32_t)L; }
 
     or_hdr h;
@@ -361,6 +458,12 @@ int32_t oracle_encode(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t
 int32_t oracle_encode_free(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
                            uint8_t** blob, uint64_t* blob_bytes) {
     return or_encode(K, n, key_bits, eps, 1, 0, 0, blob, blob_bytes);
+}
+
+/* fewest segments (oracle_segment_min): free != 0 for F7 blobs */
+int32_t oracle_encode_min(const uint64_t* K, uint64_t n, uint32_t key_bits, uint64_t eps,
+                          int32_t free_icpt, uint8_t** blob, uint64_t* blob_bytes) {
+    return or_encode(K, n, key_bits, eps, 2u | (free_icpt ? 1u : 0u), 0, 0, blob, blob_bytes);
 }
 
 void oracle_free(void* p) { free(p); }

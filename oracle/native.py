@@ -46,6 +46,10 @@ def lib():
         L.oracle_segment_free.restype = i64
         L.oracle_encode_free.argtypes = [p, u64, u32, u64, C.POINTER(p), C.POINTER(u64)]
         L.oracle_encode_free.restype = i32
+        L.oracle_segment_min.argtypes = [p, u64, u64, C.c_int, u32, u64, p, p, p]
+        L.oracle_segment_min.restype = i64
+        L.oracle_encode_min.argtypes = [p, u64, u32, u64, i32, C.POINTER(p), C.POINTER(u64)]
+        L.oracle_encode_min.restype = i32
         L.oracle_free.argtypes = [p]
         L.oracle_free.restype = None
         L.oracle_decode.argtypes = [p, u64, p]
@@ -111,8 +115,23 @@ def segment_free(keys, eps: int, F: int = 32, gmax: int = GMAX):
     return st[:L].copy(), ba[:L].copy(), sl[:L].copy()
 
 
+def segment_min(keys, eps: int, free: bool = False, F: int = 32, gmax: int = GMAX):
+    """Fewest segments (oracle_segment_min: DP over the greedy ends emax(s), F4 or F7 fits).
+    Returns (starts, base, slope) u64 arrays."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    n = k.size
+    st = np.empty(max(n, 1), np.uint64)
+    ba = np.empty(max(n, 1), np.uint64)
+    sl = np.empty(max(n, 1), np.uint64)
+    L = lib().oracle_segment_min(_ptr(k), n, eps, 1 if free else 0, F, gmax, _ptr(st), _ptr(ba),
+                                 _ptr(sl))
+    if L < 0:
+        raise OracleError(L, "segment_min")
+    return st[:L].copy(), ba[:L].copy(), sl[:L].copy()
+
+
 def encode(keys, eps: int, key_bits: int | None = None, force_break=None,
-           slope_mode: int = 0, free: bool = False) -> bytes:
+           slope_mode: int = 0, free: bool = False, min_segments: bool = False) -> bytes:
     """LCG1 blob of `keys`: anchored (FORMAT F1-F6) or, with free=True, free-intercept (F7)."""
     arr = np.asarray(keys)
     if key_bits is None:
@@ -121,7 +140,12 @@ def encode(keys, eps: int, key_bits: int | None = None, force_break=None,
     fb = None if force_break is None else np.ascontiguousarray(force_break, dtype=np.uint8)
     out = C.c_void_p()
     nb = C.c_uint64()
-    if free:
+    if min_segments:
+        if fb is not None or slope_mode:
+            raise ValueError("force_break / slope_mode apply to the greedy anchored encoder only")
+        st = lib().oracle_encode_min(_ptr(k) if k.size else None, k.size, key_bits, eps,
+                                     1 if free else 0, C.byref(out), C.byref(nb))
+    elif free:
         if fb is not None or slope_mode:
             raise ValueError("force_break / slope_mode apply to the anchored encoder only")
         st = lib().oracle_encode_free(_ptr(k) if k.size else None, k.size, key_bits, eps,

@@ -434,14 +434,49 @@ int32_t encode_t(const K* keys, uint64_t n, uint32_t key_bits, uint32_t eps, uin
     params.reserve(n / 4 + 32);
     const bool free_base = flags & LC_FLAG_FREE_INTERCEPT;
     FreeFit ff(eps);
-    for (uint64_t s = 0; s < n;) {
-        uint64_t slope, base = (uint64_t)keys[s];
-        const uint64_t e = free_base ? ff.fit(keys, n, s, &base, &slope)
-                                     : fit_segment(keys, n, s, eps, &slope);
-        starts.push_back((uint32_t)s);
-        params.push_back(base);
-        params.push_back(slope);
-        s = e;
+    if (flags & LC_FLAG_MIN_SEGMENTS) {
+        // Fewest segments on the lattice (NEXT-3): [s, e) is feasible iff
+        // e <= emax(s), the greedy end from s (a prefix keeps its line), so
+        // f(s) = 1 + min{f(e) : s < e <= emax(s)}, f(n) = 0, the largest minimising e on a
+        // tie; each chosen [s, e) is refitted on exactly its keys.  O(n * segment length).
+        std::vector<uint32_t> f(n + 1), nxt(n);
+        std::vector<uint32_t> emax(n);
+        for (uint64_t s = 0; s < n; ++s) {
+            uint64_t slope, base;
+            emax[s] = (uint32_t)(free_base ? ff.fit(keys, n, s, &base, &slope)
+                                           : fit_segment(keys, n, s, eps, &slope));
+        }
+        f[n] = 0;
+        for (uint64_t s = n; s-- > 0;) {
+            uint32_t best = 0xffffffffu, arg = (uint32_t)s + 1;
+            for (uint64_t e = s + 1; e <= emax[s]; ++e)
+                if (f[e] <= best) {
+                    best = f[e];
+                    arg = (uint32_t)e;
+                }
+            f[s] = best + 1;
+            nxt[s] = arg;
+        }
+        for (uint64_t s = 0; s < n; s = nxt[s]) {
+            const uint64_t e = nxt[s];
+            uint64_t slope, base = (uint64_t)keys[s];
+            if (free_base) ff.fit(keys, e, s, &base, &slope);
+            else fit_segment(keys, e, s, eps, &slope);
+            starts.push_back((uint32_t)s);
+            params.push_back(base);
+            params.push_back(slope);
+        }
+        flags &= ~(uint32_t)LC_FLAG_MIN_SEGMENTS;  // an encoder option, not a format flag
+    } else {
+        for (uint64_t s = 0; s < n;) {
+            uint64_t slope, base = (uint64_t)keys[s];
+            const uint64_t e = free_base ? ff.fit(keys, n, s, &base, &slope)
+                                         : fit_segment(keys, n, s, eps, &slope);
+            starts.push_back((uint32_t)s);
+            params.push_back(base);
+            params.push_back(slope);
+            s = e;
+        }
     }
     const uint64_t bias = free_base ? 0 : eps;  // FORMAT F3 decode bias c
     const uint64_t L = starts.size();
@@ -555,7 +590,7 @@ int32_t lc_encode_ex(const void* keys, uint64_t n, uint32_t key_bits, uint32_t e
                      uint32_t flags, void** blob, uint64_t* blob_bytes) {
     if (!blob || !blob_bytes) return LC_ERR_ARG;
     if (key_bits != 32 && key_bits != 64) return LC_ERR_ARG;
-    if (flags & ~(uint32_t)LC_FLAG_FREE_INTERCEPT) return LC_ERR_ARG;
+    if (flags & ~(uint32_t)(LC_FLAG_FREE_INTERCEPT | LC_FLAG_MIN_SEGMENTS)) return LC_ERR_ARG;
     if (eps > ((flags & LC_FLAG_FREE_INTERCEPT) ? kEpsMaxFree : 0x7fffffffu)) return LC_ERR_ARG;
     if (n == 0) return LC_ERR_EMPTY;
     if (!keys) return LC_ERR_ARG;

@@ -24,6 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 LC_OK, LC_ERR_ARG, LC_ERR_EMPTY, LC_ERR_UNSORTED = 0, -1, -2, -3
 LC_ERR_TOO_LARGE, LC_ERR_FORMAT, LC_ERR_ALLOC, LC_ERR_CUDA = -4, -5, -6, -7
 LC_FLAG_FREE_INTERCEPT = 1  # FORMAT F7
+LC_FLAG_MIN_SEGMENTS = 2    # encoder option: fewest segments (not stored in the blob)
 
 
 class lc_header(C.Structure):
@@ -168,9 +169,11 @@ def launch_count() -> int:
 
 
 # ---------------------------------------------------------------------------- host side
-def encode(keys: np.ndarray, eps: int, key_bits: int | None = None, free: bool = False) -> bytes:
+def encode(keys: np.ndarray, eps: int, key_bits: int | None = None, free: bool = False,
+           min_segments: bool = False) -> bytes:
     """lc_encode / lc_encode_ex: host blob of sorted keys (uint32 or uint64 numpy array);
-    anchored greedy (FORMAT F1-F6) or, with free=True, the free-intercept encoder (F7)."""
+    anchored greedy (FORMAT F1-F6) or, with free=True, the free-intercept encoder (F7);
+    min_segments=True: the fewest segments of that form (LC_FLAG_MIN_SEGMENTS)."""
     k = np.asarray(keys)
     if key_bits is None:
         key_bits = 32 if k.dtype == np.uint32 else 64
@@ -180,7 +183,9 @@ def encode(keys: np.ndarray, eps: int, key_bits: int | None = None, free: bool =
     k = np.ascontiguousarray(k, dtype=np.uint32 if key_bits == 32 else np.uint64)
     out, nb = C.c_void_p(), C.c_uint64()
     _check(_lib.lc_encode_ex(k.ctypes.data if k.size else None, k.size, key_bits, eps,
-                             LC_FLAG_FREE_INTERCEPT if free else 0, C.byref(out), C.byref(nb)),
+                             (LC_FLAG_FREE_INTERCEPT if free else 0)
+                             | (LC_FLAG_MIN_SEGMENTS if min_segments else 0),
+                             C.byref(out), C.byref(nb)),
            "lc_encode_ex")
     try:
         return C.string_at(out.value, nb.value)

@@ -210,3 +210,30 @@ def test_free_intersect_union(lc, free_a, free_b):
     wu = setops.union(a, b)
     assert int(uc.item()) == wu.size
     assert np.array_equal(_host(uo[:wu.size], a.dtype), wu)
+
+
+# ------------------------------------------------ fewest segments (LC_FLAG_MIN_SEGMENTS)
+@pytest.mark.parametrize("seed", range(1200, 1240))
+def test_min_segments_decode_fuzz(lc, seed):
+    """Blobs of the fewest-segments option (segments shorter than the greedy ones at places)
+    through every kernel family: decode, access, range."""
+    keys, eps, kb, _ = fuzz_case(seed)
+    for free in (False, True):
+        if free and eps > EPS_MAX_FREE:
+            continue
+        blob = lc.encode(keys, eps, key_bits=kb, free=free, min_segments=True)
+        assert _decode_equal(lc, blob, keys)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 5])
+def test_min_segments_configs(lc, cid):
+    keys = make_keys(cid, 400_001)
+    for free in (False, True):
+        blob = lc.encode(keys, CONFIGS[cid].eps, free=free, min_segments=True)
+        v = lc.View(blob, device=DEV)
+        out = lc.decode(v)
+        idx = np.random.default_rng(cid).integers(0, keys.size, 20_000).astype(np.uint64)
+        got = lc.access(v, _dev(idx))
+        torch.cuda.synchronize()
+        assert torch.equal(out, _dev(keys))
+        assert np.array_equal(_host(got, keys.dtype), keys[idx.astype(np.int64)])
