@@ -337,7 +337,7 @@ int32_t lc_decode_batch(const lc_batch* b, void* d_out, uint32_t* d_work, lc_str
  * lc_setop_batch_plan sizes one query batch on the host (O(pairs)): h_n[k] is list k's key
  * count (m entries, as given to lc_batch_init), h_pairs the 2 P list indices.  The device calls
  * then take the same pairs in device memory (d_pairs); other pairs give unspecified results but
- * never write outside d_scratch / d_out (a pair index >= m is clamped and flagged).
+ * never write outside d_scratch / d_out (a pair index >= m is clamped to m - 1).
  * Results: pair p's keys at d_out[d_out_off[p] .. d_out_off[p] + d_counts[p]) (device arrays of
  * P + 1 and P uint64; AND results are packed, OR results sit at capacity offsets
  * sum_{q < p} (n_s + n_l)).  d_scratch: >= plan->scratch_bytes (256-byte aligned); d_out:

@@ -177,3 +177,16 @@ def test_setop_batch_fuzz_u64_free(lc, seed):
         blobs.append(lc.encode(keys, e, free=bool(k % 2)))
     pairs = rng.integers(0, len(lists), (200, 2))
     _setop_check(lc, lists, blobs, pairs)
+
+
+@pytest.mark.gpu
+def test_batch_edges(lc):
+    """One-list batches, lists of exactly 1024 k keys (no partial chunk), exactly 64 and 65 keys
+    (the small-unit bound), and an empty query batch."""
+    for lists in ([make_keys(1, 4096)], [make_keys(1, 64), make_keys(1, 65), make_keys(1, 1024),
+                                         make_keys(1, 2048 + 64), make_keys(1, 1)]):
+        blobs = [lc.encode(k, 63) for k in lists]
+        _check_batch(lc, lists, blobs)
+    bt = lc.Batch([lc.encode(make_keys(1, 100), 63)], device=DEV)
+    r = lc.intersect_batch(bt, np.zeros((0, 2), np.int64))
+    assert r.plan.n_pairs == 0
