@@ -484,10 +484,6 @@ struct BatchArgs {
 // list.
 constexpr uint32_t kSmallUnit = 64;
 constexpr uint32_t kSmallItem = 256;  // flat small keys per work item (8 per lane)
-#ifndef LC_SMALL_ILP
-#define LC_SMALL_ILP 2
-#endif
-constexpr uint32_t kSmallIlp = LC_SMALL_ILP;  // keys per lane in flight (divides 8)
 
 __device__ __forceinline__ BatchChunk load_chunk(const BatchChunk* p) {
     BatchChunk r;
@@ -555,57 +551,30 @@ __global__ void __launch_bounds__(kThreads, 4)
             if (nitem >= ngroups && nitem < items) load_big(nitem, nr, nout);
             item = nitem;
             uint32_t u = __ldg(a.sblk + (f0 >> 5));
-            // kSmallIlp keys per lane in flight: their dependent load chains (unit, record,
-            // segment, params + words) are interleaved
 #pragma unroll 1
-            for (uint32_t q0 = 0; q0 < kSmallItem / 32; q0 += kSmallIlp) {
-                uint32_t f[kSmallIlp], uu[kSmallIlp];
-                bool live[kSmallIlp];
-#pragma unroll
-                for (uint32_t x = 0; x < kSmallIlp; ++x) {
-                    f[x] = f0 + 32 * (q0 + x) + lane;
-                    live[x] = f[x] < a.small_keys;
-                    if (live[x])
-                        while (__ldg(a.sk0 + u + 1) <= f[x]) ++u;  // the unit holding flat key f
-                    uu[x] = u;
+            for (uint32_t q = 0; q < kSmallItem / 32; ++q) {
+                const uint32_t f = f0 + 32 * q + lane;
+                if (f >= a.small_keys) break;
+                while (__ldg(a.sk0 + u + 1) <= f) ++u;  // the unit holding flat key f
+                const BatchChunk r = load_chunk(a.chunks + big + u);
+                const uint32_t k = f - __ldg(a.sk0 + u), i = r.key0 + k;
+                const uint8_t* blob = (const uint8_t*)r.blob;
+                const uint32_t* S = (const uint32_t*)(blob + 256);
+                uint32_t j = r.j0;
+                while (j < r.jlast && __ldg(S + j + 1) <= i) ++j;  // its segment (few)
+                const ulonglong2 pr = __ldg((const ulonglong2*)(blob + r.off_params) + j);
+                const uint32_t b = r.nk_b >> 16;
+                uint32_t uf = 0;
+                if (b) {
+                    const uint64_t bit = (uint64_t)i * b;
+                    const uint32_t* wp = (const uint32_t*)(blob + r.off_words) + (bit >> 5);
+                    uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) &
+                         (b >= 32 ? kFull : (1u << b) - 1);
                 }
-                BatchChunk r[kSmallIlp];
-                uint32_t k[kSmallIlp];
-#pragma unroll
-                for (uint32_t x = 0; x < kSmallIlp; ++x)
-                    if (live[x]) {
-                        r[x] = load_chunk(a.chunks + big + uu[x]);
-                        k[x] = f[x] - __ldg(a.sk0 + uu[x]);
-                    }
-                uint32_t j[kSmallIlp], s0[kSmallIlp];
-#pragma unroll
-                for (uint32_t x = 0; x < kSmallIlp; ++x)
-                    if (live[x]) {
-                        const uint32_t* S = (const uint32_t*)(r[x].blob + 256);
-                        const uint32_t i = r[x].key0 + k[x];
-                        j[x] = r[x].j0;
-                        while (j[x] < r[x].jlast && __ldg(S + j[x] + 1) <= i) ++j[x];  // few
-                        s0[x] = __ldg(S + j[x]);
-                    }
-#pragma unroll
-                for (uint32_t x = 0; x < kSmallIlp; ++x) {
-                    if (!live[x]) continue;
-                    const uint8_t* blob = (const uint8_t*)r[x].blob;
-                    const uint32_t i = r[x].key0 + k[x];
-                    const ulonglong2 pr = __ldg((const ulonglong2*)(blob + r[x].off_params) + j[x]);
-                    const uint32_t b = r[x].nk_b >> 16;
-                    uint32_t uf = 0;
-                    if (b) {
-                        const uint64_t bit = (uint64_t)i * b;
-                        const uint32_t* wp = (const uint32_t*)(blob + r[x].off_words) + (bit >> 5);
-                        uf = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (uint32_t)bit & 31) &
-                             (b >= 32 ? kFull : (1u << b) - 1);
-                    }
-                    const uint32_t t = pred_plus(pr.y, i - s0[x], uf - r[x].bias);
-                    uint8_t* o = (uint8_t*)a.out + (r[x].out + k[x]) * kw;
-                    if (K64) __stcs((unsigned long long*)o, (unsigned long long)(pr.x + t));
-                    else __stcs((unsigned int*)o, (unsigned int)pr.x + t);
-                }
+                const uint32_t t = pred_plus(pr.y, i - __ldg(S + j), uf - r.bias);
+                uint8_t* o = (uint8_t*)a.out + (r.out + k) * kw;
+                if (K64) __stcs((unsigned long long*)o, (unsigned long long)(pr.x + t));
+                else __stcs((unsigned int*)o, (unsigned int)pr.x + t);
             }
             continue;
         }
