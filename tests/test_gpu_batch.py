@@ -184,7 +184,7 @@ def test_batch_edges(lc):
     """One-list batches, lists of exactly 1024 k keys (no partial chunk), exactly 64 and 65 keys
     (the small-unit bound), and an empty query batch."""
     for lists in ([make_keys(1, 4096)], [make_keys(1, 64), make_keys(1, 65), make_keys(1, 1024),
-                                         make_keys(1, 2048 + 64), make_keys(1, 1)]):
+                                         make_keys(1, 2048 + 64), np.array([5], np.uint32)]):
         blobs = [lc.encode(k, 63) for k in lists]
         _check_batch(lc, lists, blobs)
     bt = lc.Batch([lc.encode(make_keys(1, 100), 63)], device=DEV)
