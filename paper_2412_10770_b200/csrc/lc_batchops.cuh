@@ -163,12 +163,39 @@ __global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
 // OR: every long key to its union slot
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
+    // A warp's 32 consecutive long keys usually belong to one pair and have the same rank in
+    // its short list (short lists are ~100x shorter): the first and last live lanes search the
+    // whole short list, the others only between those two ranks (usually an empty interval).
+    const uint32_t lane = threadIdx.x & 31;
     const uint64_t gl = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-    if (gl >= a.Lt) return;
-    const uint32_t p = pair_of(a.blk_l, a.l_off, gl);
-    const uint64_t y = key_at<K64>(a.keys_l, gl);
-    const uint64_t s0 = __ldg(a.s_off + p), ns = __ldg(a.s_off + p + 1) - s0;
-    const uint64_t ra = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
+    const bool live = gl < a.Lt;
+    const uint32_t lv = __ballot_sync(kFull, live);
+    if (!lv) return;
+    const uint32_t first = __ffs(lv) - 1, last = 31 - __clz(lv);
+    const uint32_t p = live ? pair_of(a.blk_l, a.l_off, gl) : 0;
+    const uint64_t y = live ? key_at<K64>(a.keys_l, gl) : 0;
+    const uint64_t s0 = live ? __ldg(a.s_off + p) : 0;
+    const uint64_t ns = live ? __ldg(a.s_off + p + 1) - s0 : 0;
+    const uint32_t p0 = __shfl_sync(kFull, p, first);
+    uint64_t ra;
+    if (__all_sync(kFull, !live || p == p0)) {  // one pair: bracket by the end lanes' ranks
+        uint64_t r = 0;
+        if (lane == first || lane == last) r = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
+        const uint64_t r0 = __shfl_sync(kFull, r, first), r1 = __shfl_sync(kFull, r, last);
+        ra = r0;
+        if (r0 != r1 && live) {  // ranks in [r0, r1]: search that sub-range only
+            uint64_t l = r0, h = r1;
+            while (l < h) {
+                const uint64_t mid = (l + h) >> 1;
+                if (key_at<K64>(a.keys_s, s0 + mid) < y) l = mid + 1;
+                else h = mid;
+            }
+            ra = l;
+        }
+    } else {
+        ra = live ? lower_bound_keys<K64>(a.keys_s, s0, ns, y) : 0;
+    }
+    if (!live) return;
     const uint64_t pos = __ldg(a.cap_off + p) + (gl - __ldg(a.l_off + p)) + ra -
                          (matches_before(a, s0 + ra) - matches_before(a, s0));
     if (K64) ((uint64_t*)a.out)[pos] = y;
