@@ -162,44 +162,59 @@ __global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
 
 // OR: every long key to its union slot
 template <bool K64>
+constexpr uint32_t kWlKeys = 256;  // long keys per warp in lc_bwrite_l_kernel (8 per lane)
 __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
-    // A warp's 32 consecutive long keys usually belong to one pair and have the same rank in
-    // its short list (short lists are ~100x shorter): the first and last live lanes search the
-    // whole short list, the others only between those two ranks (usually an empty interval).
+    // A warp places 256 consecutive long keys.  They usually belong to one pair and share one
+    // rank in its (much shorter) short list: the ranks of the range's first and last keys are
+    // searched once per warp, and a key only searches when they differ (between them).
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t gl = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-    const bool live = gl < a.Lt;
-    const uint32_t lv = __ballot_sync(kFull, live);
-    if (!lv) return;
-    const uint32_t first = __ffs(lv) - 1, last = 31 - __clz(lv);
-    const uint32_t p = live ? pair_of(a.blk_l, a.l_off, gl) : 0;
-    const uint64_t y = live ? key_at<K64>(a.keys_l, gl) : 0;
-    const uint64_t s0 = live ? __ldg(a.s_off + p) : 0;
-    const uint64_t ns = live ? __ldg(a.s_off + p + 1) - s0 : 0;
-    const uint32_t p0 = __shfl_sync(kFull, p, first);
-    uint64_t ra;
-    if (__all_sync(kFull, !live || p == p0)) {  // one pair: bracket by the end lanes' ranks
+    const uint64_t g0 = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kWlKeys;
+    if (g0 >= a.Lt) return;
+    const uint64_t g1 = min(g0 + kWlKeys, a.Lt) - 1;  // last key of the warp's range
+    const uint32_t pa = pair_of(a.blk_l, a.l_off, g0), pb = pair_of(a.blk_l, a.l_off, g1);
+    if (pa == pb) {
+        const uint64_t s0 = __ldg(a.s_off + pa), ns = __ldg(a.s_off + pa + 1) - s0;
         uint64_t r = 0;
-        if (lane == first || lane == last) r = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
-        const uint64_t r0 = __shfl_sync(kFull, r, first), r1 = __shfl_sync(kFull, r, last);
-        ra = r0;
-        if (r0 != r1 && live) {  // ranks in [r0, r1]: search that sub-range only
-            uint64_t l = r0, h = r1;
-            while (l < h) {
-                const uint64_t mid = (l + h) >> 1;
-                if (key_at<K64>(a.keys_s, s0 + mid) < y) l = mid + 1;
-                else h = mid;
+        if (lane < 2) r = lower_bound_keys<K64>(a.keys_s, s0, ns, key_at<K64>(a.keys_l, lane ? g1 : g0));
+        const uint64_t r0 = __shfl_sync(kFull, r, 0), r1 = __shfl_sync(kFull, r, 1);
+        const uint64_t m0 = matches_before(a, s0);
+        const uint64_t base = __ldg(a.cap_off + pa) - __ldg(a.l_off + pa) - m0;  // + gl + ra - M(s0 + ra)
+        const uint64_t c0 = base + r0 - matches_before(a, s0 + r0);
+#pragma unroll 4
+        for (uint32_t q = 0; q < kWlKeys / 32; ++q) {
+            const uint64_t gl = g0 + 32 * q + lane;
+            if (gl > g1) break;
+            const uint64_t y = key_at<K64>(a.keys_l, gl);
+            uint64_t pos;
+            if (r0 == r1) {
+                pos = c0 + gl;
+            } else {  // a short key falls inside the range: rank between r0 and r1
+                uint64_t l = r0, h = r1;
+                while (l < h) {
+                    const uint64_t mid = (l + h) >> 1;
+                    if (key_at<K64>(a.keys_s, s0 + mid) < y) l = mid + 1;
+                    else h = mid;
+                }
+                pos = base + gl + l - matches_before(a, s0 + l);
             }
-            ra = l;
+            if (K64) ((uint64_t*)a.out)[pos] = y;
+            else ((uint32_t*)a.out)[pos] = (uint32_t)y;
         }
-    } else {
-        ra = live ? lower_bound_keys<K64>(a.keys_s, s0, ns, y) : 0;
+        return;
     }
-    if (!live) return;
-    const uint64_t pos = __ldg(a.cap_off + p) + (gl - __ldg(a.l_off + p)) + ra -
-                         (matches_before(a, s0 + ra) - matches_before(a, s0));
-    if (K64) ((uint64_t*)a.out)[pos] = y;
-    else ((uint32_t*)a.out)[pos] = (uint32_t)y;
+    // the range spans pairs: every key on its own
+    for (uint32_t q = 0; q < kWlKeys / 32; ++q) {
+        const uint64_t gl = g0 + 32 * q + lane;
+        if (gl > g1) break;
+        const uint32_t p = pair_of(a.blk_l, a.l_off, gl);
+        const uint64_t y = key_at<K64>(a.keys_l, gl);
+        const uint64_t s0 = __ldg(a.s_off + p), ns = __ldg(a.s_off + p + 1) - s0;
+        const uint64_t ra = lower_bound_keys<K64>(a.keys_s, s0, ns, y);
+        const uint64_t pos = __ldg(a.cap_off + p) + (gl - __ldg(a.l_off + p)) + ra -
+                             (matches_before(a, s0 + ra) - matches_before(a, s0));
+        if (K64) ((uint64_t*)a.out)[pos] = y;
+        else ((uint32_t*)a.out)[pos] = (uint32_t)y;
+    }
 }
 
 // per pair: result offset and size

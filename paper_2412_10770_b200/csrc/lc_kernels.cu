@@ -937,7 +937,7 @@ int32_t setop_batch(const lc_batch* bt, const lc_setop_plan* q, const uint32_t* 
     else OR ? lc_bwrite_s_kernel<false, true><<<gs, 256, 0, st>>>(a) : lc_bwrite_s_kernel<false, false><<<gs, 256, 0, st>>>(a);
     uint32_t nl = 5;
     if (OR && q->long_keys) {
-        const unsigned gl = (unsigned)((q->long_keys + 255) / 256);
+        const unsigned gl = (unsigned)((q->long_keys + 8 * kWlKeys - 1) / (8 * kWlKeys));
         if (k64) lc_bwrite_l_kernel<true><<<gl, 256, 0, st>>>(a);
         else lc_bwrite_l_kernel<false><<<gl, 256, 0, st>>>(a);
         ++nl;
