@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
 }
 
 // OR: every long key to its union slot
-template <bool K64>
 constexpr uint32_t kWlKeys = 256;  // long keys per warp in lc_bwrite_l_kernel (8 per lane)
+template <bool K64>
 __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
     // A warp places 256 consecutive long keys.  They usually belong to one pair and share one
     // rank in its (much shorter) short list: the ranks of the range's first and last keys are
