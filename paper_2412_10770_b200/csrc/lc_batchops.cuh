@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
         if (lane < 2) r = lower_bound_keys<K64>(a.keys_s, s0, ns, key_at<K64>(a.keys_l, lane ? g1 : g0));
         const uint64_t r0 = __shfl_sync(kFull, r, 0), r1 = __shfl_sync(kFull, r, 1);
         const uint64_t m0 = matches_before(a, s0);
-        const uint64_t base = __ldg(a.cap_off + pa) - __ldg(a.l_off + pa) - m0;  // + gl + ra - M(s0 + ra)
+        const uint64_t base = __ldg(a.cap_off + pa) - __ldg(a.l_off + pa) + m0;  // + gl + ra - M(s0 + ra)
         const uint64_t c0 = base + r0 - matches_before(a, s0 + r0);
 #pragma unroll 4
         for (uint32_t q = 0; q < kWlKeys / 32; ++q) {
