@@ -451,15 +451,24 @@ def _access_block(dev, stream, reps, no_cpu):
         v5.build_access_layout(stream=stream, out=lay)
         lay_ev[1].record(stream)
         a_out.zero_()
+        r_out.zero_()
         _, pal = _time_launches(lambda: lc.access(v5, d_idx, a_out, stream=stream), stream, reps, 2)
+        # 64-key ranges through the layout: boundary masks from the directory, one contiguous
+        # gather of the record span (lc_range64_dir_kernel)
+        _, prl = _time_launches(lambda: lc.range_decode(v5, d_rs, 64, r_out, stream=stream),
+                                stream, reps, 2)
     torch.cuda.synchronize()
     d5 = torch.from_numpy(k5.view(np.int64)).to(dev)
     if not torch.equal(a_out, d5[d_idx]):
         raise SystemExit("access (layout) mismatch")
-    del d5
+    sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
+    if not torch.equal(r_out, d5[sel]):
+        raise SystemExit("range (layout) mismatch")
+    del d5, sel
     layout = {"bytes": v5.access_layout_bytes(), "build_ms": lay_ev[0].elapsed_time(lay_ev[1]),
               "lookups_per_s": idx.size / statistics.mean(pal),
-              "ns_per_lookup": statistics.mean(pal) / idx.size * 1e9}
+              "ns_per_lookup": statistics.mean(pal) / idx.size * 1e9,
+              "ranges_per_s": rs.size / statistics.mean(prl)}
     # NEXT-1 quantiles and NEXT-2 successor search / intersection / union on the same list
     qrng = np.random.default_rng(55)
     mq = 10_000_000
@@ -536,9 +545,10 @@ def _access_block(dev, stream, reps, no_cpu):
         "ns_per_lookup": statistics.mean(pal) / idx.size * 1e9,
         "lookups_per_s_no_layout": idx.size / statistics.mean(pa),
         "access_layout": layout,
-        "ranges_per_s": rs.size / statistics.mean(pr),
-        "range_keys_per_s": rs.size * 64 / statistics.mean(pr),
-        "range_out_GBps": rs.size * 64 * 8 / statistics.mean(pr) / 1e9,
+        "ranges_per_s": rs.size / statistics.mean(prl),
+        "range_keys_per_s": rs.size * 64 / statistics.mean(prl),
+        "range_out_GBps": rs.size * 64 * 8 / statistics.mean(prl) / 1e9,
+        "ranges_per_s_no_layout": rs.size / statistics.mean(pr),
         "quantiles_exact_per_s": mq / statistics.mean(pqe),
         "quantiles_approx_per_s": mq / statistics.mean(pqa),
         "quantiles_exact_per_s_no_layout": mq / statistics.mean(pqe0),

@@ -395,6 +395,216 @@ __global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, u
     }
 }
 
+// ------------------------------------------ range decode, len == 64, through the access layout
+// With the access layout attached a 64-key range needs no search, no starts and ONE contiguous
+// gather.  The directory bitmaps of its (at most three) 32-key groups, shifted to the range's
+// first key, ARE the window boundary masks the ring kernel votes for (PA: starts among keys
+// rk + 1 .. rk + 31, PB: among rk + 32 .. rk + 63), and the records of consecutive segments are
+// contiguous, so the range's data is the params unit of its first segment jk plus the span
+//   [A, E],  A = 2 jk + 1 + floor(rk b / 128)  (the unit holding key rk's residual in record jk),
+//            E = 2 je + 1 + floor(((rk + 64) b - 1) / 128)  (je: segment of key rk + 63),
+// which holds every later segment's params and all 64 residual fields.  Phase 1 (lane = range):
+// hint and directory loads (L2-resident, evict_last); masks, span and addresses parked in shared
+// memory.  Phase 2: the warp walks its 32 ranges through a ring of slots; lane 0 copies the
+// params unit, lane g >= 1 span unit g - 1 (one 16-byte cp.async each) while an earlier range
+// is decoded from its slot with popc / clz on the parked masks (no votes).  A range whose span
+// exceeds 31 units goes through L2.
+#ifndef LC_RD_SLOTS
+#define LC_RD_SLOTS 8
+#endif
+// ring depth (ranges gathered ahead - 1): 8 slots at 4 CTAs per SM beat 4 slots at 7 CTAs (1.43
+// vs 1.65 ms per 1e7 ranges on config 5): more copies in flight per warp
+constexpr uint32_t kRdSlots = LC_RD_SLOTS;
+static_assert((kRdSlots & (kRdSlots - 1)) == 0, "slot index is k % kRdSlots");
+#ifndef LC_RD_UNITS
+#define LC_RD_UNITS 32
+#endif
+constexpr uint32_t kRdUnits = LC_RD_UNITS;  // copy lanes: unit 0 first params, 1..kRdUnits-1 the span
+static_assert(kRdUnits <= 32, "one 16-byte copy per lane");
+constexpr uint32_t kRdSlotBytes = 16 * (kRdUnits + 1);  // + 1 pad unit (a field's second word)
+constexpr uint32_t kRdInfoBytes = 48;       // per range: 3 x uint4, see phase 1
+constexpr uint32_t kRdInvalid = 1u << 31, kRdSlow = 1u << 30;  // flags beside the span units
+__host__ __device__ constexpr uint32_t rd_smem_per_warp() {
+    return kRdSlots * kRdSlotBytes + 32 * kRdInfoBytes;
+}
+__device__ __forceinline__ void cp16s(uint32_t dst_s, uint64_t src) {  // shared-space address
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_s), "l"(src) : "memory");
+}
+__device__ __forceinline__ uint32_t sel_nz(uint32_t c, uint32_t a, uint32_t b) {  // c ? a : b
+    uint32_t r;
+    asm("{\n.reg .pred p;\nsetp.ne.u32 p, %1, 0;\nselp.u32 %0, %2, %3, p;\n}"
+        : "=r"(r)
+        : "r"(c), "r"(a), "r"(b));
+    return r;
+}
+
+template <bool K64>
+__global__ void __launch_bounds__(256) lc_range64_dir_kernel(const RangeArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t kw = K64 ? 8 : 4;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
+    if (r0 >= a.q) return;  // warp-uniform
+    const Sections sec = a.sec;
+    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
+    uint8_t* ring = smem + warp * rd_smem_per_warp();
+    uint4* info = (uint4*)(ring + kRdSlots * kRdSlotBytes);
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+
+    // ---- phase 1: lane = range.  Parked per range (3 x uint4):
+    //   [0] {rk, rk - s_jk, PA, PB}
+    //   [1] {address of span unit A (lo, hi), span units | flags, 16 x (A - unit of jk's params)}
+    //   [2] {jk, s_jk, -, -}  (the through-L2 path)
+    {
+        uint32_t rk = 0, jk = 0, sk = 0, PA = 0, PB = 0, units = kRdInvalid, back = 0;
+        uint64_t A = (uint64_t)(uintptr_t)sec.acc;  // ranges without copies: lane 0 reads unit 0
+        if (r0 + lane < a.q) {
+            const uint64_t s64 = __ldg(a.start + r0 + lane);
+            if (s64 <= a.n && 64 <= a.n - s64) {
+                rk = (uint32_t)s64;
+                const uint32_t e = rk + 63, g0 = rk >> 5, r5 = rk & 31;
+                const uint32_t hA = ldh(sec.hint + (rk >> 10), keep);
+                const uint32_t hB = ldh(sec.hint + (e >> 10), keep);
+                const uint2 d0 = ldh(sec.dir + g0, keep);
+                const uint2 d1 = ldh(sec.dir + g0 + 1, keep);
+                const uint2 d2 = ldh(sec.dir + (e >> 5), keep);  // group g0 + 2, or g0 + 1 again
+                const uint32_t m = d0.x & ((2u << r5) - 1);
+                jk = hA + (d0.y & 2047) + __popc(m);
+                if (m) sk = (rk & ~31u) + (31 - __clz(m));
+                else if ((d0.y >> 11) != kDistNone) sk = (rk & ~31u) - (d0.y >> 11);
+                else sk = ldh(sec.starts + jk, keep);  // a segment longer than 2^21 keys
+                PA = __funnelshift_r(d0.x, d1.x, r5) & ~1u;  // bit t: key rk + t starts a segment
+                PB = __funnelshift_r(d1.x, d2.x, r5);
+                // a start exactly at a block's first key is not in the bitmaps (the hint names
+                // it): the block's first group has dist 0 then
+                const uint32_t tb = 1024 - (rk & 1023);
+                if (tb < 64 && ((((r5 + tb) >> 5) == 1 ? d1.y : d2.y) >> 11) == 0) {
+                    if (tb < 32) PA |= 1u << tb;
+                    else PB |= 1u << (tb - 32);
+                }
+                const uint32_t je = jk + __popc(PA) + __popc(PB);
+                LC_CHECK(true, je, L);
+                (void)hB;
+                const uint64_t ur = ((uint64_t)rk * b) >> 7;
+                const uint32_t r0b = (rk * b) & 127;
+                // units in [A, E]: 2 (je - jk) + floor((r0b + 64 b - 1) / 128) + 1 (b = 0: 2 (je - jk))
+                const uint32_t span = 2 * (je - jk) + (uint32_t)(((int32_t)(r0b + 64 * b) - 1) >> 7) + 1;
+                if (span < kRdUnits) {
+                    units = span;
+                    A = (uint64_t)(uintptr_t)(sec.acc + 2 * (uint64_t)jk + 1 + ur);
+                    back = 16 * (1 + (uint32_t)(ur - (((uint64_t)sk * b) >> 7)));
+                } else {
+                    units = kRdSlow;
+                }
+            } else if (a.err) {
+                atomicOr(a.err, 1u);
+            }
+        }
+        // PA's bit 0 is free (a start at rk itself is part of jk): set = not the ring path
+        info[3 * lane] = make_uint4(rk, rk - sk, PA | (units >= kRdSlow ? 1u : 0u), PB);
+        info[3 * lane + 1] = make_uint4((uint32_t)A, (uint32_t)(A >> 32), units, back);
+        info[3 * lane + 2] = make_uint4(jk, sk, 0, 0);
+    }
+    __syncwarp();
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.q - r0);
+
+    // lane 0 copies the params unit of jk, lane g >= 1 span unit g - 1, into slot unit `lane`.
+    // Shared memory is addressed in the shared window (32-bit) throughout the walk.
+    const uint32_t ring_s = smem_addr(ring), info_s = ring_s + kRdSlots * kRdSlotBytes;
+    const uint32_t dst_lane = ring_s + 16 * lane;
+    const int32_t fwd = 16 * ((int32_t)lane - 1);
+    auto lds4 = [](uint32_t addr) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(addr));
+        return v;
+    };
+    auto lds1 = [](uint32_t addr) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+        return v;
+    };
+    auto issue = [&](uint32_t k) {
+        if (k < nr) {
+            const uint4 q1 = lds4(info_s + 48 * k + 16);
+            if (lane <= (q1.z & 63)) {
+                const int32_t off = lane ? fwd : -(int32_t)q1.w;
+                cp16s(dst_lane + (k % kRdSlots) * kRdSlotBytes,
+                      (((uint64_t)q1.y << 32) | q1.x) + (int64_t)off);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
+    };
+    for (uint32_t k = 0; k + 1 < kRdSlots; ++k) issue(k);
+    uint8_t* outk = (uint8_t*)a.out + ((size_t)r0 * 64 + lane) * kw;  // lane's slot, range 0
+    const uint32_t lmask = lanemask_le();
+    const uint32_t tbA = lane * b, tbB = tbA + 32 * b;  // bit offsets of the lane's two keys
+    const bool pow2 = (b & (b - 1)) == 0;               // b in {0, 1, 2, 4, 8, 16, 32}
+
+    for (uint32_t k = 0; k < nr; ++k, outk += 64 * kw) {
+        // range k's copies (and those of k + 1, k + 2) are in flight: wait for k's; the warp
+        // sync also orders every lane's reads of slot k - 1 before it is refilled just below
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRdSlots - 2) : "memory");
+        __syncwarp();
+        issue(k + kRdSlots - 1);
+        const uint4 q0 = lds4(info_s + 48 * k);
+        const uint32_t rk = q0.x;
+        if (!(q0.z & 1)) {
+            const uint32_t slot = ring_s + (k % kRdSlots) * kRdSlotBytes;
+            const uint32_t off0 = q0.y, PA = q0.z, PB = q0.w;
+            const uint32_t r0b = (rk * b) & 127;
+            const uint32_t offB = PA ? __clz(PA) + 1 : off0 + 32;  // uniform
+            const uint32_t mA = PA & lmask, mB = PB & lmask;
+            const uint32_t djA = __popc(mA), djB = __popc(PA) + __popc(mB);
+            const uint32_t dA = sel_nz(mA, (uint32_t)__clz(mA) - 31, off0) + lane;
+            const uint32_t dB = sel_nz(mB, (uint32_t)__clz(mB) - 31, offB) + lane;
+            // params: slot unit 0 for jk, else 2 dj + floor((r0b + (s - rk) b) / 128)
+            const uint32_t puA = sel_nz(djA, 2 * djA + ((r0b + (lane - dA) * b) >> 7), 0);
+            const uint32_t puB = sel_nz(djB, 2 * djB + ((r0b + (32 + lane - dB) * b) >> 7), 0);
+            LC_CHECK(true, puB, kRdUnits);
+            const uint4 pA = lds4(slot + 16 * puA), pB = lds4(slot + 16 * puB);
+            const uint32_t wbA = r0b + tbA, wbB = r0b + tbB;
+            const uint32_t wA = slot + 16 + 32 * djA + ((wbA >> 3) & ~3u);
+            const uint32_t wB = slot + 16 + 32 * djB + ((wbB >> 3) & ~3u);
+            LC_CHECK(true, 4 + 8 * djB + (wbB >> 5) + 1, kRdSlotBytes / 4);
+            uint32_t uA, uB;
+            if (pow2) {  // widths dividing 32 never straddle a word (warp-uniform)
+                uA = (lds1(wA) >> (wbA & 31)) & mask;
+                uB = (lds1(wB) >> (wbB & 31)) & mask;
+            } else {
+                uA = __funnelshift_r(lds1(wA), lds1(wA + 4), wbA & 31) & mask;
+                uB = __funnelshift_r(lds1(wB), lds1(wB + 4), wbB & 31) & mask;
+            }
+            put<K64>(outk, ((uint64_t)pA.y << 32) | pA.x,
+                     pred_plus(((uint64_t)pA.w << 32) | pA.z, dA, uA - bias));
+            put<K64>(outk + 32 * kw, ((uint64_t)pB.y << 32) | pB.x,
+                     pred_plus(((uint64_t)pB.w << 32) | pB.z, dB, uB - bias));
+        } else if (lds1(info_s + 48 * k + 24) & kRdInvalid) {
+            put<K64>(outk, 0, 0);
+            put<K64>(outk + 32 * kw, 0, 0);
+        } else {  // two 32-key windows through L2
+            const uint4 q2 = info[3 * k + 2];
+            uint32_t jb = q2.x, sbw = q2.y;
+            for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
+                const uint32_t wb = rk + w0;
+                const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
+                const uint32_t Pm = __reduce_or_sync(kFull, bit_or_zero(xw));
+                const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
+                const uint32_t m = Pm & lmask;
+                const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
+                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
+                const uint32_t u =
+                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
+                jb += adv;
+                sbw = ldh(sec.starts + min(jb, L), keep);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Q queries per thread through the access layout: all loads of one step are issued for the Q
 // queries before any is consumed.
 template <bool K64, int MODE, int Q>

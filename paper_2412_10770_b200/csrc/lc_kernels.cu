@@ -431,6 +431,16 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
+    if (len == 64 && v->d_acc) {  // access layout attached: no search, one contiguous gather
+        const uint32_t smem = 8 * rd_smem_per_warp();
+        const void* fn = k64 ? (const void*)lc_range64_dir_kernel<true>
+                             : (const void*)lc_range64_dir_kernel<false>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (k64) lc_range64_dir_kernel<true><<<(unsigned)grid, 256, smem, st>>>(a);
+        else lc_range64_dir_kernel<false><<<(unsigned)grid, 256, smem, st>>>(a);
+        lc_detail::count_launch(1);
+        return cuda_status();
+    }
     if (len == 64) {  // the config-5 shape: cp.async ring kernel
         const uint32_t smem = 8 * r64_smem_per_warp(a.b);
         const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;

@@ -101,7 +101,7 @@ def _check_blob(lc, blob, keys, rng, m=20_000, layout_bytes=True):
     bad = np.array([n, n + 5, 1 << 40], np.uint64)  # out of range: 0 and the error bit
     ab = lc.access(v, _dev(bad), err=err)
     rgs = {}
-    for ln in (1, 33, 64, 100):  # range decodes with the layout attached (unaffected by it)
+    for ln in (1, 33, 64, 100):  # range decodes with the layout attached (64 keys: lc_range64_dir_kernel)
         if n >= ln:
             st = rng.integers(0, n - ln, 700, endpoint=True).astype(np.uint64)
             rgs[ln] = (st, lc.range_decode(v, _dev(st), ln))
@@ -185,3 +185,29 @@ def test_layout_full_config5(lc):
     qi = torch.clamp(ranks * keys.size // (1 << 20), max=keys.size - 1)
     torch.cuda.synchronize()
     assert torch.equal(q, d_keys[qi])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("eps", [0, 3, 1000])
+def test_layout_long_segments(lc, eps):
+    """Segments longer than 2^21 keys (the directory's dist field saturates, kDistNone): lookups
+    and 64-key ranges deep inside them, around their ends, and across a dense stretch."""
+    rng = np.random.default_rng(77 + eps)
+    ap1 = np.arange(5_000_000, dtype=np.uint64) * np.uint64(7) + np.uint64(3)
+    mid = ap1[-1] + np.cumsum(rng.integers(1, 1 << 20, 3000)).astype(np.uint64)
+    ap2 = mid[-1] + np.uint64(1) + np.arange(2_500_000, dtype=np.uint64) * np.uint64(2)
+    keys = np.concatenate([ap1, mid, ap2])
+    blob = lc.encode(keys, eps)
+    assert lc.header(blob).n_seg < keys.size // 1000
+    v = lc.View(blob, device=DEV)
+    v.build_access_layout()
+    n = keys.size
+    edges = np.array([0, 1, (1 << 21) - 70, (1 << 21) - 1, 1 << 21, (1 << 22) + 5, ap1.size - 64,
+                      ap1.size - 63, ap1.size - 1, ap1.size, ap1.size + mid.size - 10,
+                      ap1.size + mid.size, n - 64], np.uint64)
+    st = np.concatenate([edges, rng.integers(0, n - 64, 4000, endpoint=True).astype(np.uint64)])
+    rg = lc.range_decode(v, _dev(st), 64)
+    a = lc.access(v, _dev(st))
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(rg, np.uint64).reshape(-1, 64), keys[st.astype(np.int64)[:, None] + np.arange(64)])
+    assert np.array_equal(_host(a, np.uint64), keys[st.astype(np.int64)])

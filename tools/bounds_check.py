@@ -104,6 +104,14 @@ def main():
         gi, gk = lc.next_geq(view, d(x))
         wi, wk = setops.next_geq(keys, x)
         check(f"next_geq {law}", np.array_equal(h(gi, np.uint64), wi) and np.array_equal(h(gk, keys.dtype), wk))
+        # the same lookups and 64-key ranges through the access layout (directory + records)
+        view.build_access_layout()
+        check(f"access-layout {law}", np.array_equal(h(lc.access(view, d(idx)), keys.dtype), keys[idx.astype(np.int64)]))
+        if keys.size >= 64:
+            st = np.concatenate([rng.integers(0, keys.size - 64, 500, endpoint=True),
+                                 [0, keys.size - 64]]).astype(np.uint64)
+            want, _ = orc.range_decode(blob, st, 64)
+            check(f"range64-layout {law}", np.array_equal(h(lc.range_decode(view, d(st), 64), keys.dtype), want))
     a = np.unique(np.concatenate([k5[::3], rng.integers(0, int(k5[-1]), 5000, dtype=np.uint64)]))
     va, vb = lc.View(lc.encode(a, 31), device=dev), lc.View(lc.encode(k5, 127), device=dev)
     out, cnt = lc.intersect(va, vb)

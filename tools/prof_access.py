@@ -70,6 +70,11 @@ def main():
         assert torch.equal(out, d_keys[d_idx])
         res["layout_ms"] = ms
         res["layout_lookups_per_s"] = idx.size / ms * 1e3
+        res["layout_range64_ms"] = timeit(lambda: lc.range_decode(v, d_rs, 64, r_out), args.reps)
+        sel = (d_rs[:, None] + torch.arange(64, device=dev)[None, :]).reshape(-1)
+        assert torch.equal(r_out, d_keys[sel])
+        del sel
+        res["layout_ranges_per_s"] = rs.size / res["layout_range64_ms"] * 1e3
         ranks = d_idx[:10_000_000]
         qo = torch.empty(ranks.numel(), dtype=torch.int64, device=dev)
         res["quantile_exact_layout_ms_1e7"] = timeit(

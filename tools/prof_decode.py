@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--access", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="experiment builds (LC_LIB)")
+    ap.add_argument("--cache", default=None, help="directory to keep keys + blob between runs (A/B)")
     args = ap.parse_args()
     import torch
 
@@ -32,9 +33,18 @@ def main():
     t0 = time.time()
     if args.access:
         keys, idx, rs = make_queries(n=args.n)
+        blob = lc.encode(keys, spec.eps)
     else:
-        keys = make_keys(args.config, args.n)
-    blob = lc.encode(keys, spec.eps)
+        ck = args.cache and os.path.join(args.cache, f"lc_c{args.config}_{args.n}.npy")
+        if ck and os.path.exists(ck) and os.path.exists(ck + ".blob"):
+            keys = np.load(ck)
+            blob = open(ck + ".blob", "rb").read()
+        else:
+            keys = make_keys(args.config, args.n)
+            blob = lc.encode(keys, spec.eps)
+            if ck:
+                np.save(ck, keys)
+                open(ck + ".blob", "wb").write(blob)
     print(f"gen+encode {time.time() - t0:.1f}s n={keys.size} blob={len(blob)}", flush=True)
     view = lc.View(blob)
     out = view.out_tensor(keys.size)
