@@ -355,10 +355,11 @@ __device__ __forceinline__ bool ins_describe(Ins& s, uint32_t lane) {
 // prefetch of the next chunk (A/B: it costs config 4 +1.4% time) and the per-quad
 // single-segment fast path (config 4 -2.3%; it costs dense lists, so dense kernels omit it).
 // UNI: lc_union's fused path (stores shifted by Ins; dense settings).
-// All: 4 CTAs / <= 64 registers per SM.  A/B on B200 against the former 5 CTAs / 48 registers
-// (dense) and 6 / 40 (sparse): bench config 2 5370 -> 5430 GB/s (three alternating pairs),
-// config 5 -1.4% time, config 3 flat, config 4 5530 -> 5562 GB/s; the union's shifted decode
-// spilled at 48 (0.367 -> 0.358 ms).
+// All: <= 64 registers (4 CTAs per SM fit).  A/B on B200 against the former 5 CTAs / 48
+// registers (dense) and 6 / 40 (sparse): bench config 2 5370 -> 5430 GB/s (three alternating
+// pairs), config 5 -1.4% time, config 3 flat, config 4 5530 -> 5562 GB/s; the union's shifted
+// decode spilled at 48 (0.367 -> 0.358 ms).  The persistent grid is smaller than what fits:
+// see persistent_grid (2 CTAs per SM for sparse lists, 3 for dense ones).
 template <bool K64, uint32_t B, bool SPARSE, bool UNI = false>
 __global__ void __launch_bounds__(kThreads, 4)
     lc_decode_kernel(const DecodeArgs a) {

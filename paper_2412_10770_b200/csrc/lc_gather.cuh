@@ -410,11 +410,20 @@ __global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, u
 // is decoded from its slot with popc / clz on the parked masks (no votes).  A range whose span
 // exceeds 31 units goes through L2.
 #ifndef LC_RD_SLOTS
-#define LC_RD_SLOTS 8
+#define LC_RD_SLOTS 4
 #endif
-// ring depth (ranges gathered ahead - 1): 8 slots at 4 CTAs per SM beat 4 slots at 7 CTAs (1.43
-// vs 1.65 ms per 1e7 ranges on config 5): more copies in flight per warp
+// Ring depth (ranges gathered ahead + 1) and the shared-memory carve-out (kRdCarveout, set by
+// the launcher).  What decides this kernel's speed is how much of the SM's 256 KB stays L1 (the
+// in-flight gathers and stores live there): with the driver's default carve-out (228 KB as soon
+// as the resident CTAs need > 196 KB) 4 slots / 7 CTAs per SM take 1.65 ms per 1e7 ranges and
+// 8 slots / 4 CTAs 1.76 ms; capped at 164 KB (5 CTAs, 92 KB of L1) 4 slots take 1.40 ms, 8 slots
+// (3 CTAs) 1.40 ms, 2 slots 1.61 ms; at 196 KB 1.41 / 1.43 ms; at 132 KB 1.44 / 1.67 ms.
 constexpr uint32_t kRdSlots = LC_RD_SLOTS;
+constexpr int kRdCarveout = 71;  // percent of 228 KB: the 164 KB configuration
+#ifndef LC_RD_WARPS
+#define LC_RD_WARPS 8
+#endif
+constexpr uint32_t kRdWarps = LC_RD_WARPS;  // warps per CTA (2 / 4 / 16 measured slower)
 static_assert((kRdSlots & (kRdSlots - 1)) == 0, "slot index is k % kRdSlots");
 #ifndef LC_RD_UNITS
 #define LC_RD_UNITS 32
@@ -439,11 +448,11 @@ __device__ __forceinline__ uint32_t sel_nz(uint32_t c, uint32_t a, uint32_t b) {
 }
 
 template <bool K64>
-__global__ void __launch_bounds__(256) lc_range64_dir_kernel(const RangeArgs a) {
+__global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t kw = K64 ? 8 : 4;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t r0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * kRdWarps + warp) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
     const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;

@@ -22,7 +22,9 @@
 //  * Batches: one launch for many lists (chunk records + a work queue; short lists' keys one
 //    thread each), batched AND / OR over list pairs (lc_batchops.cuh).
 //  * Range decode: one warp per 32 ranges (lane-parallel search); len == 64 gathers each
-//    range's slices through a per-warp cp.async ring and decodes from shared memory.
+//    range's slices through a per-warp cp.async ring and decodes from shared memory; with the
+//    access layout the boundary masks come from the directory bitmaps and a range is one
+//    contiguous gather of its record span (no search, no starts).
 //  * Successor search / intersection: binary search over the segments' first keys (the
 //    anchored bases, or decoded first keys for F7 blobs: segments as skip pointers), then
 //    inside one segment.
@@ -93,6 +95,15 @@ int persistent_grid(int kind, bool k64, uint32_t b) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
         if (occ < 1) occ = 1;
+        // Fewer resident warps than fit: the decode is bound by the HBM read / write mix, and
+        // that mix runs faster with fewer concurrent chunk streams.  Measured on B200 (ms per
+        // launch at 16 / 24 / 32 warps per SM = 2 / 3 / 4 CTAs): config 4 (sparse) 0.724 /
+        // 0.797 / 0.802 (also -9.5% / -12% at N = 5e7 / 2e8), config 2 0.200 / 0.207 / 0.211,
+        // config 5 0.200 / 0.199 / 0.205, config 3 0.421 / 0.377 / 0.382 (its tail of 1-key
+        // segments is paged chunk by chunk: a latency chain that needs the warps), the union's
+        // shifted decode 0.368 / 0.341 / 0.353 (whole union).  12 warps per SM: 0.81 (config 4).
+        const int want = kind == 1 ? 2 : 3;
+        if (occ > want) occ = want;
     }
     return occ * g_grid.sms;
 }
@@ -432,12 +443,14 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
     if (len == 64 && v->d_acc) {  // access layout attached: no search, one contiguous gather
-        const uint32_t smem = 8 * rd_smem_per_warp();
+        const uint32_t smem = kRdWarps * rd_smem_per_warp();
+        const uint64_t grid = (q + 32 * kRdWarps - 1) / (32 * kRdWarps);
         const void* fn = k64 ? (const void*)lc_range64_dir_kernel<true>
                              : (const void*)lc_range64_dir_kernel<false>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (k64) lc_range64_dir_kernel<true><<<(unsigned)grid, 256, smem, st>>>(a);
-        else lc_range64_dir_kernel<false><<<(unsigned)grid, 256, smem, st>>>(a);
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, kRdCarveout);
+        if (k64) lc_range64_dir_kernel<true><<<(unsigned)grid, 32 * kRdWarps, smem, st>>>(a);
+        else lc_range64_dir_kernel<false><<<(unsigned)grid, 32 * kRdWarps, smem, st>>>(a);
         lc_detail::count_launch(1);
         return cuda_status();
     }
