@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) lc_bwrite_s_kernel(const SetopArgs a) {
 }
 
 // OR: every long key to its union slot
-constexpr uint32_t kWlKeys = 256;  // long keys per warp in lc_bwrite_l_kernel (8 per lane)
+constexpr uint32_t kWlKeys = 512;  // long keys per warp in lc_bwrite_l_kernel (16 per lane; A/B on the corpus OR: 256 1.10 ms, 512 1.04, 1024 1.03, 2048 1.06)
 template <bool K64>
 __global__ void __launch_bounds__(256) lc_bwrite_l_kernel(const SetopArgs a) {
     // A warp places 256 consecutive long keys.  They usually belong to one pair and share one

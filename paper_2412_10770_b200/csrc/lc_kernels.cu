@@ -78,8 +78,19 @@ struct GridCache {
 };
 GridCache g_grid;
 
-// persistent grid size for the decode kernel: SMs x resident CTAs at this smem footprint
-int persistent_grid(int kind, bool k64, uint32_t b) {
+// Persistent grid of the decode kernel for a launch over `nchunks` chunks: SMs x CTAs per SM.
+// Fewer CTAs than fit for long lists: the decode is bound by the HBM read / write mix, and that
+// mix runs faster when the offered load stays just below what HBM delivers (16-24 single-
+// buffered warps per SM) than when the memory system is over-subscribed (32 warps per SM).
+// Measured on B200 (ms per launch at 16 / 24 / 32 warps per SM = 2 / 3 / 4 CTAs): config 4
+// (sparse) 0.724 / 0.797 / 0.802 (also -9.5% / -12% at N = 5e7 / 2e8), config 2 0.200 / 0.207 /
+// 0.211, config 5 0.200 / 0.199 / 0.205, config 3 0.421 / 0.377 / 0.382 (its tail of 1-key
+// segments is paged chunk by chunk: a latency chain that needs the warps), the union's shifted
+// decode 0.368 / 0.341 / 0.353 (whole union); 12 warps per SM: 0.81 (config 4).  Short launches
+// are latency-bound and keep every CTA that fits (N = 1e7: 4 CTAs 0.030 / 0.035 ms sparse /
+// dense against 0.032 / 0.038 at 2; N = 3e7: 0.058 / 0.077 against 0.054 / 0.074 at 2 / 3).
+constexpr uint32_t kLongLaunchChunks = 24 * 1024;  // 2.5e7 keys
+int persistent_grid(int kind, bool k64, uint32_t b, uint32_t nchunks) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_grid.mu);
@@ -95,17 +106,9 @@ int persistent_grid(int kind, bool k64, uint32_t b) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
         if (occ < 1) occ = 1;
-        // Fewer resident warps than fit: the decode is bound by the HBM read / write mix, and
-        // that mix runs faster with fewer concurrent chunk streams.  Measured on B200 (ms per
-        // launch at 16 / 24 / 32 warps per SM = 2 / 3 / 4 CTAs): config 4 (sparse) 0.724 /
-        // 0.797 / 0.802 (also -9.5% / -12% at N = 5e7 / 2e8), config 2 0.200 / 0.207 / 0.211,
-        // config 5 0.200 / 0.199 / 0.205, config 3 0.421 / 0.377 / 0.382 (its tail of 1-key
-        // segments is paged chunk by chunk: a latency chain that needs the warps), the union's
-        // shifted decode 0.368 / 0.341 / 0.353 (whole union).  12 warps per SM: 0.81 (config 4).
-        const int want = kind == 1 ? 2 : 3;
-        if (occ > want) occ = want;
     }
-    return occ * g_grid.sms;
+    const int want = nchunks < kLongLaunchChunks ? occ : kind == 1 ? 2 : 3;
+    return (occ < want ? occ : want) * g_grid.sms;
 }
 
 // rho / coff non-null: lc_union's fused path (whole list, stores shifted by the insertions)
@@ -128,7 +131,7 @@ int32_t launch_decode(const lc_view* v, uint64_t i0, uint64_t i1, void* d_out, c
     const bool k64 = v->h.key_bits == 64;
     const bool sparse = v->h.n_seg * 64 < v->h.n;  // < 1 segment per 64 keys
     const int kind = coff ? 2 : sparse;
-    const int full = persistent_grid(kind, k64, b);
+    const int full = persistent_grid(kind, k64, b, a.nchunks);
     const uint32_t need = (a.nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const uint32_t grid = need < (uint32_t)full ? need : (uint32_t)full;
     void* args[] = {&a};

@@ -23,7 +23,18 @@ def main():
         lc.intersect_batch(bt, bufs=ia)
         lc.union_batch(bt, bufs=ua)
     torch.cuda.synchronize()
-    print("and", int(ia.counts.sum()), "or", int(ua.counts.sum()))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    reps = 10
+    ev[0].record()
+    for _ in range(reps):
+        lc.intersect_batch(bt, bufs=ia)
+    ev[1].record()
+    for _ in range(reps):
+        lc.union_batch(bt, bufs=ua)
+    ev[2].record()
+    torch.cuda.synchronize()
+    print("and", int(ia.counts.sum()), "or", int(ua.counts.sum()),
+          f"and_ms {ev[0].elapsed_time(ev[1]) / reps:.4f} or_ms {ev[1].elapsed_time(ev[2]) / reps:.4f}")
 
 
 if __name__ == "__main__":
