@@ -89,6 +89,7 @@ GridCache g_grid;
 // decode 0.368 / 0.341 / 0.353 (whole union); 12 warps per SM: 0.81 (config 4).  Short launches
 // are latency-bound and keep every CTA that fits (N = 1e7: 4 CTAs 0.030 / 0.035 ms sparse /
 // dense against 0.032 / 0.038 at 2; N = 3e7: 0.058 / 0.077 against 0.054 / 0.074 at 2 / 3).
+// Only 64-bit lists: see below.
 constexpr uint32_t kLongLaunchChunks = 24 * 1024;  // 2.5e7 keys
 int persistent_grid(int kind, bool k64, uint32_t b, uint32_t nchunks) {
     int dev = 0;
@@ -107,7 +108,9 @@ int persistent_grid(int kind, bool k64, uint32_t b, uint32_t nchunks) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
         if (occ < 1) occ = 1;
     }
-    const int want = nchunks < kLongLaunchChunks ? occ : kind == 1 ? 2 : 3;
+    // u32 lists move half the bytes per key: their decode is issue-bound and keeps every warp
+    // (5e7 sparse u32 keys: 0.086 / 0.076 / 0.074 ms at 2 / 3 / 4 CTAs per SM)
+    const int want = (nchunks < kLongLaunchChunks || !k64) ? occ : kind == 1 ? 2 : 3;
     return (occ < want ? occ : want) * g_grid.sms;
 }
 
