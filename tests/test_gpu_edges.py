@@ -130,3 +130,26 @@ def test_max_words_b32(lc, key_bits):
             assert torch.equal(rg[r], want(s, s + ln)), (ln, s)
     del d, words, v
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kind", ["sparse", "dense"])
+@pytest.mark.parametrize("extra", [0, 1, 777, 8 * 1024 + 5])
+def test_launch_shape_threshold(lc, kind, extra):
+    """Launches just below and above the long-launch threshold (24 K chunks: the persistent grid
+    drops to 2 / 3 CTAs per SM for u64 lists, lc_kernels.cu persistent_grid) with ragged tails:
+    every key, and the same list decoded as spans that straddle the threshold."""
+    from synth import make_keys
+    n = 24 * 1024 * 1024 - 1024 + extra
+    keys = make_keys(4 if kind == "sparse" else 2, n + 2048)
+    blob = lc.encode(keys, 31 if kind == "sparse" else 127)
+    bl = parse(blob)
+    assert (bl.L * 64 < keys.size) == (kind == "sparse")
+    v = lc.View(blob, device=DEV)
+    ref = _dev(keys)
+    out = lc.decode(v)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    for i0, i1 in ((0, n), (1024, n + 1024), (2048, keys.size), (0, 24 * 1024 * 1024 - 1)):
+        part = lc.decode_span(v, i0, i1)
+        torch.cuda.synchronize()
+        assert torch.equal(part, ref[i0:i1]), (i0, i1)
