@@ -185,8 +185,8 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
  * over len consecutive indices, the blocked decode inside and across segments
  * (K[i] = floor(f(i)) + Delta[i]; BASELINE config 5: 10^7 ranges of 64 keys).
  * A range with start + len > n yields zeros and sets bit 0 of *d_err.  1 <= len <= 2^20;
- * q == 0 is a no-op.  With an access layout attached (lc_access_layout_build), 64-key ranges
- * are decoded through it (same results). */
+ * q == 0 is a no-op.  With an access layout attached (lc_access_layout_build), ranges of up to
+ * 64 keys are decoded through it (same results). */
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
                         void* d_out, uint32_t* d_err, lc_stream stream);
 
@@ -248,8 +248,8 @@ uint64_t lc_access_layout_bytes(const lc_view* v);
  *     j's {base, slope_fx} (16 B) followed by the 16-byte units floor(s_j b / 128) ..
  *     floor(s_{j+1} b / 128) of the residual words (a copy), so params and the residual field
  *     come from one record (usually one DRAM line) instead of two sections.
- * lc_range_decode with len == 64 uses it too: the bitmaps shifted to a range's first key are the
- * segment-boundary masks of its 64 keys, and the records of consecutive segments are contiguous,
+ * lc_range_decode with len <= 64 uses it too: the bitmaps shifted to a range's first key are the
+ * segment-boundary masks of its keys, and the records of consecutive segments are contiguous,
  * so a range is one gather of <= 31 units plus its first segment's params (no search).
  * The blob (FORMAT F1-F7) is unchanged; results of lc_access / lc_quantile / lc_range_decode are
  * identical with and without the layout.  Errors: LC_ERR_ARG (null or misaligned d_layout,

@@ -395,9 +395,9 @@ __global__ void __launch_bounds__(256) lc_acc_build_kernel(const Sections sec, u
     }
 }
 
-// ------------------------------------------ range decode, len == 64, through the access layout
-// With the access layout attached a 64-key range needs no search, no starts and ONE contiguous
-// gather.  The directory bitmaps of its (at most three) 32-key groups, shifted to the range's
+// ------------------------------------------ range decode, len <= 64, through the access layout
+// With the access layout attached a range of up to 64 keys (written for the 64 of BASELINE
+// config 5) needs no search, no starts and ONE contiguous gather.  The directory bitmaps of its (at most three) 32-key groups, shifted to the range's
 // first key, ARE the window boundary masks the ring kernel votes for (PA: starts among keys
 // rk + 1 .. rk + 31, PB: among rk + 32 .. rk + 63), and the records of consecutive segments are
 // contiguous, so the range's data is the params unit of its first segment jk plus the span
@@ -448,14 +448,14 @@ __device__ __forceinline__ uint32_t sel_nz(uint32_t c, uint32_t a, uint32_t b) {
 }
 
 template <bool K64>
-__global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const RangeArgs a) {
+__global__ void __launch_bounds__(32 * kRdWarps, 5) lc_range64_dir_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t kw = K64 ? 8 : 4;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t r0 = ((uint64_t)blockIdx.x * kRdWarps + warp) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
-    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
+    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias, len = a.len;  // len <= 64
     uint8_t* ring = smem + warp * rd_smem_per_warp();
     uint4* info = (uint4*)(ring + kRdSlots * kRdSlotBytes);
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
@@ -469,14 +469,13 @@ __global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const Ran
         uint64_t A = (uint64_t)(uintptr_t)sec.acc;  // ranges without copies: lane 0 reads unit 0
         if (r0 + lane < a.q) {
             const uint64_t s64 = __ldg(a.start + r0 + lane);
-            if (s64 <= a.n && 64 <= a.n - s64) {
+            if (s64 <= a.n && len <= a.n - s64) {
                 rk = (uint32_t)s64;
-                const uint32_t e = rk + 63, g0 = rk >> 5, r5 = rk & 31;
+                const uint32_t e = rk + len - 1, g0 = rk >> 5, r5 = rk & 31;  // e: the last key
                 const uint32_t hA = ldh(sec.hint + (rk >> 10), keep);
-                const uint32_t hB = ldh(sec.hint + (e >> 10), keep);
                 const uint2 d0 = ldh(sec.dir + g0, keep);
-                const uint2 d1 = ldh(sec.dir + g0 + 1, keep);
-                const uint2 d2 = ldh(sec.dir + (e >> 5), keep);  // group g0 + 2, or g0 + 1 again
+                const uint2 d1 = ldh(sec.dir + min(g0 + 1, e >> 5), keep);
+                const uint2 d2 = ldh(sec.dir + (e >> 5), keep);  // group g0 + 2, or an earlier one again
                 const uint32_t m = d0.x & ((2u << r5) - 1);
                 jk = hA + (d0.y & 2047) + __popc(m);
                 if (m) sk = (rk & ~31u) + (31 - __clz(m));
@@ -484,20 +483,22 @@ __global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const Ran
                 else sk = ldh(sec.starts + jk, keep);  // a segment longer than 2^21 keys
                 PA = __funnelshift_r(d0.x, d1.x, r5) & ~1u;  // bit t: key rk + t starts a segment
                 PB = __funnelshift_r(d1.x, d2.x, r5);
+                // only the starts among keys rk + 1 .. rk + len - 1 count
+                PA &= len >= 32 ? kFull : (1u << len) - 1;
+                PB &= len >= 64 ? kFull : len > 32 ? (1u << (len - 32)) - 1 : 0u;
                 // a start exactly at a block's first key is not in the bitmaps (the hint names
                 // it): the block's first group has dist 0 then
                 const uint32_t tb = 1024 - (rk & 1023);
-                if (tb < 64 && ((((r5 + tb) >> 5) == 1 ? d1.y : d2.y) >> 11) == 0) {
+                if (tb < len && ((((r5 + tb) >> 5) == 1 ? d1.y : d2.y) >> 11) == 0) {
                     if (tb < 32) PA |= 1u << tb;
                     else PB |= 1u << (tb - 32);
                 }
                 const uint32_t je = jk + __popc(PA) + __popc(PB);
                 LC_CHECK(true, je, L);
-                (void)hB;
                 const uint64_t ur = ((uint64_t)rk * b) >> 7;
                 const uint32_t r0b = (rk * b) & 127;
-                // units in [A, E]: 2 (je - jk) + floor((r0b + 64 b - 1) / 128) + 1 (b = 0: 2 (je - jk))
-                const uint32_t span = 2 * (je - jk) + (uint32_t)(((int32_t)(r0b + 64 * b) - 1) >> 7) + 1;
+                // units in [A, E]: 2 (je - jk) + floor((r0b + len b - 1) / 128) + 1 (b = 0: 2 (je - jk))
+                const uint32_t span = 2 * (je - jk) + (uint32_t)(((int32_t)(r0b + len * b) - 1) >> 7) + 1;
                 if (span < kRdUnits) {
                     units = span;
                     A = (uint64_t)(uintptr_t)(sec.acc + 2 * (uint64_t)jk + 1 + ur);
@@ -546,12 +547,13 @@ __global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const Ran
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
     };
     for (uint32_t k = 0; k + 1 < kRdSlots; ++k) issue(k);
-    uint8_t* outk = (uint8_t*)a.out + ((size_t)r0 * 64 + lane) * kw;  // lane's slot, range 0
+    uint8_t* outk = (uint8_t*)a.out + ((size_t)r0 * len + lane) * kw;  // lane's slot, range 0
+    const bool liveA = lane < len, liveB = 32 + lane < len;
     const uint32_t lmask = lanemask_le();
     const uint32_t tbA = lane * b, tbB = tbA + 32 * b;  // bit offsets of the lane's two keys
     const bool pow2 = (b & (b - 1)) == 0;               // b in {0, 1, 2, 4, 8, 16, 32}
 
-    for (uint32_t k = 0; k < nr; ++k, outk += 64 * kw) {
+    for (uint32_t k = 0; k < nr; ++k, outk += (size_t)len * kw) {
         // range k's copies (and those of k + 1, k + 2) are in flight: wait for k's; the warp
         // sync also orders every lane's reads of slot k - 1 before it is refilled just below
         asm volatile("cp.async.wait_group %0;" ::"n"(kRdSlots - 2) : "memory");
@@ -571,12 +573,12 @@ __global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const Ran
             // params: slot unit 0 for jk, else 2 dj + floor((r0b + (s - rk) b) / 128)
             const uint32_t puA = sel_nz(djA, 2 * djA + ((r0b + (lane - dA) * b) >> 7), 0);
             const uint32_t puB = sel_nz(djB, 2 * djB + ((r0b + (32 + lane - dB) * b) >> 7), 0);
-            LC_CHECK(true, puB, kRdUnits);
+            LC_CHECK(liveB, puB, kRdUnits);
             const uint4 pA = lds4(slot + 16 * puA), pB = lds4(slot + 16 * puB);
             const uint32_t wbA = r0b + tbA, wbB = r0b + tbB;
             const uint32_t wA = slot + 16 + 32 * djA + ((wbA >> 3) & ~3u);
             const uint32_t wB = slot + 16 + 32 * djB + ((wbB >> 3) & ~3u);
-            LC_CHECK(true, 4 + 8 * djB + (wbB >> 5) + 1, kRdSlotBytes / 4);
+            LC_CHECK(liveB, 4 + 8 * djB + (wbB >> 5) + 1, kRdSlotBytes / 4);
             uint32_t uA, uB;
             if (pow2) {  // widths dividing 32 never straddle a word (warp-uniform)
                 uA = (lds1(wA) >> (wbA & 31)) & mask;
@@ -585,27 +587,31 @@ __global__ void __launch_bounds__(32 * kRdWarps) lc_range64_dir_kernel(const Ran
                 uA = __funnelshift_r(lds1(wA), lds1(wA + 4), wbA & 31) & mask;
                 uB = __funnelshift_r(lds1(wB), lds1(wB + 4), wbB & 31) & mask;
             }
-            put<K64>(outk, ((uint64_t)pA.y << 32) | pA.x,
-                     pred_plus(((uint64_t)pA.w << 32) | pA.z, dA, uA - bias));
-            put<K64>(outk + 32 * kw, ((uint64_t)pB.y << 32) | pB.x,
-                     pred_plus(((uint64_t)pB.w << 32) | pB.z, dB, uB - bias));
+            if (liveA)
+                put<K64>(outk, ((uint64_t)pA.y << 32) | pA.x,
+                         pred_plus(((uint64_t)pA.w << 32) | pA.z, dA, uA - bias));
+            if (liveB)
+                put<K64>(outk + 32 * kw, ((uint64_t)pB.y << 32) | pB.x,
+                         pred_plus(((uint64_t)pB.w << 32) | pB.z, dB, uB - bias));
         } else if (lds1(info_s + 48 * k + 24) & kRdInvalid) {
-            put<K64>(outk, 0, 0);
-            put<K64>(outk + 32 * kw, 0, 0);
-        } else {  // two 32-key windows through L2
+            if (liveA) put<K64>(outk, 0, 0);
+            if (liveB) put<K64>(outk + 32 * kw, 0, 0);
+        } else {  // 32-key windows through L2
             const uint4 q2 = info[3 * k + 2];
             uint32_t jb = q2.x, sbw = q2.y;
-            for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
+            for (uint32_t w0 = 0; w0 < len; w0 += 32) {
                 const uint32_t wb = rk + w0;
                 const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
                 const uint32_t Pm = __reduce_or_sync(kFull, bit_or_zero(xw));
                 const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
                 const uint32_t m = Pm & lmask;
                 const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
-                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
-                const uint32_t u =
-                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
-                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
+                if (w0 + lane < len) {
+                    const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
+                    const uint32_t u =
+                        b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                    put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
+                }
                 jb += adv;
                 sbw = ldh(sec.starts + min(jb, L), keep);
             }

@@ -448,7 +448,7 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (grid > 0x7fffffffULL) return LC_ERR_ARG;
     const bool k64 = v->h.key_bits == 64;
     cudaStream_t st = (cudaStream_t)stream;
-    if (len == 64 && v->d_acc) {  // access layout attached: no search, one contiguous gather
+    if (len <= 64 && v->d_acc) {  // access layout attached: no search, one contiguous gather
         const uint32_t smem = kRdWarps * rd_smem_per_warp();
         const uint64_t grid = (q + 32 * kRdWarps - 1) / (32 * kRdWarps);
         const void* fn = k64 ? (const void*)lc_range64_dir_kernel<true>

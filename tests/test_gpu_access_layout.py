@@ -101,7 +101,7 @@ def _check_blob(lc, blob, keys, rng, m=20_000, layout_bytes=True):
     bad = np.array([n, n + 5, 1 << 40], np.uint64)  # out of range: 0 and the error bit
     ab = lc.access(v, _dev(bad), err=err)
     rgs = {}
-    for ln in (1, 33, 64, 100):  # range decodes with the layout attached (64 keys: lc_range64_dir_kernel)
+    for ln in (1, 2, 31, 32, 33, 63, 64, 100):  # with the layout attached, len <= 64: lc_range64_dir_kernel
         if n >= ln:
             st = rng.integers(0, n - ln, 700, endpoint=True).astype(np.uint64)
             rgs[ln] = (st, lc.range_decode(v, _dev(st), ln))
