@@ -185,8 +185,9 @@ int32_t lc_access(const lc_view* v, const uint64_t* d_idx, uint64_t q, void* d_o
  * over len consecutive indices, the blocked decode inside and across segments
  * (K[i] = floor(f(i)) + Delta[i]; BASELINE config 5: 10^7 ranges of 64 keys).
  * A range with start + len > n yields zeros and sets bit 0 of *d_err.  1 <= len <= 2^20;
- * q == 0 is a no-op.  With an access layout attached (lc_access_layout_build), ranges of up to
- * 64 keys are decoded through it (same results). */
+ * q == 0 is a no-op.  Ranges of up to 64 keys run a staged kernel (a shared-memory ring of the
+ * ranges' slices); with an access layout attached (lc_access_layout_build) they are decoded
+ * through it (same results). */
 int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, uint32_t len,
                         void* d_out, uint32_t* d_err, lc_stream stream);
 

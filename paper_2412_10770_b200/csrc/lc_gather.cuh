@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const RangeArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- range decode, len == 64
+// ---------------------------------------------------------------- range decode, len <= 64
 // cp.async (LDGSTS) 16-byte copy with zero fill when `valid` is false
 __device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -166,7 +166,8 @@ __host__ __device__ constexpr uint32_t r64_bytes(uint32_t b) {  // per slot: par
     return 16 * kR64Segs + 16 * kR64StartGroups + 4 * r64_words(b);
 }
 
-// 64-key ranges (BASELINE config 5).  Phase 1: lane r binary-searches range r's first segment
+// Ranges of up to 64 keys (written for the 64 of BASELINE config 5; shorter ones mask the
+// tail).  Phase 1: lane r binary-searches range r's first segment
 // (32 independent searches) and parks {start, segment, segment start, first word} in shared
 // memory.  Phase 2: the warp walks its 32 ranges through a 4-slot shared-memory ring: lane g
 // gathers 16-byte group g of range k+3's slot (params[j..j+8), starts[j+1..j+9), residual
@@ -181,7 +182,8 @@ __host__ __device__ constexpr uint32_t r64_smem_per_warp(uint32_t b) {
     return kR64Slots * r64_bytes(b) + kR64Info;
 }
 
-template <bool K64>
+// FULL: len == 64 (no tail predicates, the tuned config-5 kernel); otherwise len < 64.
+template <bool K64, bool FULL>
 __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t kw = K64 ? 8 : 4;
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
     const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
+    const uint32_t len = FULL ? 64 : a.len;  // len <= 64
     const uint32_t RB = r64_bytes(b), nw16 = r64_words(b) / 4;
     uint8_t* wbase = smem + warp * r64_smem_per_warp(b);
     uint4* info = (uint4*)(wbase + kR64Slots * RB);
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         uint32_t rs = 0, j = kFull, sj = 0;
         if (r0 + lane < a.q) {
             const uint64_t s64 = __ldg(a.start + r0 + lane);
-            if (s64 <= a.n && 64 <= a.n - s64) {
+            if (s64 <= a.n && len <= a.n - s64) {
                 rs = (uint32_t)s64;
                 j = seg_search(sec, rs, keep);
                 sj = ldh(sec.starts + j, keep);
@@ -242,7 +245,10 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         asm volatile("cp.async.commit_group;" ::: "memory");  // one group per range (maybe empty)
     };
     for (uint32_t k = 0; k + 1 < kR64Slots; ++k) issue(k);
-    uint8_t* const out0 = (uint8_t*)a.out + ((size_t)r0 * 64 + lane) * kw;  // lane's slot, range 0
+    uint8_t* const out0 = (uint8_t*)a.out + ((size_t)r0 * len + lane) * kw;  // lane's slot, range 0
+    // ranges shorter than 64 keys: the slot still stages the slices of 64 keys (zero-filled past
+    // the sections), the tail is not stored
+    const bool liveA = FULL || lane < len, liveB = FULL || 32 + lane < len;
 
     for (uint32_t k = 0; k < nr; ++k) {
         issue(k + kR64Slots - 1);
@@ -250,10 +256,10 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
         __syncwarp();
         const uint4 ri = info[k];
         const uint32_t rk = ri.x, jk = ri.y, sb = ri.z;
-        uint8_t* outk = out0 + (size_t)k * 64 * kw;
+        uint8_t* outk = out0 + (size_t)k * len * kw;
         if (jk == kFull) {
-            put<K64>(outk, 0, 0);
-            put<K64>(outk + 32 * kw, 0, 0);
+            if (liveA) put<K64>(outk, 0, 0);
+            if (liveB) put<K64>(outk + 32 * kw, 0, 0);
             __syncwarp();
             continue;
         }
@@ -278,25 +284,27 @@ __global__ void __launch_bounds__(256) lc_range64_kernel(const RangeArgs a) {
                 // bit offset inside the staged words; exact mod 2^32 (the true value is small)
                 const uint32_t bA = (rk + lane) * b - (ri.w << 5);
                 const uint32_t bB = bA + 32 * b;
-                LC_CHECK(true, (bB >> 5) + 1, r64_words(b));
+                LC_CHECK(liveB, (bB >> 5) + 1, r64_words(b));
                 uA = __funnelshift_r(Wd[bA >> 5], Wd[(bA >> 5) + 1], bA & 31) & mask;
                 uB = __funnelshift_r(Wd[bB >> 5], Wd[(bB >> 5) + 1], bB & 31) & mask;
             }
-            put<K64>(outk, pA.x, pred_plus(pA.y, dA, uA - bias));
-            put<K64>(outk + 32 * kw, pB.x, pred_plus(pB.y, dB, uB - bias));
-        } else {  // dense range: two 32-key windows through L2
+            if (liveA) put<K64>(outk, pA.x, pred_plus(pA.y, dA, uA - bias));
+            if (liveB) put<K64>(outk + 32 * kw, pB.x, pred_plus(pB.y, dB, uB - bias));
+        } else {  // dense range: 32-key windows through L2
             uint32_t jb = jk, sbw = sb;
-            for (uint32_t w0 = 0; w0 < 64; w0 += 32) {
+            for (uint32_t w0 = 0; w0 < len; w0 += 32) {
                 const uint32_t wb = rk + w0;
                 const uint32_t xw = ldh(sec.starts + min(jb + 1 + lane, L), keep) - wb;
                 const uint32_t Pm = __reduce_or_sync(kFull, bit_or_zero(xw));
                 const uint32_t adv = __popc(__ballot_sync(kFull, xw <= 32));
                 const uint32_t m = Pm & lmask;
                 const uint32_t d = m ? lane - (31 - __clz(m)) : wb - sbw + lane;
-                const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
-                const uint32_t u =
-                    b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
-                put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
+                if (w0 + lane < len) {
+                    const ulonglong2 pr = ldh(sec.params + LC_BOUND(true, jb + __popc(m), L), once);
+                    const uint32_t u =
+                        b ? field_of(field_words(sec, wb + lane, b, once), wb + lane, b, mask) : 0;
+                    put<K64>(outk + w0 * kw, pr.x, pred_plus(pr.y, d, u - bias));
+                }
                 jb += adv;
                 sbw = ldh(sec.starts + min(jb, L), keep);
             }

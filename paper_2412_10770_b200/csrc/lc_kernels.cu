@@ -460,12 +460,16 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
         lc_detail::count_launch(1);
         return cuda_status();
     }
-    if (len == 64) {  // the config-5 shape: cp.async ring kernel
+    if (len <= 64) {  // the config-5 shape (and shorter): cp.async ring kernel
         const uint32_t smem = 8 * r64_smem_per_warp(a.b);
-        const void* fn = k64 ? (const void*)lc_range64_kernel<true> : (const void*)lc_range64_kernel<false>;
+        const void* fn = len == 64 ? (k64 ? (const void*)lc_range64_kernel<true, true>
+                                          : (const void*)lc_range64_kernel<false, true>)
+                                   : (k64 ? (const void*)lc_range64_kernel<true, false>
+                                          : (const void*)lc_range64_kernel<false, false>);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (k64) lc_range64_kernel<true><<<(unsigned)grid, 256, smem, st>>>(a);
-        else lc_range64_kernel<false><<<(unsigned)grid, 256, smem, st>>>(a);
+        void* args[] = {&a};
+        if (cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st) != cudaSuccess)
+            return LC_ERR_CUDA;
         lc_detail::count_launch(1);
         return cuda_status();
     }
