@@ -455,7 +455,8 @@ __device__ __forceinline__ uint32_t sel_nz(uint32_t c, uint32_t a, uint32_t b) {
     return r;
 }
 
-template <bool K64>
+// FULL: len == 64 (no tail masks: the tuned config-5 kernel); otherwise len < 64.
+template <bool K64, bool FULL>
 __global__ void __launch_bounds__(32 * kRdWarps, 5) lc_range64_dir_kernel(const RangeArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t kw = K64 ? 8 : 4;
@@ -463,7 +464,8 @@ __global__ void __launch_bounds__(32 * kRdWarps, 5) lc_range64_dir_kernel(const 
     const uint64_t r0 = ((uint64_t)blockIdx.x * kRdWarps + warp) * 32;
     if (r0 >= a.q) return;  // warp-uniform
     const Sections sec = a.sec;
-    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias, len = a.len;  // len <= 64
+    const uint32_t b = a.b, mask = a.mask, L = a.L, bias = a.bias;
+    const uint32_t len = FULL ? 64 : a.len;  // len <= 64
     uint8_t* ring = smem + warp * rd_smem_per_warp();
     uint4* info = (uint4*)(ring + kRdSlots * kRdSlotBytes);
     const uint64_t keep = policy_evict_last(), once = policy_evict_first();
@@ -492,8 +494,10 @@ __global__ void __launch_bounds__(32 * kRdWarps, 5) lc_range64_dir_kernel(const 
                 PA = __funnelshift_r(d0.x, d1.x, r5) & ~1u;  // bit t: key rk + t starts a segment
                 PB = __funnelshift_r(d1.x, d2.x, r5);
                 // only the starts among keys rk + 1 .. rk + len - 1 count
-                PA &= len >= 32 ? kFull : (1u << len) - 1;
-                PB &= len >= 64 ? kFull : len > 32 ? (1u << (len - 32)) - 1 : 0u;
+                if (!FULL) {
+                    PA &= len >= 32 ? kFull : (1u << len) - 1;
+                    PB &= len > 32 ? (1u << (len - 32)) - 1 : 0u;
+                }
                 // a start exactly at a block's first key is not in the bitmaps (the hint names
                 // it): the block's first group has dist 0 then
                 const uint32_t tb = 1024 - (rk & 1023);
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(32 * kRdWarps, 5) lc_range64_dir_kernel(const 
     };
     for (uint32_t k = 0; k + 1 < kRdSlots; ++k) issue(k);
     uint8_t* outk = (uint8_t*)a.out + ((size_t)r0 * len + lane) * kw;  // lane's slot, range 0
-    const bool liveA = lane < len, liveB = 32 + lane < len;
+    const bool liveA = FULL || lane < len, liveB = FULL || 32 + lane < len;
     const uint32_t lmask = lanemask_le();
     const uint32_t tbA = lane * b, tbB = tbA + 32 * b;  // bit offsets of the lane's two keys
     const bool pow2 = (b & (b - 1)) == 0;               // b in {0, 1, 2, 4, 8, 16, 32}

@@ -451,12 +451,15 @@ int32_t lc_range_decode(const lc_view* v, const uint64_t* d_start, uint64_t q, u
     if (len <= 64 && v->d_acc) {  // access layout attached: no search, one contiguous gather
         const uint32_t smem = kRdWarps * rd_smem_per_warp();
         const uint64_t grid = (q + 32 * kRdWarps - 1) / (32 * kRdWarps);
-        const void* fn = k64 ? (const void*)lc_range64_dir_kernel<true>
-                             : (const void*)lc_range64_dir_kernel<false>;
+        const void* fn = len == 64 ? (k64 ? (const void*)lc_range64_dir_kernel<true, true>
+                                          : (const void*)lc_range64_dir_kernel<false, true>)
+                                   : (k64 ? (const void*)lc_range64_dir_kernel<true, false>
+                                          : (const void*)lc_range64_dir_kernel<false, false>);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, kRdCarveout);
-        if (k64) lc_range64_dir_kernel<true><<<(unsigned)grid, 32 * kRdWarps, smem, st>>>(a);
-        else lc_range64_dir_kernel<false><<<(unsigned)grid, 32 * kRdWarps, smem, st>>>(a);
+        void* args[] = {&a};
+        if (cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(32 * kRdWarps), args, smem, st) != cudaSuccess)
+            return LC_ERR_CUDA;
         lc_detail::count_launch(1);
         return cuda_status();
     }
